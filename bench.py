@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the logits -> PPO-loss path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama8b] [--impl ours|reference]
+
+One step = one PPO iteration of the whole hot path on every rank (S1 old,
+S1+S2+S3 ref, S4 advantages, S6 + collective C1, S1+S7..S9 actor, S10 +
+collective C2) over a resident synthetic rollout of the named BASELINE.json
+configuration (default configs[1], "llama8b": B=128, T=1024, V=128256 bf16).
+N > 1 is launched by torchrun (one process per GPU); per-GPU work is fixed
+(weak scaling: each rank holds its own B-sequence shard of a B*N batch).
+
+Prints ONE JSON line on rank 0 (see DESIGN.md section 7 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "tokens/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _workload_desc(name, c, B, world):
+    return (f"{name}: B={B}/rank T={c['T']} V={c['V']} {c['dtype']} logits x3 models resident in HBM, "
+            f"adv={c['adv_kind']} gamma={c['gamma']} lambda={c['lam']} whiten={c['whiten']} "
+            f"eps=({c['eps_low']},{c['eps_high']}) eps_v={c['eps_v']} kl={c.get('kl_mode', 'reward')}, "
+            f"micro-batch {c['mb']} seq, all L_b = T")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) leg
+def _oracle_sample(logits_fn, batch_np, c, n_seq, cores):
+    """Time the fp64 oracle on the first n_seq sequences: S1 for the three models
+    (rows split over `cores` threads; ctypes releases the GIL), then the rest of
+    the pipeline.  Returns (tokens, seconds)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+
+    sh = {k: v[:n_seq] for k, v in batch_np.items()}
+    T = sh["tokens"].shape[1]
+    t0 = time.perf_counter()
+    for role in ("old", "ref", "new"):
+        x = logits_fn(role, n_seq)                       # host [n_seq, T, V]
+        flat = x.reshape(n_seq * T, 1, x.shape[-1])
+        tok = sh["tokens"].reshape(-1, 1)
+        ones = np.minimum(np.arange(T)[None, :] < sh["lengths"][:, None], 1).astype(np.int32).reshape(-1)
+        parts = np.array_split(np.arange(n_seq * T), cores)
+
+        def work(idx):
+            if idx.size == 0:
+                return idx, None
+            return idx, oracle.logprobs(flat[idx[0]:idx[-1] + 1], tok[idx[0]:idx[-1] + 1], ones[idx[0]:idx[-1] + 1])
+
+        lp = np.zeros(n_seq * T)
+        ent = np.zeros(n_seq * T)
+        with ThreadPoolExecutor(cores) as ex:
+            for idx, o in ex.map(work, parts):
+                if o is not None:
+                    lp[idx] = o["logp"][:, 0]
+                    ent[idx] = o["entropy"][:, 0]
+        sh[f"logp_{role}"] = lp.reshape(n_seq, T)
+        if role == "new":
+            sh["entropy_new"] = ent.reshape(n_seq, T)
+    oracle.pipeline([sh], c)
+    dt = time.perf_counter() - t0
+    return int(np.minimum(sh["lengths"], T).sum()), dt
+
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle on the host cores, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2405_11143_b200 import synth
+
+    c = dict(synth.CONFIGS[args.config])
+    n_seq = args.ref_seqs
+    T, V = c["T"], c["V"]
+    cores = len(os.sched_getaffinity(0))
+    dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
+    batch = synth.make_batch(1234, n_seq, T, V, c["dtype"], "realistic", "full", c["rewards"], c["group_size"],
+                             device=dev)
+    bnp = synth.batch_to_numpy(batch)
+    fn = lambda role, n: bnp[f"logits_{role}"][:n]  # noqa: E731
+    times, toks = [], 0
+    for i in range(args.warmup + args.steps):
+        toks, dt = _oracle_sample(fn, {k: v for k, v in bnp.items() if not k.startswith("logits_")}, c, n_seq, cores)
+        if i >= args.warmup:
+            times.append(dt)
+    mean = sum(times) / len(times)
+    val = toks / mean
+    sample = f"first {n_seq} sequences x {T} tokens of {args.config} (3 x {n_seq * T} vocab rows), per step"
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload_desc(args.config, c, n_seq, 1) + " (oracle sample)",
+                       "global_batch": n_seq, "seq_len": T, "parallelism": "host threads"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch.distributed as dist
+
+    from paper_2405_11143_b200 import orl, synth
+    from paper_2405_11143_b200.pipeline import Buffers, PathConfig, run_iteration
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        uid = [orl.orl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = orl.Context(local, world, rank, uid[0])
+    else:
+        ctx = orl.Context(local)
+
+    c = dict(synth.CONFIGS[args.config])
+    B, T, V, mb = c["B"], c["T"], c["V"], c["mb"]
+    if args.batch:
+        B = args.batch
+    cfg = PathConfig.from_synth(c)
+    seed = 1234 + rank
+    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    elt = 2 if tdt == torch.bfloat16 else 4
+
+    # ---- resident synthetic rollout (generated up front; not timed) ----------
+    L = synth.lengths_for(B, T, seed, "full").to(dev)
+    tok = synth.tokens_for(B, T, V, seed).to(dev)
+    R = synth.rewards_for(B, seed, c["rewards"], c["group_size"]).to(dev)
+    v_old, v_new = (v.to(dev) for v in synth.values_for(B, T, seed))
+    logits = {r: torch.empty(B, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
+    for s in range(0, B, mb):
+        e = min(B, s + mb)
+        synth.fill_logits_(tuple(logits[r][s:e] for r in synth.ROLES), tok[s:e], seed, s // mb, "realistic")
+    batch = dict(tokens=tok, lengths=L, seq_reward=R, values_old=v_old, values_new=v_new)
+    bufs = Buffers(B, T, dev, c["group_size"])
+    stream = torch.cuda.current_stream()
+    src = lambda role, s, e: logits[role][s:e]  # noqa: E731
+    n_tok_rank = int(L.clamp(max=T).sum().item())
+
+    # per-K1-launch event timing on the launching stream
+    events = []
+
+    def hook(tag):
+        a = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+
+        def done():
+            b = torch.cuda.Event(enable_timing=True)
+            b.record(stream)
+            events.append((tag, a, b))
+        return done
+
+    def step(timing):
+        return run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream, on_k1=hook if timing else None)
+
+    for _ in range(args.warmup):
+        status, st = step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launch_count
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        status, st = step(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = (ctx.launch_count - l0) // args.steps
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    total_tokens = n_tok_rank * world
+    value = total_tokens / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (K1) --------------------------------
+    side = {"old": 8, "ref": 8 + 12, "new": 8 + 24 + 16}   # side bytes per token (DESIGN 5.1)
+    k1_ms = sum(a.elapsed_time(b) for _, a, b in events)
+    k1_bytes = 0
+    for tag, _, _ in events:
+        k1_bytes += (mb * T) * (V * elt + side[tag])
+    k1_bytes = k1_bytes * (n_tok_rank / (B * T))           # only valid rows are read
+    n_k1 = len(events)
+    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
+    peak, peak_src = _peaks()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("V") == V and pj.get("T") == T and pj.get("mb") == mb:
+                traffic = pj["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": "k1_tma_kernel (S1 + epilogues)", "launches_per_step": n_k1 // args.steps,
+            "algorithmic_bytes_per_launch": int(k1_bytes / max(n_k1, 1)), "k1_share_of_step": round(k1_ms / (ms * args.steps), 4),
+            "peak_source": peak_src}
+
+    # ---- e2e: host buffers, H2D/D2H inside the timed region --------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank)
+
+    # ---- oracle on the host cores (rank 0, N = 1 only) ------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_seq = args.ref_seqs
+        cores = len(os.sched_getaffinity(0))
+        bnp = {k: v[:n_seq].detach().cpu().numpy() for k, v in batch.items()}
+        host_logits = {r: synth.to_numpy_logits(logits[r][:n_seq]) for r in synth.ROLES}
+        toks, dt = _oracle_sample(lambda role, n: host_logits[role][:n], bnp, c, n_seq, cores)
+        cpu = {"value": toks / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {n_seq} sequences x {T} tokens of the same rollout (3 x {n_seq * T} vocab rows), "
+                         f"{dt:.1f} s wall"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
+                "config": {"workload": _workload_desc(args.config, c, B, world), "global_batch": B * world,
+                           "seq_len": T, "vocab": V, "parallelism": f"dp{world}",
+                           "l2": "inputs larger than L2 (3 x %.1f GB logits per rank vs 126 MB L2)" % (B * T * V * elt / 1e9)},
+                "status": status, "stats": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in st.items()},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
+                "per_gpu_tokens_per_s": round(value / world, 1)}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank):
+    """Same iteration through the public API with the step's inputs in pinned
+    HOST memory: every step copies each micro-batch's three logits blocks plus
+    the per-token inputs host->device (double-buffered on a copy stream) and
+    orl_finalize reads the stats back (D2H) and synchronises.  The pinned pool
+    holds one micro-batch per role and is re-sent for every micro-batch, so the
+    bytes moved per step are the full step's."""
+    import torch.distributed as dist
+
+    from paper_2405_11143_b200.pipeline import run_iteration
+
+    B = batch["tokens"].shape[0]
+    host = {r: logits[r][:mb].cpu().pin_memory() for r in logits}
+    small = {k: v.cpu().pin_memory() for k, v in batch.items()}
+    stage = [{r: torch.empty_like(logits[r][:mb]) for r in logits} for _ in range(2)]
+    dbatch = {k: torch.empty_like(v) for k, v in batch.items()}
+    comp, copy = torch.cuda.current_stream(), torch.cuda.Stream()
+    order = [(r, s) for r in ("old", "ref", "new") for s in range(0, B, mb)]
+    h2d = sum(v.numel() * v.element_size() for v in small.values())
+    h2d += sum((min(B, s + mb) - s) * host[r][0].numel() * host[r].element_size() for r, s in order)
+    d2h = 16 * 8 + 4 * 8
+
+    def one_step():
+        for k, v in small.items():
+            dbatch[k].copy_(v, non_blocking=True)
+        slot_free = [None, None]
+        pending = {}
+        counter = {"i": 0}
+
+        def fetch(i):
+            r, s = order[i]
+            e = min(B, s + mb)
+            with torch.cuda.stream(copy):
+                if slot_free[i % 2] is not None:
+                    copy.wait_event(slot_free[i % 2])
+                stage[i % 2][r][: e - s].copy_(host[r][: e - s], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            pending[i] = ev
+
+        def src(role, s, e):
+            i = counter["i"]
+            counter["i"] += 1
+            comp.wait_event(pending.pop(i))
+            if i + 1 < len(order):
+                fetch(i + 1)
+            return stage[i % 2][role][: e - s]
+
+        def hook(tag):
+            def after():
+                i = counter["i"] - 1
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                slot_free[i % 2] = ev          # slot i%2 may be refilled after this K1
+            return after
+
+        fetch(0)
+        return run_iteration(ctx, dbatch, cfg, bufs, src, mb, stream=comp, on_k1=hook)
+
+    steps = max(2, args.steps // 5)
+    one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    del stage, host
+    return {"value": round(total_tokens / dt, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": d2h, "steps": steps,
+            "note": "logits streamed from pinned host memory over PCIe each step (double-buffered); host clock"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama8b")
+    ap.add_argument("--batch", type=int, default=0, help="override B per rank (testing)")
+    ap.add_argument("--ref-seqs", type=int, default=4, help="oracle sample size (sequences)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,297 @@
+/*
+ * orl.h -- C ABI of liborl.so: the B200 (sm_100a) hot path that turns rollout
+ * logits into PPO / GRPO / REINFORCE++ training signal, after the PPO workflow
+ * of OpenRLHF (arXiv 2405.11143), Appendix C, lines 189-201.
+ *
+ * Citation key: P:n = PAPER.md line n, S:n = SPEC.md line n (the CPU spec
+ * written from the paper; used here for interfaces and error semantics),
+ * Z-numbers = the readings listed in DESIGN.md section 3.
+ *
+ * One iteration on one rank (one process per GPU), in this order:
+ *
+ *   orl_begin_iteration                          reset accumulators/counters
+ *   for each micro-batch: orl_logprobs(old)      S1
+ *   for each micro-batch: orl_logprobs(ref,      S1+S2+S3
+ *                               partner = old logp)
+ *   orl_advantages                               S4 / S4' / S5
+ *   orl_whiten_stats                             S6 + collective C1
+ *   for each micro-batch: orl_ppo_loss           S1+S7+S8+S9
+ *   orl_finalize                                 S10 + collective C2
+ *
+ * Conventions shared by every call
+ *  - Pointers are DEVICE pointers on the context's device unless a comment
+ *    says "host".  The caller owns every buffer; the library never frees or
+ *    retains a caller pointer after a call returns.
+ *  - Every call is asynchronous and stream-ordered on `stream` (a
+ *    cudaStream_t passed as void*; NULL = legacy default stream), except
+ *    orl_finalize, which synchronises `stream` before returning.
+ *  - Per-token arrays are row-major [B_total, T] over the RANK-LOCAL batch of
+ *    B_total responses, 4-byte aligned (ORL_E_ALIGN otherwise).  Position
+ *    (b,t) is valid iff t < lengths[b] (right-padded prefix mask, Z10).
+ *    Outputs at masked positions are written as exactly 0.0f; inputs there
+ *    (logits included) are never read.  lengths[b] == 0 is allowed.
+ *  - A micro-batch is the sequence range [seq_offset, seq_offset + B) of the
+ *    rank-local batch; its logits are addressed relative to sequence
+ *    seq_offset (see orl_logits).
+ *  - Argument errors are detected on the host before any launch and return a
+ *    status without side effects.  Data errors found on the device (token out
+ *    of range, non-finite values, ratio guard) never abort a launch: the
+ *    offending token's outputs become NaN and a device counter is
+ *    incremented; orl_finalize reports them.
+ *  - Not thread-safe per context: one context per device per host thread.
+ */
+#ifndef ORL_H
+#define ORL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORL_VERSION 1
+#define ORL_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
+#define ORL_STATS_N 16          /* length of the device stats vector */
+#define ORL_MAX_SEQ_PER_CALL 8192
+
+typedef enum {
+    ORL_OK = 0,
+    ORL_E_INVALID_ARG = 1,   /* NULL required pointer, bad enum, bad scalar    */
+    ORL_E_SHAPE = 2,         /* non-positive/oversized dims, stride < V        */
+    ORL_E_ALIGN = 3,         /* per-token array not 4-byte aligned             */
+    ORL_E_DTYPE = 4,         /* unknown logits dtype                           */
+    ORL_E_TOKEN_RANGE = 5,   /* some valid token outside [0, V)       */
+    ORL_E_MASK = 6,          /* lengths[b] < 0 or > T                          */
+    ORL_E_NONFINITE = 7,     /* non-finite logits / loss terms    (Z26)        */
+    ORL_E_NUMERIC_GUARD = 8, /* |logp_new - logp_old| > guard     (Z22) */
+    ORL_E_EMPTY_BATCH = 9,   /* no valid token on any rank                     */
+    ORL_E_GROUP_SPLIT = 10,  /* GRPO batch not a whole number of groups        */
+    ORL_E_CUDA = 11,         /* CUDA runtime error (see orl_last_error)        */
+    ORL_E_NCCL = 12,         /* NCCL error (see orl_last_error)                */
+    ORL_E_STATE = 13         /* calls out of order (e.g. loss before whitening)*/
+} orl_status;
+
+typedef enum { ORL_BF16 = 0, ORL_F32 = 1 } orl_dtype;
+
+/* KL estimators with d = logp - logp_ref (Z6):
+ * k1 = d, k2 = d^2/2, k3 = exp(-d) - 1 + d. */
+typedef enum { ORL_KL_K1 = 1, ORL_KL_K2 = 2, ORL_KL_K3 = 3 } orl_kl;
+
+/* Advantage estimators.
+ *  GAE          P:195  delta_t = r'_t + gamma V_{t+1} - V_t,
+ *                      A_t = sum_l (gamma lambda)^l delta_{t+l}, R_t = A_t + V_t
+ *  GRPO         P:102 (name): A_b = (R_b - mu_g)/(sigma_g + 1e-8)
+ *  RPP          REINFORCE++ (north star, Z23): A_t = sum_{s>=t} gamma^{s-t} r'_s
+ *  RPP_BASELINE RPP after R_b <- R_b - mu_g (group mean)                     */
+typedef enum {
+    ORL_ADV_GAE = 0,
+    ORL_ADV_GRPO = 1,
+    ORL_ADV_RPP = 2,
+    ORL_ADV_RPP_BASELINE = 3
+} orl_adv;
+
+typedef struct orl_ctx orl_ctx; /* opaque */
+
+/* A [B,T,V] logits view.  Row (b,t) of the micro-batch starts at element
+ * b*stride_b + t*stride_t of `ptr` (b relative to the micro-batch), with
+ * unit stride along V.  Response-aligned (Z1): row (b,t) is the distribution
+ * token tokens[b,t] was sampled from; pass a view offset by prompt_len-1 to
+ * use a model's full-sequence logits.  Requires stride_t >= V and
+ * stride_b >= 0 (ORL_E_SHAPE).  When the base address and both byte pitches
+ * are 16-byte aligned and V*elt is a multiple of 16, rows are streamed by the
+ * TMA bulk-copy kernel; otherwise a generic (non-TMA) kernel runs. */
+typedef struct {
+    const void *ptr;
+    int32_t dtype; /* orl_dtype */
+    int32_t pad_;
+    int64_t V;
+    int64_t stride_b; /* elements */
+    int64_t stride_t; /* elements */
+} orl_logits;
+
+/* The response rows of one micro-batch. */
+typedef struct {
+    int64_t B;              /* sequences in this call, 1..ORL_MAX_SEQ_PER_CALL */
+    int64_t T;              /* max response length; pitch of per-token arrays */
+    int64_t seq_offset;     /* first sequence of the call in the rank batch   */
+    const int32_t *tokens;  /* [B_total, T] sampled token ids y_{b,t}         */
+    const int32_t *lengths; /* [B_total] response lengths L_b, 0 <= L_b <= T  */
+} orl_rows;
+
+/* PPO loss configuration. */
+typedef struct {
+    double eps_low;     /* clip(rho, 1-eps_low, 1+eps_high); DAPO decoupled */
+    double eps_high;    /*   clip when eps_low != eps_high (Z15)      */
+    double eps_value;   /* value clip half-width; <= 0: plain (V-R)^2 (Z13) */
+    double c1;          /* value-loss coefficient                           */
+    double c2;          /* entropy-bonus coefficient                        */
+    double beta_loss;   /* KL-in-loss coefficient ("k2 as the loss")   */
+    int32_t kl_loss_est;/* orl_kl used for the loss term and the kl stat    */
+    int32_t kl_in_loss; /* 1: total += beta_loss * mean k(new, ref)  (Z5)   */
+    double ratio_guard; /* |logp_new - logp_old| > guard counts (Z22); 30   */
+} orl_ppo_cfg;
+
+/* Host-side statistics.  Means are over the N valid tokens of
+ * ALL ranks (Z11).  total_loss = policy_loss + c1 value_loss - c2 entropy
+ * + [kl_in_loss] beta_loss kl (Z12). */
+typedef struct {
+    double n_tokens;
+    double policy_loss;     /* -mean min(rho A', clip(rho) A')                 */
+    double value_loss;      /* mean of the (clipped) squared error, no 1/2     */
+    double entropy;         /* mean full-vocabulary entropy (nats)             */
+    double kl;              /* mean k(logp_new - logp_ref), loss estimator     */
+    double approx_kl_old;   /* mean k3(logp_old - logp_new) (Z27)              */
+    double clip_frac;       /* share of tokens whose clipped branch is active  */
+    double value_clip_frac; /* share whose clipped value branch strictly wins  */
+    double ratio_mean;      /* mean rho                                        */
+    double total_loss;
+    double adv_mean;        /* global whitening moments (0 when not whitened)  */
+    double adv_std;
+    int64_t n_guard;
+    int64_t n_nonfinite;
+    int64_t n_token_range;
+    int32_t whiten_warn;    /* whitening requested with < 2 tokens     */
+    int32_t pad_;
+} orl_stats;
+/* The device stats vector (double[ORL_STATS_N]) holds, in order: n_tokens,
+ * policy_loss, value_loss, entropy, kl, approx_kl_old, clip_frac,
+ * value_clip_frac, ratio_mean, total_loss, adv_mean, adv_std, n_guard,
+ * n_nonfinite, n_token_range, whiten_warn. */
+
+/* ---- context ----------------------------------------------------------- */
+
+/* Library version (ORL_VERSION). */
+int orl_version(void);
+
+/* Host.  Rank 0 creates an NCCL unique id (ORL_UNIQUE_ID_BYTES bytes into
+ * `id_out`) and broadcasts it to the other ranks (e.g. torch.distributed). */
+orl_status orl_get_unique_id(unsigned char *id_out);
+
+/* Create a context on CUDA `device` for rank `rank` of `world` ranks.
+ * world == 1: no communicator, `id` may be NULL.  world > 1: `id` (host,
+ * ORL_UNIQUE_ID_BYTES) from orl_get_unique_id; collective (all ranks must
+ * call).  The context owns the NCCL communicator, fp64 partial buffers,
+ * device error counters and a pinned host stats slot. */
+orl_status orl_create(int device, int world, int rank, const unsigned char *id, orl_ctx **out);
+
+/* Destroy a context (synchronises its device first).  NULL is a no-op. */
+orl_status orl_destroy(orl_ctx *ctx);
+
+/* Human-readable text of the last error on `ctx` (or of the calling thread
+ * when ctx is NULL).  Valid until the next call on the same ctx/thread. */
+const char *orl_last_error(const orl_ctx *ctx);
+
+/* Number of kernels the context has launched so far (for bench accounting). */
+uint64_t orl_launch_count(const orl_ctx *ctx);
+
+/* Start an iteration: zero the loss accumulators, error counters and
+ * advantage partials on `stream`. */
+orl_status orl_begin_iteration(orl_ctx *ctx, void *stream);
+
+/* ---- S1 (+S2+S3): log-softmax, gather, entropy ------------------------- */
+
+/* For each valid (b,t) of the micro-batch, with x = inv_temp * logits[b,t,:]
+ * (Z2):  lse = log sum_v exp(x_v)
+ *        logp = x_y - lse,  y = tokens[b,t]
+ *        entropy = -sum_v p_v log p_v  (nats, Z3)
+ *        gathered = logits[b,t,y] as float (bit-exact)
+ * If partner_logp != NULL (the reference pass, partner = logp_old, Z4):
+ *        d = partner_logp - logp;  kl = k(d) with estimator kl_est   S2
+ *        shaped_reward = [t == L_b-1] seq_reward[b] - beta_reward * kl
+ *                                                        S3, Z7
+ * logp is required; entropy, lse, gathered, kl, shaped_reward may be NULL.
+ * seq_reward is [B_total] (indexed by rank-local sequence) and is required
+ * when shaped_reward != NULL.  inv_temp > 0.  All per-token arrays are
+ * [B_total, T] and only the micro-batch's rows are written. */
+orl_status orl_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_logits *logits,
+                        float inv_temp, float *logp, float *entropy, float *lse,
+                        float *gathered, const float *partner_logp, int kl_est,
+                        double beta_reward, const float *seq_reward, float *kl,
+                        float *shaped_reward, void *stream);
+
+/* ---- S4 / S4' / S5: advantages over the whole rank-local batch --------- */
+
+/* kind = GAE:  needs shaped_reward, values (V_old, Z9); writes adv, ret.
+ *        RPP:  needs shaped_reward; writes adv (= return G_t) and, if
+ *              given, ret (= adv).
+ *        RPP_BASELINE: as RPP but first subtracts the group mean of
+ *              seq_reward (group_size consecutive sequences) from the
+ *              reward at t = L_b-1 (equivalent to shaping R_b - mu_g, Z23).
+ *        GRPO: needs seq_reward, group_size; writes adv[b,t] = A_b on valid
+ *              tokens; ret unused; constant groups give exactly 0.
+ * group_keep (optional, [B/group_size] uint8, GRPO and RPP_BASELINE) is the
+ * DAPO dynamic-sampling flag max_g - min_g >= 1e-12.
+ * gamma, lambda in [0,1].  The whitening partials (count, mean, M2 over valid
+ * tokens, fp64) are staged in ctx for orl_whiten_stats.
+ * ORL_E_GROUP_SPLIT if B is not a multiple of group_size (GRPO/RPP_BASELINE). */
+orl_status orl_advantages(orl_ctx *ctx, int64_t B, int64_t T, const int32_t *lengths,
+                          int kind, double gamma, double lambda, int group_size,
+                          const float *shaped_reward, const float *values,
+                          const float *seq_reward, float *adv, float *ret,
+                          uint8_t *group_keep, void *stream);
+
+/* ---- S6 + C1: global whitening moments -------------------------------- */
+
+/* Combines every rank's (count, mean, M2) in rank order (all-gather over
+ * NCCL when world > 1, then a fixed-order Chan merge on the device, so every
+ * rank gets bit-identical results).  whiten = 1: orl_ppo_loss will use
+ * A' = (A - mu)/(sigma + 1e-8) with the population sigma (Z18, Z19);
+ * with fewer than 2 tokens this is a no-op and whiten_warn is set.
+ * whiten = 0: only the global token count N is formed (needed for the
+ * token-mean loss, Z11).  Must follow orl_advantages. */
+orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream);
+
+/* ---- S1 + S7..S9: actor pass with the loss epilogue -------------------- */
+
+/* Recomputes logp_new and entropy from the actor logits (as orl_logprobs)
+ * and, per valid token, in fp64:
+ *   rho = exp(logp_new - logp_old); A' = whitened adv (if whitening on)
+ *   obj = min(rho A', clip(rho, 1-eps_low, 1+eps_high) A')
+ *   vl  = max((Vn-R)^2, (Vo + clip(Vn-Vo, +-eps_v) - R)^2)       P:197, Z13
+ *   k(new, ref) with cfg->kl_loss_est when logp_ref != NULL
+ * and accumulates fp64 sums into the context (fixed order: deterministic).
+ * Optional per-token outputs:
+ *   dloss_dlogp = (-[not clipped] rho A' + [kl_in_loss] beta k'(d_ref)) / N
+ *   dloss_dv    = c1 dvl/dVn / N   (ties take the unclipped branch, Z17)
+ * with N the global token count from orl_whiten_stats.
+ * logp_old, adv required; logp_ref optional; ret, v_new, v_old together or
+ * all NULL (no critic).  logp_new required; entropy, dloss_* optional. */
+orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
+                        float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
+                        const float *logp_ref, const float *adv, const float *ret,
+                        const float *v_new, const float *v_old, float *logp_new,
+                        float *entropy, float *dloss_dlogp, float *dloss_dv, void *stream);
+
+/* ---- S10 + C2: statistics ---------------------------------------------- */
+
+/* Sums the context's accumulators and error counters over ranks (all-gather
+ * + rank-ordered sum, C2), forms the means and total loss with cfg's c1,c2,
+ * beta_loss, writes the device vector dev_out (optional, double[16]) and the
+ * host struct host_out (optional), synchronises `stream`, and maps the error
+ * counters to a status: TOKEN_RANGE > NONFINITE > NUMERIC_GUARD >
+ * EMPTY_BATCH > OK (outputs are written in every case). */
+orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
+                        double *dev_out, void *stream);
+
+/* ---- collective boundary hooks (testing / custom transports) ----------- */
+
+/* which = 0: this rank's whitening partial (double[4]: count, mean, M2, 0),
+ *            valid after orl_advantages;
+ * which = 1: this rank's loss/stat partial (double[ORL_STATS_N]), valid
+ *            after the last orl_ppo_loss.
+ * Copies it to host memory `host_out` (synchronises `stream`). */
+orl_status orl_export_partials(orl_ctx *ctx, int which, double *host_out, void *stream);
+
+/* Supplies the gathered partials of `world` ranks (host, [world][4] or
+ * [world][ORL_STATS_N], rank order) in place of the NCCL all-gather for the
+ * next orl_whiten_stats (which = 0) or orl_finalize (which = 1) on this
+ * context.  Lets one process emulate n ranks on one GPU with the exact
+ * device merge the NCCL path runs. */
+orl_status orl_import_partials(orl_ctx *ctx, int which, const double *host_all, int world,
+                               void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORL_H */

@@ -1,0 +1,622 @@
+// k1_logprobs.cu -- K1: streaming full-vocabulary log-softmax + target gather +
+// entropy over [B,T,V] logits, with the S2/S3 reward epilogue (reference pass)
+// or the S7-S9 PPO-loss epilogue (actor pass).
+//
+//   lse = ln sum_v exp(x_v), logp = x_y - lse, H = -sum_v p_v ln p_v
+//
+//
+// B200 design: the path is HBM-bound (every logit is read
+// exactly once, ~0.013% of the bytes are anything else), so K1 is a
+// persistent, warp-specialised streaming kernel:
+//   * 2 CTAs/SM x (1 producer warp + 8 consumer warps).
+//   * The producer's elected lane streams each row in 16 KB chunks with 1-D
+//     TMA bulk copies (cp.async.bulk ... complete_tx, L2 evict_first) into a
+//     6-stage shared-memory ring guarded by full/empty mbarriers, so up to
+//     2 x 96 KB per SM is in flight (Little's law needs ~45 KB at ~7 TB/s).
+//   * Consumers read the ring with conflict-free 128-bit ld.shared and keep a
+//     per-thread online (max, sum, first-moment) state in log2 units with
+//     packed f32x2 FMA/ADD (FFMA2/FADD2) and bf16x2 max (HMNMX2), one
+//     MUFU.EX2 per element, one rescale per 32-element chunk.
+//   * Row end: warp shuffle merge, per-warp partials into a 4-slot row ring
+//     (mbarrier protected); the row's epilogue warp (row % 8) merges the 8
+//     partials in fixed order and runs the fp64 epilogue while the other
+//     warps already stream the next row.  Side inputs of the epilogue are
+//     prefetched at row start so their latency hides under the row.
+//   * Valid rows are enumerated compactly (prefix sum of lengths in smem) and
+//     dealt round-robin to CTAs: equal work per CTA, masked rows never read.
+//   * Loss partials: fp64 per warp in smem, per CTA in a workspace, reduced in
+//     fixed order by the last CTA (ticket) -> deterministic, no extra launch.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "orl_device.cuh"
+#include "orl_internal.h"
+
+namespace orl {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;
+constexpr int kChunk = 16384;  // bytes per TMA stage
+constexpr int kStages = 6;
+constexpr int kSlots = 4;
+constexpr int kVecPerThread = kChunk / 16 / kConsumers;  // 4 x 16 B per thread per chunk
+static_assert(kVecPerThread == 4, "chunk processing is written for 4 vectors per thread");
+
+struct RowSlot {
+    float m[kConsumerWarps], s[kConsumerWarps], u[kConsumerWarps];
+    float target;
+    float pad[7];
+};
+
+struct __align__(128) K1Smem {
+    uint8_t stage[kStages][kChunk];
+    uint64_t full[kStages];
+    uint64_t empty[kStages];
+    uint64_t row_full[kSlots];
+    uint64_t row_empty[kSlots];
+    RowSlot slot[kSlots];
+    double wacc[kConsumerWarps][kNumPartials];
+    int32_t misc[4];
+};
+
+size_t k1_tma_smem_bytes(int B) { return sizeof(K1Smem) + sizeof(int32_t) * (size_t)(B + 32); }
+
+// ---------------------------------------------------------------- prologue
+// Inclusive prefix of the clamped lengths of the micro-batch into cum[0..B).
+// Counts invalid lengths (< 0 or > T) once (block 0) in err[2].
+__device__ void build_prefix(const K1Params &p, int32_t *cum, int32_t *warp_tot) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int per = (p.B + nthr - 1) / nthr;
+    const int beg = min(p.B, tid * per), end = min(p.B, beg + per);
+    int local = 0, bad = 0;
+    for (int b = beg; b < end; ++b) {
+        int L = p.lengths[p.seq_offset + b];
+        if (L < 0 || L > p.T) ++bad;
+        L = L < 0 ? 0 : (L > p.T ? p.T : L);
+        local += L;
+        cum[b] = local;
+    }
+    if (bad && blockIdx.x == 0) atomicAdd(&p.err[2], (unsigned long long)bad);
+    // exclusive scan of the per-thread totals across the block
+    const int lane = tid & 31, warp = tid >> 5;
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int w = 0; w < (nthr + 31) / 32; ++w) {
+            int v = warp_tot[w];
+            warp_tot[w] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    const int excl = warp_tot[warp] + incl - local;
+    for (int b = beg; b < end; ++b) cum[b] += excl;
+    __syncthreads();
+}
+
+// Write exact zeros to every output at the masked positions of the call.
+__device__ void zero_masked(const K1Params &p, const int32_t *cum, int lt, int nthr, int mode) {
+    const int64_t total = (int64_t)p.B * p.T;
+    for (int64_t q = (int64_t)blockIdx.x * nthr + lt; q < total; q += (int64_t)gridDim.x * nthr) {
+        const int b = (int)(q / p.T), t = (int)(q % p.T);
+        const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+        if (t < L) continue;
+        const int64_t i = (p.seq_offset + b) * (int64_t)p.T + t;
+        if (p.logp) p.logp[i] = 0.f;
+        if (p.entropy) p.entropy[i] = 0.f;
+        if (p.lse) p.lse[i] = 0.f;
+        if (p.gathered) p.gathered[i] = 0.f;
+        if (mode == kModeLogprob) {
+            if (p.kl_out) p.kl_out[i] = 0.f;
+            if (p.shaped) p.shaped[i] = 0.f;
+        } else {
+            if (p.dlogp) p.dlogp[i] = 0.f;
+            if (p.dv) p.dv[i] = 0.f;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- epilogue
+// Side inputs of one row (loaded ahead of time): loss mode {logp_old,
+// logp_ref, adv, ret, v_new, v_old}; logprob mode {partner, seq_reward}.
+__device__ __forceinline__ float load_side(const K1Params &p, int mode, int k, int64_t i, int b) {
+    const float *ptr = nullptr;
+    int64_t idx = i;
+    if (mode == kModeLoss) {
+        ptr = k == 0 ? p.logp_old : k == 1 ? p.logp_ref : k == 2 ? p.adv : k == 3 ? p.ret
+            : k == 4 ? p.v_new : k == 5 ? p.v_old : nullptr;
+    } else {
+        if (k == 0) ptr = p.partner;
+        if (k == 1) { ptr = p.seq_reward; idx = p.seq_offset + b; }
+    }
+    return ptr ? __ldg(ptr + idx) : 0.f;
+}
+
+// fp64 per-row epilogue (runs on one thread).  `tot` is the merged online
+// state of the row, `target` the raw logit x[b,t,y] (as float, exact).
+template <int MODE>
+__device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Online tot,
+                             float target, const float *side, const double *wh, double *wacc) {
+    const int64_t i = (p.seq_offset + b) * (int64_t)p.T + t;
+    const bool oob = (y < 0) || (y >= p.V);
+    const double log2s = log2((double)tot.s);
+    double lse = kLn2 * ((double)tot.m + log2s);
+    double H = kLn2 * (log2s - (double)tot.u / (double)tot.s);
+    double logp = (double)target * (double)p.inv_temp - lse;
+    const bool dead = tot.m / p.c2 < 0.5f * kNegClampF32;  // every logit -inf
+    if (oob) {
+        atomicAdd(&p.err[0], 1ull);
+        lse = H = logp = __longlong_as_double(0x7ff8000000000000ll);
+    } else if (dead || !(isfinite(lse) && isfinite(logp) && isfinite(H))) {
+        atomicAdd(&p.err[1], 1ull);
+        if (dead) lse = H = logp = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    const float logp_f = (float)logp, H_f = (float)H;
+    p.logp[i] = logp_f;
+    if (p.entropy) p.entropy[i] = H_f;
+    if (p.lse) p.lse[i] = (float)lse;
+    if (p.gathered) p.gathered[i] = oob ? __int_as_float(0x7fc00000) : target;
+
+    if (MODE == kModeLogprob) {
+        if (p.partner) {
+            // S2 + S3 (Z4, Z7): d = logp_old - logp_ref,
+            // r'_t = [t = L_b - 1] R_b - beta k(d)
+            const double d = (double)side[0] - (double)logp_f;
+            const double k = kl_est(d, p.kl_est);
+            if (p.kl_out) p.kl_out[i] = (float)k;
+            if (p.shaped) {
+                const double r = (t == L - 1) ? (double)side[1] : 0.0;
+                p.shaped[i] = (float)(r - p.beta_reward * k);
+            }
+        }
+        return;
+    } else {
+        // S7-S9 (Z11-Z17, Z22), all in fp64
+        const double N = wh[0];
+        double A = (double)side[2];
+        if (wh[3] != 0.0) A = (A - wh[1]) / (wh[2] + 1e-8);
+        const double lpn = (double)logp_f, lpo = (double)side[0];
+        const double dold = lpn - lpo;
+        const double rho = exp(dold);
+        const double rc = fmin(fmax(rho, 1.0 - p.eps_low), 1.0 + p.eps_high);
+        const double unc = rho * A, clt = rc * A;
+        const bool clipped = clt < unc;
+        const double obj = clipped ? clt : unc;
+        double vl = 0.0, dvl = 0.0;
+        bool vclipped = false;
+        if (p.v_new) {
+            const double vn = side[4], vo = side[5], R = side[3];
+            const double e1 = vn - R;
+            if (p.eps_v > 0.0) {
+                const double dvv = vn - vo;
+                const double dvc = fmin(fmax(dvv, -p.eps_v), p.eps_v);
+                const double e2 = vo + dvc - R;
+                vclipped = (e2 * e2) > (e1 * e1);
+                vl = vclipped ? e2 * e2 : e1 * e1;
+                dvl = vclipped ? (fabs(dvv) < p.eps_v ? 2.0 * e2 : 0.0) : 2.0 * e1;
+            } else {
+                vl = e1 * e1;
+                dvl = 2.0 * e1;
+            }
+        }
+        double kref = 0.0, dkref = 0.0;
+        if (p.logp_ref) {
+            const double dr = lpn - (double)side[1];
+            kref = kl_est(dr, p.kl_loss_est);
+            dkref = kl_grad(dr, p.kl_loss_est);
+        }
+        const double k3old = kl_est(lpo - lpn, 3);
+        const double Hd = (double)H_f;
+        wacc[0] += 1.0;
+        wacc[1] += obj;
+        wacc[2] += vl;
+        wacc[3] += Hd;
+        wacc[4] += kref;
+        wacc[5] += clipped ? 1.0 : 0.0;
+        wacc[6] += vclipped ? 1.0 : 0.0;
+        wacc[7] += k3old;
+        wacc[8] += rho;
+        if (fabs(dold) > p.ratio_guard) wacc[9] += 1.0;
+        if (!(isfinite(obj) && isfinite(vl) && isfinite(Hd) && isfinite(kref))) wacc[10] += 1.0;
+        if (p.dlogp)
+            p.dlogp[i] = (float)(((clipped ? 0.0 : -rho * A) +
+                                  (p.kl_in_loss ? p.beta_loss * dkref : 0.0)) / N);
+        if (p.dv) p.dv[i] = (float)(p.c1 * dvl / N);
+    }
+}
+
+// ---------------------------------------------------------------- CTA partials
+// Deterministic reduction of the loss partials: per-warp smem accumulators
+// summed in warp order, per-CTA partials summed in CTA order by the last CTA.
+__device__ void finish_partials(const K1Params &p, double (*wacc)[kNumPartials], int nwarps,
+                                int lt, int nthr, int bar_id) {
+    __shared__ double scratch[8][kNumPartials];
+    if (bar_id >= 0) named_bar_sync(bar_id, nthr);
+    else __syncthreads();
+    if (lt < kNumPartials) {
+        double s = 0.0;
+        for (int w = 0; w < nwarps; ++w) s += wacc[w][lt];
+        p.ws[(size_t)lt * p.ws_stride + blockIdx.x] = s;
+    }
+    __threadfence();
+    if (bar_id >= 0) named_bar_sync(bar_id, nthr);
+    else __syncthreads();
+    __shared__ unsigned int s_last;
+    if (lt == 0) s_last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    if (bar_id >= 0) named_bar_sync(bar_id, nthr);
+    else __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // fixed-shape reduction over CTAs: thread lt sums CTAs lt, lt+nthr, ...
+    // per column, then a fixed warp tree and a fixed in-order warp sum.
+    const int lane = lt & 31, w = lt >> 5;
+    for (int c = 0; c < kNumPartials; ++c) {
+        double s = 0.0;
+        for (int q = lt; q < (int)gridDim.x; q += nthr)
+            s += __ldcg(&p.ws[(size_t)c * p.ws_stride + q]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) scratch[w][c] = s;
+    }
+    if (bar_id >= 0) named_bar_sync(bar_id, nthr);
+    else __syncthreads();
+    if (lt < kNumPartials) {
+        double s = 0.0;
+        for (int q = 0; q < nthr / 32; ++q) s += scratch[q][lt];
+        p.acc[lt] += s;
+    }
+    if (lt == 0) *p.ticket = 0u;
+}
+
+// ---------------------------------------------------------------- TMA kernel
+template <typename Tin, int MODE>
+__global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    K1Smem &S = *reinterpret_cast<K1Smem *>(smem_raw);
+    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw + sizeof(K1Smem));
+    int32_t *warp_tot = cum + p.B;  // 32 ints after the prefix
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], kConsumerWarps);
+        }
+        for (int s = 0; s < kSlots; ++s) {
+            mbar_init(&S.row_full[s], kConsumerWarps);
+            mbar_init(&S.row_empty[s], 1);
+        }
+        fence_mbar_init();
+    }
+    if (tid < kConsumerWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
+    build_prefix(p, cum, warp_tot);  // contains __syncthreads
+    const int64_t N = cum[p.B - 1];
+    const int64_t row_bytes = p.row_bytes;
+
+    if (warp == kConsumerWarps) {
+        // ===================== producer: one elected lane issues TMA ==========
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t j = blockIdx.x; j < N; j += gridDim.x) {
+                int b, t;
+                locate_row(cum, p.B, j, b, t);
+                const char *src = p.base + ((int64_t)b * p.stride_b + (int64_t)t * p.stride_t) * p.elt;
+                for (int64_t off = 0; off < row_bytes; off += kChunk) {
+                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
+                    mbar_wait(&S.empty[stage], phase ^ 1u);
+                    mbar_arrive_expect_tx(&S.full[stage], bytes);
+                    tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+        return;  // the producer warp takes no part in the consumer barriers
+    }
+
+    // ========================= consumers ======================================
+    const int ct = tid;  // 0..255
+    zero_masked(p, cum, ct, kConsumers, MODE);
+    double wh[4] = {0.0, 0.0, 0.0, 0.0};
+    if (MODE == kModeLoss) {
+        wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
+    }
+    constexpr int EPV = 16 / sizeof(Tin);  // elements per 16-byte vector
+    const int nside = MODE == kModeLoss ? 6 : 2;
+
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t j = blockIdx.x;
+    int b = 0, t = 0, y = 0;
+    if (j < N) {
+        locate_row(cum, p.B, j, b, t);
+        y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
+    }
+    for (int rl = 0; j < N; j += gridDim.x, ++rl) {
+        // prefetch the next row's token id
+        const int64_t jn = j + gridDim.x;
+        int bn = 0, tn = 0, yn = 0;
+        if (jn < N) {
+            locate_row(cum, p.B, jn, bn, tn);
+            yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
+        }
+        const bool epi = (rl % kConsumerWarps) == warp;
+        const int slot = rl % kSlots;
+        const uint32_t slot_par = (uint32_t)(rl / kSlots) & 1u;
+        const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
+        float side = 0.f;
+        if (epi && lane < nside) side = load_side(p, MODE, lane, gi, b);
+
+        const uint64_t c2p = pack2(p.c2, p.c2);
+        float m = kMInit;
+        uint64_t sA = 0, sB = 0, uA = 0, uB = 0;  // packed (even, odd) accumulators
+        float tgt = 0.f;
+        bool have_tgt = false;
+
+        for (int64_t off = 0; off < row_bytes; off += kChunk) {
+            const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
+            const int nvec = bytes >> 4;
+            mbar_wait(&S.full[stage], phase);
+            const uint8_t *sb = S.stage[stage];
+            // target capture (raw value, before clamping)
+            {
+                const int64_t first = off / sizeof(Tin);
+                const int64_t loc = (int64_t)y - first;
+                if (loc >= 0 && loc < bytes / (int)sizeof(Tin)) {
+                    const int vec = (int)(loc / EPV);
+                    if ((vec % kConsumers) == ct) {
+                        if (sizeof(Tin) == 2)
+                            tgt = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(sb)[loc]) << 16);
+                        else
+                            tgt = reinterpret_cast<const float *>(sb)[loc];
+                        have_tgt = true;
+                    }
+                }
+            }
+            if (sizeof(Tin) == 2) {
+                uint32_t w[16];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int vi = ct + k * kConsumers;
+                    uint4 v = make_uint4(kNegClampBf16x2, kNegClampBf16x2, kNegClampBf16x2, kNegClampBf16x2);
+                    if (vi < nvec) v = lds128(sb + vi * 16);
+                    w[4 * k + 0] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+                }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) w[q] = hmax2_nan(w[q], kNegClampBf16x2);
+                uint32_t mx[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) mx[q] = hmax2_nan(w[q], w[q + 8]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) mx[q] = hmax2_nan(mx[q], mx[q + 4]);
+                mx[0] = hmax2_nan(hmax2_nan(mx[0], mx[2]), hmax2_nan(mx[1], mx[3]));
+                const float cm = fmax_nan(bf16lo(mx[0]), bf16hi(mx[0])) * p.c2;
+                const float mn = fmax_nan(m, cm);
+                const float d = m - mn;
+                const float r = ex2(d);
+                const uint64_t d2 = pack2(d, d), r2 = pack2(r, r);
+                uA = fmul2(r2, ffma2(d2, sA, uA));
+                uB = fmul2(r2, ffma2(d2, sB, uB));
+                sA = fmul2(r2, sA);
+                sB = fmul2(r2, sB);
+                m = mn;
+                const uint64_t nm = pack2(-m, -m);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const uint64_t x = pack2(bf16lo(w[q]), bf16hi(w[q]));
+                    const uint64_t tt = ffma2(x, c2p, nm);
+                    float t0, t1;
+                    unpack2(tt, t0, t1);
+                    const uint64_t e = pack2(ex2(t0), ex2(t1));
+                    if (q & 1) { sB = fadd2(sB, e); uB = ffma2(e, tt, uB); }
+                    else       { sA = fadd2(sA, e); uA = ffma2(e, tt, uA); }
+                }
+            } else {
+                float f[16];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int vi = ct + k * kConsumers;
+                    uint4 v = make_uint4(__float_as_uint(kNegClampF32), __float_as_uint(kNegClampF32),
+                                         __float_as_uint(kNegClampF32), __float_as_uint(kNegClampF32));
+                    if (vi < nvec) v = lds128(sb + vi * 16);
+                    f[4 * k + 0] = __uint_as_float(v.x); f[4 * k + 1] = __uint_as_float(v.y);
+                    f[4 * k + 2] = __uint_as_float(v.z); f[4 * k + 3] = __uint_as_float(v.w);
+                }
+                float cmx = kNegClampF32;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    f[q] = fmax_nan(f[q], kNegClampF32);
+                    cmx = fmax_nan(cmx, f[q]);
+                }
+                const float mn = fmax_nan(m, cmx * p.c2);
+                const float d = m - mn;
+                const float r = ex2(d);
+                const uint64_t d2 = pack2(d, d), r2 = pack2(r, r);
+                uA = fmul2(r2, ffma2(d2, sA, uA));
+                uB = fmul2(r2, ffma2(d2, sB, uB));
+                sA = fmul2(r2, sA);
+                sB = fmul2(r2, sB);
+                m = mn;
+                const uint64_t nm = pack2(-m, -m);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint64_t x = pack2(f[2 * q], f[2 * q + 1]);
+                    const uint64_t tt = ffma2(x, c2p, nm);
+                    float t0, t1;
+                    unpack2(tt, t0, t1);
+                    const uint64_t e = pack2(ex2(t0), ex2(t1));
+                    if (q & 1) { sB = fadd2(sB, e); uB = ffma2(e, tt, uB); }
+                    else       { sA = fadd2(sA, e); uA = ffma2(e, tt, uA); }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1u; }
+        }
+
+        // ---- row end: thread -> warp -> slot ----
+        float s0, s1, s2, s3, u0, u1, u2, u3;
+        unpack2(sA, s0, s1);
+        unpack2(sB, s2, s3);
+        unpack2(uA, u0, u1);
+        unpack2(uB, u2, u3);
+        Online st{m, (s0 + s1) + (s2 + s3), (u0 + u1) + (u2 + u3)};
+        st = warp_merge(st);
+        mbar_wait(&S.row_empty[slot], slot_par ^ 1u);
+        if (lane == 0) {
+            S.slot[slot].m[warp] = st.m;
+            S.slot[slot].s[warp] = st.s;
+            S.slot[slot].u[warp] = st.u;
+        }
+        if (have_tgt) S.slot[slot].target = tgt;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.row_full[slot]);
+
+        if (epi) {
+            float sv[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
+            mbar_wait(&S.row_full[slot], slot_par);
+            Online tot{S.slot[slot].m[0], S.slot[slot].s[0], S.slot[slot].u[0]};
+#pragma unroll
+            for (int w = 1; w < kConsumerWarps; ++w)
+                tot = online_merge(tot, Online{S.slot[slot].m[w], S.slot[slot].s[w], S.slot[slot].u[w]});
+            const float target = S.slot[slot].target;
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&S.row_empty[slot]);
+                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+                row_epilogue<MODE>(p, b, t, L, y, tot, target, sv, wh, S.wacc[warp]);
+            }
+        }
+        b = bn; t = tn; y = yn;
+    }
+    if (MODE == kModeLoss) finish_partials(p, S.wacc, kConsumerWarps, ct, kConsumers, 1);
+}
+
+// ---------------------------------------------------------------- generic kernel
+// Unaligned rows (e.g. V = 50257 bf16): 256 threads per row, element-strided
+// global loads, the same online state and epilogue.  Correctness path.
+template <typename Tin, int MODE>
+__global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ double wacc[1][kNumPartials];
+    __shared__ float sm_m[8], sm_s[8], sm_u[8];
+    __shared__ float sm_tgt;
+    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw);
+    int32_t *warp_tot = cum + p.B;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < kNumPartials) wacc[0][tid] = 0.0;
+    build_prefix(p, cum, warp_tot);
+    const int64_t N = cum[p.B - 1];
+    zero_masked(p, cum, tid, 256, MODE);
+    double wh[4] = {0.0, 0.0, 0.0, 0.0};
+    if (MODE == kModeLoss) {
+        wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
+    }
+    for (int64_t j = blockIdx.x; j < N; j += gridDim.x) {
+        int b, t;
+        locate_row(cum, p.B, j, b, t);
+        const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
+        const int y = __ldg(p.tokens + gi);
+        const Tin *row = reinterpret_cast<const Tin *>(p.base) + (int64_t)b * p.stride_b + (int64_t)t * p.stride_t;
+        Online st{kMInit, 0.f, 0.f};
+        for (int64_t v0 = 0; v0 < p.V; v0 += 256 * 8) {
+            float x[8];
+            float cmx = kNegClampF32;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int64_t v = v0 + tid + k * 256;
+                float xv = kNegClampF32;
+                if (v < p.V) {
+                    if (sizeof(Tin) == 2)
+                        xv = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(row)[v]) << 16);
+                    else
+                        xv = reinterpret_cast<const float *>(row)[v];
+                    if (v == y) sm_tgt = xv;
+                }
+                x[k] = fmax_nan(xv, kNegClampF32);
+                cmx = fmax_nan(cmx, x[k]);
+            }
+            const float mn = fmax_nan(st.m, cmx * p.c2);
+            const float d = st.m - mn, r = ex2(d);
+            st.u = r * fmaf(d, st.s, st.u);
+            st.s = r * st.s;
+            st.m = mn;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float tt = fmaf(x[k], p.c2, -st.m);
+                const float e = ex2(tt);
+                st.s += e;
+                st.u = fmaf(e, tt, st.u);
+            }
+        }
+        st = warp_merge(st);
+        if (lane == 0) { sm_m[warp] = st.m; sm_s[warp] = st.s; sm_u[warp] = st.u; }
+        __syncthreads();
+        float side[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (tid == 0) {
+            Online tot{sm_m[0], sm_s[0], sm_u[0]};
+            for (int w = 1; w < 8; ++w) tot = online_merge(tot, Online{sm_m[w], sm_s[w], sm_u[w]});
+            const int nside = MODE == kModeLoss ? 6 : 2;
+            for (int k = 0; k < nside; ++k) side[k] = load_side(p, MODE, k, gi, b);
+            const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+            row_epilogue<MODE>(p, b, t, L, y, tot, sm_tgt, side, wh, wacc[0]);
+        }
+        __syncthreads();
+    }
+    if (MODE == kModeLoss) finish_partials(p, wacc, 1, tid, 256, -1);
+}
+
+// ---------------------------------------------------------------- launcher
+template <typename Tin, int MODE>
+static cudaError_t launch_typed(const K1Params &p, bool tma, int num_sms, cudaStream_t s) {
+    const int64_t N_upper = (int64_t)p.B * p.T;  // rows are counted on device; size by the bound
+    if (tma) {
+        const size_t smem = k1_tma_smem_bytes(p.B);
+        cudaError_t e = cudaFuncSetAttribute(k1_tma_kernel<Tin, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tma_kernel<Tin, MODE>, kThreads, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorInvalidConfiguration;
+        int64_t grid = (int64_t)num_sms * per_sm;
+        if (grid > N_upper) grid = N_upper;
+        if (grid > p.ws_stride) grid = p.ws_stride;
+        if (grid < 1) grid = 1;
+        k1_tma_kernel<Tin, MODE><<<(unsigned)grid, kThreads, smem, s>>>(p);
+    } else {
+        const size_t smem = sizeof(int32_t) * (size_t)(p.B + 32);
+        cudaError_t e = cudaFuncSetAttribute(k1_generic_kernel<Tin, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int64_t grid = (int64_t)num_sms * 4;
+        if (grid > N_upper) grid = N_upper;
+        if (grid > p.ws_stride) grid = p.ws_stride;
+        if (grid < 1) grid = 1;
+        k1_generic_kernel<Tin, MODE><<<(unsigned)grid, 256, smem, s>>>(p);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaStream_t s) {
+    if (p.elt == 2)
+        return mode == kModeLoss ? launch_typed<uint16_t, kModeLoss>(p, tma, num_sms, s)
+                                 : launch_typed<uint16_t, kModeLogprob>(p, tma, num_sms, s);
+    return mode == kModeLoss ? launch_typed<float, kModeLoss>(p, tma, num_sms, s)
+                             : launch_typed<float, kModeLogprob>(p, tma, num_sms, s);
+}
+
+}  // namespace orl

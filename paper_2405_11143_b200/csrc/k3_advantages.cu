@@ -1,0 +1,273 @@
+// k3_advantages.cu -- K3/K4: advantages over the rank-local batch.
+//
+//   GAE:  delta_t = r'_t + gamma V_{t+1} [t+1 < L] - V_t
+//                 A_t = delta_t + gamma lambda A_{t+1},  A_{L} = 0,  R_t = A_t + V_t
+//   REINFORCE++ (north star, Z23):  G_t = r'_t + gamma G_{t+1}
+//   RPP-baseline: same with R_b - mu_g at t = L_b - 1
+//   GRPO: A_b = (R_b - mu_g)/(sigma_g + 1e-8), constant group -> 0
+//
+// One CTA (256 threads) per response.  The backward recursion is an affine
+// map per token (x -> delta_t + c x); each thread composes the maps of a
+// contiguous chunk in fp64, a block-wide suffix scan of the chunk maps gives
+// every chunk its carry-in, and a second pass writes A and R (fp32) from the
+// fp64 carry.  Depth O(T/256 + log 256) instead of O(T), fp64 carry as the
+// 1e-5 bar at T=8192, gamma=lambda=1 requires.
+// The CTA also forms the fp64 whitening partial (n_b, mean_b, M2_b) of the
+// stored fp32 advantages (two-pass within the response).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "orl_internal.h"
+
+namespace orl {
+
+constexpr int kK3Threads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int q = 0; q < kK3Threads / 32; ++q) s += sh[q];  // fixed order
+    return s;
+}
+
+__global__ void __launch_bounds__(kK3Threads) k3_kernel(const K3Params p) {
+    __shared__ double sh_m[kK3Threads], sh_b[kK3Threads];
+    __shared__ double sh_red[kK3Threads / 32];
+    __shared__ double sh_seq[2];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    int L = p.lengths[b];
+    if (L < 0 || L > p.T) {
+        if (tid == 0) atomicAdd(&p.err[2], 1ull);
+        L = L < 0 ? 0 : p.T;
+    }
+    const int64_t row = (int64_t)b * p.T;
+    const bool grpo = p.kind == 1;
+    const bool gae = p.kind == 0;
+    const bool base = p.kind == 3;
+
+    // ---- group statistics (GRPO, RPP-baseline), fp64, thread 0 -------------
+    if (tid == 0 && (grpo || base)) {
+        const int g0 = (b / p.G) * p.G;
+        double mx = p.seq_reward[g0], mn = mx, sum = 0.0;
+        for (int j = 0; j < p.G; ++j) {
+            const double r = p.seq_reward[g0 + j];
+            mx = fmax(mx, r);
+            mn = fmin(mn, r);
+            sum += r;
+        }
+        const double mu = sum / (double)p.G;
+        double ss = 0.0;
+        for (int j = 0; j < p.G; ++j) {
+            const double r = (double)p.seq_reward[g0 + j] - mu;
+            ss += r * r;
+        }
+        const double sigma = sqrt(ss / (double)p.G);
+        const double Rb = p.seq_reward[b];
+        sh_seq[0] = grpo ? ((mx == mn) ? 0.0 : (Rb - mu) / (sigma + 1e-8)) : mu;
+        if (p.keep && b == g0) p.keep[b / p.G] = (mx - mn >= 1e-12) ? 1 : 0;
+    }
+    __syncthreads();
+
+    if (grpo) {
+        const float a = (float)sh_seq[0];
+        for (int t = tid; t < p.T; t += kK3Threads) {
+            const float v = t < L ? a : 0.f;
+            p.adv[row + t] = v;
+            if (p.ret) p.ret[row + t] = v;
+        }
+        if (tid == 0) {
+            double *o = p.seq_part + 3 * (int64_t)b;
+            o[0] = (double)L;
+            o[1] = L > 0 ? (double)a : 0.0;
+            o[2] = 0.0;
+        }
+        return;
+    }
+
+    const double c = gae ? p.gamma * p.lambda : p.gamma;
+    const double mu_g = base ? sh_seq[0] : 0.0;
+    // delta_t in fp64 from the fp32 inputs
+    auto delta = [&](int t) -> double {
+        double d = (double)p.shaped[row + t];
+        if (base && t == L - 1) d -= mu_g;
+        if (gae) {
+            const double vn = (t + 1 < L) ? (double)p.values[row + t + 1] : 0.0;
+            d += p.gamma * vn - (double)p.values[row + t];
+        }
+        return d;
+    };
+    const int per = (L + kK3Threads - 1) / kK3Threads;
+    const int beg = min(L, tid * per), end = min(L, beg + per);
+
+    // pass 1: chunk map x -> M x + Bc over tokens [beg, end)
+    double M = 1.0, Bc = 0.0;
+    for (int t = end - 1; t >= beg; --t) {
+        Bc = delta(t) + c * Bc;
+        M *= c;
+    }
+    // suffix composition F_k = f_k o f_{k+1} o ... (inclusive), fixed shape
+    sh_m[tid] = M;
+    sh_b[tid] = Bc;
+    __syncthreads();
+    for (int off = 1; off < kK3Threads; off <<= 1) {
+        double m2 = 1.0, b2 = 0.0;
+        if (tid + off < kK3Threads) { m2 = sh_m[tid + off]; b2 = sh_b[tid + off]; }
+        __syncthreads();
+        // (M, Bc) o (m2, b2): x -> Bc + M (b2 + m2 x)
+        Bc = Bc + M * b2;
+        M = M * m2;
+        sh_m[tid] = M;
+        sh_b[tid] = Bc;
+        __syncthreads();
+    }
+    const double carry = (tid + 1 < kK3Threads) ? sh_b[tid + 1] : 0.0;  // A at t = end
+
+    // pass 2: write A, R; local sum of the stored fp32 advantages
+    double A = carry, lsum = 0.0;
+    for (int t = end - 1; t >= beg; --t) {
+        A = delta(t) + c * A;
+        const float af = (float)A;
+        p.adv[row + t] = af;
+        if (p.ret) p.ret[row + t] = gae ? (float)(A + (double)p.values[row + t]) : af;
+        lsum += (double)af;
+    }
+    for (int t = L + tid; t < p.T; t += kK3Threads) {
+        p.adv[row + t] = 0.f;
+        if (p.ret) p.ret[row + t] = 0.f;
+    }
+    // whitening partial of this response: n, mean, M2 (two-pass, fp64)
+    const double S = block_sum(lsum, sh_red);
+    const double mean = L > 0 ? S / (double)L : 0.0;
+    double lss = 0.0;
+    for (int t = beg; t < end; ++t) {
+        const double d = (double)p.adv[row + t] - mean;  // own writes
+        lss += d * d;
+    }
+    const double M2 = block_sum(lss, sh_red);
+    if (tid == 0) {
+        double *o = p.seq_part + 3 * (int64_t)b;
+        o[0] = (double)L;
+        o[1] = mean;
+        o[2] = M2;
+    }
+}
+
+cudaError_t launch_k3(const K3Params &p, cudaStream_t s) {
+    k3_kernel<<<p.B, kK3Threads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- whitening
+// Chan et al. pairwise merge of (n, mean, M2); fixed order -> deterministic.
+__device__ __forceinline__ void chan_merge(double &n, double &mean, double &M2, double nb,
+                                           double meanb, double M2b) {
+    if (nb <= 0.0) return;
+    if (n <= 0.0) { n = nb; mean = meanb; M2 = M2b; return; }
+    const double nt = n + nb;
+    const double d = meanb - mean;
+    mean = mean + d * (nb / nt);
+    M2 = M2 + M2b + d * d * (n * nb / nt);
+    n = nt;
+}
+
+__global__ void whiten_local_kernel(const double *seq_part, int B, double *slot) {
+    __shared__ double sn[256], sm[256], s2[256];
+    const int tid = threadIdx.x;
+    const int per = (B + 255) / 256;
+    const int beg = min(B, tid * per), end = min(B, beg + per);
+    double n = 0.0, mean = 0.0, M2 = 0.0;
+    for (int q = beg; q < end; ++q) chan_merge(n, mean, M2, seq_part[3 * q], seq_part[3 * q + 1], seq_part[3 * q + 2]);
+    sn[tid] = n; sm[tid] = mean; s2[tid] = M2;
+    __syncthreads();
+    if (tid == 0) {
+        double N = 0.0, mu = 0.0, m2 = 0.0;
+        for (int q = 0; q < 256; ++q) chan_merge(N, mu, m2, sn[q], sm[q], s2[q]);
+        slot[0] = N; slot[1] = mu; slot[2] = m2; slot[3] = 0.0;
+    }
+}
+
+cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_slot, cudaStream_t s) {
+    whiten_local_kernel<<<1, 256, 0, s>>>(seq_part, B, gather_slot);
+    return cudaGetLastError();
+}
+
+__global__ void whiten_merge_kernel(const double *gather, int world, int want, double *whiten,
+                                    double *flags) {
+    double N = 0.0, mu = 0.0, M2 = 0.0;
+    for (int r = 0; r < world; ++r) chan_merge(N, mu, M2, gather[4 * r], gather[4 * r + 1], gather[4 * r + 2]);
+    const bool apply = want && N >= 2.0;
+    whiten[0] = N;
+    whiten[1] = apply ? mu : 0.0;
+    whiten[2] = apply ? sqrt(M2 / N) : 0.0;
+    whiten[3] = apply ? 1.0 : 0.0;
+    flags[0] = (want && N < 2.0) ? 1.0 : 0.0;
+}
+
+cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten, double *whiten,
+                                double *flags, cudaStream_t s) {
+    whiten_merge_kernel<<<1, 1, 0, s>>>(gather, world, want_whiten, whiten, flags);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- statistics
+__global__ void stats_pack_kernel(const double *acc, const unsigned long long *err, double *out) {
+    const int k = threadIdx.x;
+    if (k < kNumPartials) out[k] = acc[k];
+    if (k == 12) out[12] = (double)err[0];
+    if (k == 13) out[13] = (double)err[1];
+    if (k == 14) out[14] = (double)err[2];
+    if (k == 15) out[15] = 0.0;
+}
+
+cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, double *out,
+                              cudaStream_t s) {
+    stats_pack_kernel<<<1, 32, 0, s>>>(acc, err, out);
+    return cudaGetLastError();
+}
+
+// S10: rank-ordered sum of the gathered partials, then the means.
+__global__ void stats_final_kernel(const double *gather, int world, const double *whiten,
+                                   double *flags, double c1, double c2, double beta_loss,
+                                   int kl_in_loss, double *st) {
+    double t[kStatsSlots];
+    for (int k = 0; k < kStatsSlots; ++k) t[k] = 0.0;
+    for (int r = 0; r < world; ++r)
+        for (int k = 0; k < kStatsSlots; ++k) t[k] += gather[kStatsSlots * r + k];
+    const double N = t[0];
+    const double inv = N > 0.0 ? 1.0 / N : 0.0;
+    st[0] = N;
+    st[1] = N > 0.0 ? -t[1] / N : 0.0;
+    st[2] = N > 0.0 ? t[2] / N : 0.0;
+    st[3] = N > 0.0 ? t[3] / N : 0.0;
+    st[4] = N > 0.0 ? t[4] / N : 0.0;
+    st[5] = N > 0.0 ? t[7] / N : 0.0;
+    st[6] = N > 0.0 ? t[5] / N : 0.0;
+    st[7] = N > 0.0 ? t[6] / N : 0.0;
+    st[8] = N > 0.0 ? t[8] / N : 0.0;
+    (void)inv;
+    st[9] = st[1] + c1 * st[2] - c2 * st[3] + (kl_in_loss ? beta_loss * st[4] : 0.0);
+    st[10] = whiten[1];
+    st[11] = whiten[2];
+    st[12] = t[9];
+    st[13] = t[10] + t[13];
+    st[14] = t[12];
+    st[15] = flags[0];
+    flags[1] = t[14];  // invalid lengths (ORL_E_MASK)
+}
+
+cudaError_t launch_stats_final(const double *gather, int world, const double *whiten,
+                               const double *flags, double c1, double c2, double beta_loss,
+                               int kl_in_loss, double *stats_out, cudaStream_t s) {
+    stats_final_kernel<<<1, 1, 0, s>>>(gather, world, whiten, const_cast<double *>(flags), c1, c2,
+                                       beta_loss, kl_in_loss, stats_out);
+    return cudaGetLastError();
+}
+
+}  // namespace orl

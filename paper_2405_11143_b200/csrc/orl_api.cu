@@ -1,0 +1,533 @@
+// orl_api.cu -- the C ABI of liborl.so (include/orl.h): host-side validation,
+// context (NCCL communicator, fp64 accumulators, device error counters,
+// pinned stats slot), launch configuration and the two collectives:
+//   C1 = all-gather of the rank whitening partials (count, mean, M2) + a
+//        fixed-order Chan merge on the device (orl_whiten_stats),
+//   C2 = all-gather of the rank loss/stat partials + a rank-ordered sum
+//        (orl_finalize).
+// An all-gather of a few doubles followed by an ordered merge gives every
+// rank bit-identical results (a ring all-reduce would not fix the order);
+// messages are <= 128 B per rank, so the cost is NCCL launch latency.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/orl.h"
+#include "orl_internal.h"
+
+using namespace orl;
+
+static_assert(sizeof(ncclUniqueId) == ORL_UNIQUE_ID_BYTES, "unique id size");
+
+namespace {
+constexpr int kMaxWorld = 256;
+thread_local std::string g_thread_err;
+}  // namespace
+
+struct orl_ctx {
+    int device = 0, world = 1, rank = 0, num_sms = 148;
+    ncclComm_t comm = nullptr;
+    double *d_acc = nullptr;           // [16] loss accumulators
+    unsigned long long *d_err = nullptr;  // [kNumErr]
+    double *d_ws = nullptr;            // [kNumPartials][ws_stride]
+    int ws_stride = 0;
+    unsigned int *d_ticket = nullptr;
+    double *d_seq_part = nullptr;      // [cap][3]
+    int64_t seq_cap = 0;
+    int64_t adv_B = 0;
+    double *d_gather_w = nullptr;      // [kMaxWorld][4]
+    double *d_whiten = nullptr;        // [4] N, mu, sigma, apply
+    double *d_flags = nullptr;         // [4] whiten_warn, mask errors
+    double *d_gather_s = nullptr;      // [kMaxWorld][16]
+    double *d_stats = nullptr;         // [16]
+    double *h_stats = nullptr;         // pinned [16 + 4]
+    bool have_adv = false, have_whiten = false;
+    int imported_w = 0, imported_s = 0;
+    uint64_t launches = 0;
+    std::string err;
+};
+
+// ------------------------------------------------------------------ helpers
+static orl_status fail(orl_ctx *ctx, orl_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    g_thread_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                     \
+    do {                                                                                        \
+        cudaError_t e_ = (expr);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail((ctx), ORL_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),      \
+                        __FILE__, __LINE__);                                                    \
+    } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                     \
+    do {                                                                                        \
+        ncclResult_t r_ = (expr);                                                               \
+        if (r_ != ncclSuccess)                                                                  \
+            return fail((ctx), ORL_E_NCCL, "%s: %s", #expr, ncclGetErrorString(r_));           \
+    } while (0)
+
+static bool aligned4(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+static cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static orl_status set_device(orl_ctx *ctx) {
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    return ORL_OK;
+}
+
+static orl_status validate_rows_logits(orl_ctx *ctx, const orl_rows *rows, const orl_logits *lg,
+                                       float inv_temp) {
+    if (!rows || !lg) return fail(ctx, ORL_E_INVALID_ARG, "rows/logits is NULL");
+    if (!rows->tokens || !rows->lengths || !lg->ptr)
+        return fail(ctx, ORL_E_INVALID_ARG, "tokens, lengths and logits.ptr are required");
+    if (lg->dtype != ORL_BF16 && lg->dtype != ORL_F32)
+        return fail(ctx, ORL_E_DTYPE, "unknown logits dtype %d", lg->dtype);
+    if (rows->B < 1 || rows->B > ORL_MAX_SEQ_PER_CALL)
+        return fail(ctx, ORL_E_SHAPE, "B=%lld outside [1, %d]", (long long)rows->B, ORL_MAX_SEQ_PER_CALL);
+    if (rows->T < 1 || rows->seq_offset < 0)
+        return fail(ctx, ORL_E_SHAPE, "T=%lld / seq_offset=%lld invalid", (long long)rows->T,
+                    (long long)rows->seq_offset);
+    if (rows->B * rows->T >= (int64_t)1 << 31 || (rows->seq_offset + rows->B) * rows->T >= (int64_t)1 << 40)
+        return fail(ctx, ORL_E_SHAPE, "B*T too large");
+    if (lg->V < 1 || lg->V >= ((int64_t)1 << 31))
+        return fail(ctx, ORL_E_SHAPE, "V=%lld invalid", (long long)lg->V);
+    if (lg->stride_t < lg->V || lg->stride_b < 0)
+        return fail(ctx, ORL_E_SHAPE, "strides (%lld, %lld) invalid for V=%lld", (long long)lg->stride_b,
+                    (long long)lg->stride_t, (long long)lg->V);
+    if (!(inv_temp > 0.f) || !(inv_temp <= 1.0e4f))
+        return fail(ctx, ORL_E_INVALID_ARG, "inv_temp=%g must be in (0, 1e4]", (double)inv_temp);
+    if (!aligned4(rows->tokens) || !aligned4(rows->lengths))
+        return fail(ctx, ORL_E_ALIGN, "tokens/lengths must be 4-byte aligned");
+    return ORL_OK;
+}
+
+static bool tma_eligible(const orl_logits *lg) {
+    if (getenv("ORL_FORCE_GENERIC")) return false;
+    const int64_t elt = lg->dtype == ORL_BF16 ? 2 : 4;
+    const uintptr_t base = reinterpret_cast<uintptr_t>(lg->ptr);
+    return (base % 16 == 0) && ((lg->V * elt) % 16 == 0) && ((lg->stride_t * elt) % 16 == 0) &&
+           ((lg->stride_b * elt) % 16 == 0);
+}
+
+static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const orl_logits *lg,
+                        float inv_temp) {
+    std::memset(&p, 0, sizeof p);
+    p.base = static_cast<const char *>(lg->ptr);
+    p.V = lg->V;
+    p.stride_b = lg->stride_b;
+    p.stride_t = lg->stride_t;
+    p.elt = lg->dtype == ORL_BF16 ? 2 : 4;
+    p.row_bytes = lg->V * p.elt;
+    p.inv_temp = inv_temp;
+    p.c2 = inv_temp * 1.4426950408889634f;
+    p.B = (int)rows->B;
+    p.T = (int)rows->T;
+    p.seq_offset = rows->seq_offset;
+    p.tokens = rows->tokens;
+    p.lengths = rows->lengths;
+    p.ws = ctx->d_ws;
+    p.ws_stride = ctx->ws_stride;
+    p.ticket = ctx->d_ticket;
+    p.acc = ctx->d_acc;
+    p.err = ctx->d_err;
+    p.whiten = ctx->d_whiten;
+}
+
+// ------------------------------------------------------------------ context
+extern "C" int orl_version(void) { return ORL_VERSION; }
+
+extern "C" orl_status orl_get_unique_id(unsigned char *id_out) {
+    if (!id_out) return fail(nullptr, ORL_E_INVALID_ARG, "id_out is NULL");
+    ncclUniqueId id;
+    NCCL_TRY(nullptr, ncclGetUniqueId(&id));
+    std::memcpy(id_out, &id, sizeof id);
+    return ORL_OK;
+}
+
+extern "C" orl_status orl_create(int device, int world, int rank, const unsigned char *id, orl_ctx **out) {
+    if (!out) return fail(nullptr, ORL_E_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+        return fail(nullptr, ORL_E_INVALID_ARG, "world=%d rank=%d invalid", world, rank);
+    if (world > 1 && !id) return fail(nullptr, ORL_E_INVALID_ARG, "world > 1 needs a unique id");
+    int ndev = 0;
+    CUDA_TRY(nullptr, cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(nullptr, ORL_E_INVALID_ARG, "device %d of %d", device, ndev);
+    orl_ctx *ctx = new orl_ctx();
+    ctx->device = device;
+    ctx->world = world;
+    ctx->rank = rank;
+    auto cleanup_fail = [&](orl_status st) {
+        orl_destroy(ctx);
+        return st;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return cleanup_fail(fail(nullptr, ORL_E_CUDA, "cudaSetDevice"));
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+        return cleanup_fail(fail(nullptr, ORL_E_CUDA, "cudaGetDeviceProperties"));
+    if (prop.major != 10)
+        return cleanup_fail(fail(nullptr, ORL_E_CUDA, "liborl is built for sm_100a; device is sm_%d%d",
+                                 prop.major, prop.minor));
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->ws_stride = ctx->num_sms * 8;
+    bool ok = cudaMalloc(&ctx->d_acc, 16 * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_err, kNumErr * sizeof(unsigned long long)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_ws, (size_t)kNumPartials * ctx->ws_stride * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_ticket, sizeof(unsigned int)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_gather_w, (size_t)kMaxWorld * 4 * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_whiten, 4 * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_flags, 4 * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_gather_s, (size_t)kMaxWorld * kStatsSlots * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_stats, kStatsSlots * sizeof(double)) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_stats, (kStatsSlots + 4) * sizeof(double)) == cudaSuccess;
+    if (!ok) return cleanup_fail(fail(nullptr, ORL_E_CUDA, "device allocation failed"));
+    ok = cudaMemset(ctx->d_acc, 0, 16 * sizeof(double)) == cudaSuccess &&
+         cudaMemset(ctx->d_err, 0, kNumErr * sizeof(unsigned long long)) == cudaSuccess &&
+         cudaMemset(ctx->d_ticket, 0, sizeof(unsigned int)) == cudaSuccess &&
+         cudaMemset(ctx->d_whiten, 0, 4 * sizeof(double)) == cudaSuccess &&
+         cudaMemset(ctx->d_flags, 0, 4 * sizeof(double)) == cudaSuccess &&
+         cudaDeviceSynchronize() == cudaSuccess;
+    if (!ok) return cleanup_fail(fail(nullptr, ORL_E_CUDA, "device init failed"));
+    if (world > 1) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof uid);
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, world, uid, rank);
+        if (r != ncclSuccess)
+            return cleanup_fail(fail(nullptr, ORL_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    }
+    *out = ctx;
+    return ORL_OK;
+}
+
+extern "C" orl_status orl_destroy(orl_ctx *ctx) {
+    if (!ctx) return ORL_OK;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    cudaFree(ctx->d_acc);
+    cudaFree(ctx->d_err);
+    cudaFree(ctx->d_ws);
+    cudaFree(ctx->d_ticket);
+    cudaFree(ctx->d_seq_part);
+    cudaFree(ctx->d_gather_w);
+    cudaFree(ctx->d_whiten);
+    cudaFree(ctx->d_flags);
+    cudaFree(ctx->d_gather_s);
+    cudaFree(ctx->d_stats);
+    if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
+    delete ctx;
+    return ORL_OK;
+}
+
+extern "C" const char *orl_last_error(const orl_ctx *ctx) {
+    return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+extern "C" uint64_t orl_launch_count(const orl_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" orl_status orl_begin_iteration(orl_ctx *ctx, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_acc, 0, 16 * sizeof(double), s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_err, 0, kNumErr * sizeof(unsigned long long), s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_whiten, 0, 4 * sizeof(double), s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(double), s));
+    ctx->have_adv = ctx->have_whiten = false;
+    ctx->imported_w = ctx->imported_s = 0;
+    return ORL_OK;
+}
+
+// ------------------------------------------------------------------ S1 (+S2/S3)
+extern "C" orl_status orl_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_logits *logits,
+                                   float inv_temp, float *logp, float *entropy, float *lse,
+                                   float *gathered, const float *partner_logp, int kl_est,
+                                   double beta_reward, const float *seq_reward, float *kl,
+                                   float *shaped_reward, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    orl_status st = validate_rows_logits(ctx, rows, logits, inv_temp);
+    if (st) return st;
+    if (!logp) return fail(ctx, ORL_E_INVALID_ARG, "logp is required");
+    if (!aligned4(logp) || !aligned4(entropy) || !aligned4(lse) || !aligned4(gathered) ||
+        !aligned4(partner_logp) || !aligned4(seq_reward) || !aligned4(kl) || !aligned4(shaped_reward))
+        return fail(ctx, ORL_E_ALIGN, "per-token arrays must be 4-byte aligned");
+    if ((kl || shaped_reward) && !partner_logp)
+        return fail(ctx, ORL_E_INVALID_ARG, "kl/shaped_reward need partner_logp");
+    if (partner_logp && (kl_est < 1 || kl_est > 3))
+        return fail(ctx, ORL_E_INVALID_ARG, "kl_est=%d not in {1,2,3}", kl_est);
+    if (shaped_reward && !seq_reward) return fail(ctx, ORL_E_INVALID_ARG, "shaped_reward needs seq_reward");
+    if (!std::isfinite(beta_reward)) return fail(ctx, ORL_E_INVALID_ARG, "beta_reward not finite");
+    if ((st = set_device(ctx))) return st;
+    K1Params p;
+    fill_common(ctx, p, rows, logits, inv_temp);
+    p.logp = logp;
+    p.entropy = entropy;
+    p.lse = lse;
+    p.gathered = gathered;
+    p.partner = partner_logp;
+    p.kl_est = kl_est;
+    p.beta_reward = beta_reward;
+    p.seq_reward = seq_reward;
+    p.kl_out = kl;
+    p.shaped = shaped_reward;
+    CUDA_TRY(ctx, launch_k1(p, tma_eligible(logits), kModeLogprob, ctx->num_sms, as_stream(stream)));
+    ctx->launches += 1;
+    return ORL_OK;
+}
+
+// ------------------------------------------------------------------ S4/S4'/S5
+extern "C" orl_status orl_advantages(orl_ctx *ctx, int64_t B, int64_t T, const int32_t *lengths,
+                                     int kind, double gamma, double lambda, int group_size,
+                                     const float *shaped_reward, const float *values,
+                                     const float *seq_reward, float *adv, float *ret,
+                                     uint8_t *group_keep, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (B < 1 || B > (1 << 24) || T < 1 || B * T >= ((int64_t)1 << 40))
+        return fail(ctx, ORL_E_SHAPE, "B=%lld T=%lld invalid", (long long)B, (long long)T);
+    if (kind < ORL_ADV_GAE || kind > ORL_ADV_RPP_BASELINE)
+        return fail(ctx, ORL_E_INVALID_ARG, "unknown advantage kind %d", kind);
+    if (!lengths || !adv) return fail(ctx, ORL_E_INVALID_ARG, "lengths and adv are required");
+    if (!(gamma >= 0.0 && gamma <= 1.0) || !(lambda >= 0.0 && lambda <= 1.0))
+        return fail(ctx, ORL_E_INVALID_ARG, "gamma=%g lambda=%g must be in [0,1]", gamma, lambda);
+    const bool grouped = kind == ORL_ADV_GRPO || kind == ORL_ADV_RPP_BASELINE;
+    if (kind == ORL_ADV_GAE && (!shaped_reward || !values))
+        return fail(ctx, ORL_E_INVALID_ARG, "GAE needs shaped_reward and values");
+    if ((kind == ORL_ADV_RPP || kind == ORL_ADV_RPP_BASELINE) && !shaped_reward)
+        return fail(ctx, ORL_E_INVALID_ARG, "REINFORCE++ needs shaped_reward");
+    if (grouped && !seq_reward) return fail(ctx, ORL_E_INVALID_ARG, "group advantages need seq_reward");
+    if (grouped && (group_size < 1 || B % group_size != 0))
+        return fail(ctx, ORL_E_GROUP_SPLIT, "B=%lld is not a multiple of group_size=%d", (long long)B, group_size);
+    if (!aligned4(lengths) || !aligned4(shaped_reward) || !aligned4(values) || !aligned4(seq_reward) ||
+        !aligned4(adv) || !aligned4(ret))
+        return fail(ctx, ORL_E_ALIGN, "per-token arrays must be 4-byte aligned");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    if (B > ctx->seq_cap) {
+        cudaFree(ctx->d_seq_part);
+        ctx->d_seq_part = nullptr;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->d_seq_part, (size_t)B * 3 * sizeof(double)));
+        ctx->seq_cap = B;
+    }
+    K3Params p;
+    std::memset(&p, 0, sizeof p);
+    p.B = (int)B;
+    p.T = (int)T;
+    p.kind = kind;
+    p.G = grouped ? group_size : 1;
+    p.gamma = gamma;
+    p.lambda = lambda;
+    p.lengths = lengths;
+    p.shaped = shaped_reward;
+    p.values = values;
+    p.seq_reward = seq_reward;
+    p.adv = adv;
+    p.ret = ret;
+    p.keep = grouped ? group_keep : nullptr;
+    p.seq_part = ctx->d_seq_part;
+    p.err = ctx->d_err;
+    CUDA_TRY(ctx, launch_k3(p, as_stream(stream)));
+    ctx->launches += 1;
+    ctx->adv_B = B;
+    ctx->have_adv = true;
+    ctx->have_whiten = false;
+    return ORL_OK;
+}
+
+// ------------------------------------------------------------------ S6 + C1
+extern "C" orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (!ctx->have_adv && !ctx->imported_w)
+        return fail(ctx, ORL_E_STATE, "orl_whiten_stats before orl_advantages");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    int world = ctx->world;
+    if (ctx->imported_w) {
+        world = ctx->imported_w;
+    } else {
+        CUDA_TRY(ctx, launch_whiten_local(ctx->d_seq_part, (int)ctx->adv_B, ctx->d_gather_w + 4 * ctx->rank, s));
+        ctx->launches += 1;
+        if (ctx->world > 1) {
+            NCCL_TRY(ctx, ncclAllGather(ctx->d_gather_w + 4 * ctx->rank, ctx->d_gather_w, 4, ncclDouble,
+                                        ctx->comm, s));
+        }
+    }
+    CUDA_TRY(ctx, launch_whiten_merge(ctx->d_gather_w, world, whiten ? 1 : 0, ctx->d_whiten, ctx->d_flags, s));
+    ctx->launches += 1;
+    ctx->imported_w = 0;
+    ctx->have_whiten = true;
+    return ORL_OK;
+}
+
+// ------------------------------------------------------------------ S1 + S7..S9
+extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
+                                   float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
+                                   const float *logp_ref, const float *adv, const float *ret,
+                                   const float *v_new, const float *v_old, float *logp_new,
+                                   float *entropy, float *dloss_dlogp, float *dloss_dv, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    orl_status st = validate_rows_logits(ctx, rows, actor, inv_temp);
+    if (st) return st;
+    if (!cfg || !logp_old || !adv || !logp_new)
+        return fail(ctx, ORL_E_INVALID_ARG, "cfg, logp_old, adv and logp_new are required");
+    const int critic = (ret != nullptr) + (v_new != nullptr) + (v_old != nullptr);
+    if (critic != 0 && critic != 3) return fail(ctx, ORL_E_INVALID_ARG, "ret, v_new, v_old go together");
+    if (dloss_dv && critic == 0) return fail(ctx, ORL_E_INVALID_ARG, "dloss_dv needs the critic arrays");
+    if (!aligned4(logp_old) || !aligned4(logp_ref) || !aligned4(adv) || !aligned4(ret) || !aligned4(v_new) ||
+        !aligned4(v_old) || !aligned4(logp_new) || !aligned4(entropy) || !aligned4(dloss_dlogp) ||
+        !aligned4(dloss_dv))
+        return fail(ctx, ORL_E_ALIGN, "per-token arrays must be 4-byte aligned");
+    if (!(cfg->eps_low >= 0.0 && cfg->eps_low < 1.0) || !(cfg->eps_high >= 0.0) ||
+        !std::isfinite(cfg->eps_high) || !std::isfinite(cfg->eps_value) || !std::isfinite(cfg->c1) ||
+        !std::isfinite(cfg->c2) || !std::isfinite(cfg->beta_loss) || !(cfg->ratio_guard > 0.0))
+        return fail(ctx, ORL_E_INVALID_ARG, "invalid orl_ppo_cfg values");
+    if (cfg->kl_loss_est < 1 || cfg->kl_loss_est > 3)
+        return fail(ctx, ORL_E_INVALID_ARG, "kl_loss_est=%d not in {1,2,3}", cfg->kl_loss_est);
+    if (cfg->kl_in_loss && !logp_ref) return fail(ctx, ORL_E_INVALID_ARG, "kl_in_loss needs logp_ref");
+    if (!ctx->have_whiten) return fail(ctx, ORL_E_STATE, "orl_ppo_loss before orl_whiten_stats");
+    if ((st = set_device(ctx))) return st;
+    K1Params p;
+    fill_common(ctx, p, rows, actor, inv_temp);
+    p.logp = logp_new;
+    p.entropy = entropy;
+    p.logp_old = logp_old;
+    p.logp_ref = logp_ref;
+    p.adv = adv;
+    p.ret = ret;
+    p.v_new = v_new;
+    p.v_old = v_old;
+    p.dlogp = dloss_dlogp;
+    p.dv = dloss_dv;
+    p.eps_low = cfg->eps_low;
+    p.eps_high = cfg->eps_high;
+    p.eps_v = cfg->eps_value;
+    p.c1 = cfg->c1;
+    p.beta_loss = cfg->beta_loss;
+    p.ratio_guard = cfg->ratio_guard;
+    p.kl_loss_est = cfg->kl_loss_est;
+    p.kl_in_loss = cfg->kl_in_loss;
+    CUDA_TRY(ctx, launch_k1(p, tma_eligible(actor), kModeLoss, ctx->num_sms, as_stream(stream)));
+    ctx->launches += 1;
+    return ORL_OK;
+}
+
+// ------------------------------------------------------------------ S10 + C2
+extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
+                                   double *dev_out, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (!cfg) return fail(ctx, ORL_E_INVALID_ARG, "cfg is NULL");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    int world = ctx->world;
+    if (ctx->imported_s) {
+        world = ctx->imported_s;
+    } else {
+        CUDA_TRY(ctx, launch_stats_pack(ctx->d_acc, ctx->d_err, ctx->d_gather_s + kStatsSlots * ctx->rank, s));
+        ctx->launches += 1;
+        if (ctx->world > 1)
+            NCCL_TRY(ctx, ncclAllGather(ctx->d_gather_s + kStatsSlots * ctx->rank, ctx->d_gather_s,
+                                        kStatsSlots, ncclDouble, ctx->comm, s));
+    }
+    CUDA_TRY(ctx, launch_stats_final(ctx->d_gather_s, world, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
+                                     cfg->beta_loss, cfg->kl_in_loss, ctx->d_stats, s));
+    ctx->launches += 1;
+    ctx->imported_s = 0;
+    if (dev_out)
+        CUDA_TRY(ctx, cudaMemcpyAsync(dev_out, ctx->d_stats, kStatsSlots * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, kStatsSlots * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats + kStatsSlots, ctx->d_flags, 4 * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    const double *h = ctx->h_stats;
+    if (host_out) {
+        host_out->n_tokens = h[0];
+        host_out->policy_loss = h[1];
+        host_out->value_loss = h[2];
+        host_out->entropy = h[3];
+        host_out->kl = h[4];
+        host_out->approx_kl_old = h[5];
+        host_out->clip_frac = h[6];
+        host_out->value_clip_frac = h[7];
+        host_out->ratio_mean = h[8];
+        host_out->total_loss = h[9];
+        host_out->adv_mean = h[10];
+        host_out->adv_std = h[11];
+        host_out->n_guard = (int64_t)h[12];
+        host_out->n_nonfinite = (int64_t)h[13];
+        host_out->n_token_range = (int64_t)h[14];
+        host_out->whiten_warn = h[15] != 0.0;
+        host_out->pad_ = 0;
+    }
+    const double mask_err = h[kStatsSlots + 1];
+    if (h[14] > 0) return fail(ctx, ORL_E_TOKEN_RANGE, "%lld token(s) outside [0, V)", (long long)h[14]);
+    if (mask_err > 0) return fail(ctx, ORL_E_MASK, "%lld invalid length(s)", (long long)mask_err);
+    if (h[13] > 0) return fail(ctx, ORL_E_NONFINITE, "%lld non-finite value(s)", (long long)h[13]);
+    if (h[12] > 0)
+        return fail(ctx, ORL_E_NUMERIC_GUARD, "%lld token(s) with |logp_new - logp_old| > %g", (long long)h[12],
+                    cfg->ratio_guard);
+    if (!(h[0] > 0)) return fail(ctx, ORL_E_EMPTY_BATCH, "no valid tokens");
+    return ORL_OK;
+}
+
+// ------------------------------------------------------------------ hooks
+extern "C" orl_status orl_export_partials(orl_ctx *ctx, int which, double *host_out, void *stream) {
+    if (!ctx || !host_out) return fail(ctx, ORL_E_INVALID_ARG, "ctx/host_out is NULL");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    if (which == 0) {
+        if (!ctx->have_adv) return fail(ctx, ORL_E_STATE, "export of whitening partial before orl_advantages");
+        double *slot = ctx->d_gather_w + 4 * ctx->rank;
+        CUDA_TRY(ctx, launch_whiten_local(ctx->d_seq_part, (int)ctx->adv_B, slot, s));
+        ctx->launches += 1;
+        CUDA_TRY(ctx, cudaMemcpyAsync(host_out, slot, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    } else if (which == 1) {
+        double *slot = ctx->d_gather_s + kStatsSlots * ctx->rank;
+        CUDA_TRY(ctx, launch_stats_pack(ctx->d_acc, ctx->d_err, slot, s));
+        ctx->launches += 1;
+        CUDA_TRY(ctx, cudaMemcpyAsync(host_out, slot, kStatsSlots * sizeof(double), cudaMemcpyDeviceToHost, s));
+    } else {
+        return fail(ctx, ORL_E_INVALID_ARG, "which=%d not in {0,1}", which);
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    return ORL_OK;
+}
+
+extern "C" orl_status orl_import_partials(orl_ctx *ctx, int which, const double *host_all, int world,
+                                          void *stream) {
+    if (!ctx || !host_all) return fail(ctx, ORL_E_INVALID_ARG, "ctx/host_all is NULL");
+    if (world < 1 || world > kMaxWorld) return fail(ctx, ORL_E_INVALID_ARG, "world=%d invalid", world);
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    if (which == 0) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_gather_w, host_all, (size_t)world * 4 * sizeof(double),
+                                      cudaMemcpyHostToDevice, s));
+        ctx->imported_w = world;
+    } else if (which == 1) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->d_gather_s, host_all, (size_t)world * kStatsSlots * sizeof(double),
+                                      cudaMemcpyHostToDevice, s));
+        ctx->imported_s = world;
+    } else {
+        return fail(ctx, ORL_E_INVALID_ARG, "which=%d not in {0,1}", which);
+    }
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    return ORL_OK;
+}

@@ -1,0 +1,89 @@
+// orl_internal.h -- host/device contract between the C-ABI layer (orl_api.cu)
+// and the kernels (k1_logprobs.cu, k3_advantages.cu, k6_stats.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace orl {
+
+// K1 modes: S1 (+ the S2/S3 reward epilogue when `partner` is set) or the
+// actor pass with the S7-S9 loss epilogue.
+enum K1Mode { kModeLogprob = 0, kModeLoss = 1 };
+
+// Loss-partial vector (fp64), one per CTA and per context accumulator:
+//  0 n  1 sum obj  2 sum vl  3 sum H  4 sum k(new,ref)  5 n clipped
+//  6 n value-clipped  7 sum k3(old-new)  8 sum rho  9 n guard
+//  10 n non-finite loss terms  11 unused
+constexpr int kNumPartials = 12;
+// Device error counters (uint64): 0 token out of range, 1 non-finite S1 rows,
+// 2 invalid lengths (L_b < 0 or > T).
+constexpr int kNumErr = 4;
+
+struct K1Params {
+    const char *base;  // logits of the micro-batch's first sequence
+    int64_t V, stride_b, stride_t;  // elements
+    int64_t row_bytes;
+    int elt;            // 2 (bf16) or 4 (fp32)
+    float inv_temp;
+    float c2;           // inv_temp * log2(e)
+    int B, T;
+    int64_t seq_offset;
+    const int32_t *tokens, *lengths;
+    float *logp, *entropy, *lse, *gathered;
+    // S2+S3 reward epilogue (reference pass)
+    const float *partner;
+    int kl_est;
+    double beta_reward;
+    const float *seq_reward;
+    float *kl_out, *shaped;
+    // S7-S9 loss epilogue (actor pass)
+    const float *logp_old, *logp_ref, *adv, *ret, *v_new, *v_old;
+    float *dlogp, *dv;
+    double eps_low, eps_high, eps_v, c1, beta_loss, ratio_guard;
+    int kl_loss_est, kl_in_loss;
+    const double *whiten;  // device [4]: N_global, mu, sigma, apply
+    // accounting
+    double *ws;            // [kNumPartials][ws_stride] per-CTA partials
+    int ws_stride;
+    unsigned int *ticket;  // last-CTA ticket (self-resetting)
+    double *acc;           // [kNumPartials] context accumulator
+    unsigned long long *err;  // [kNumErr]
+};
+
+// Launch K1.  Returns the CUDA launch error.  `tma` selects the TMA bulk-copy
+// kernel (requires 16-byte aligned rows and row_bytes % 16 == 0).
+cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaStream_t s);
+// Shared-memory footprint of the TMA kernel for B sequences.
+size_t k1_tma_smem_bytes(int B);
+
+struct K3Params {
+    int B, T, kind, G;
+    double gamma, lambda;
+    const int32_t *lengths;
+    const float *shaped, *values, *seq_reward;
+    float *adv, *ret;
+    uint8_t *keep;
+    double *seq_part;  // [B][3]: n_b, mean_b, M2_b of the stored fp32 advantages
+    unsigned long long *err;
+};
+cudaError_t launch_k3(const K3Params &p, cudaStream_t s);
+
+// Whitening: merge per-sequence partials [B][3] in order into the rank partial
+// (count, mean, M2) -> gather[rank*4 ...].
+cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_slot, cudaStream_t s);
+// Merge gathered [world][4] rank partials in rank order -> whiten[4] =
+// {N, mu, sigma, apply}; warn flag into flags[0].
+cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten, double *whiten,
+                                double *flags, cudaStream_t s);
+
+// Fold the error counters into the loss accumulator copy for the collective:
+// out[kStatsSlots] = acc[0..11], err -> slots 12..14.
+constexpr int kStatsSlots = 16;
+cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, double *out,
+                              cudaStream_t s);
+// Sum gathered [world][16] in rank order and form the stats vector.
+cudaError_t launch_stats_final(const double *gather, int world, const double *whiten,
+                               const double *flags, double c1, double c2, double beta_loss,
+                               int kl_in_loss, double *stats_out, cudaStream_t s);
+
+}  // namespace orl

@@ -1,0 +1,250 @@
+"""Thin ctypes binding of liborl.so (include/orl.h).
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of
+liborl.so.  Functions carry the C names (orl_logprobs, orl_advantages, ...)
+and take torch CUDA tensors (PyTorch is used for device memory and streams).
+Importing this module fails loudly if liborl.so is missing: there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liborl.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2405_11143_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+_lib = ctypes.CDLL(LIB_PATH)
+
+UNIQUE_ID_BYTES = 128
+STATS_N = 16
+MAX_SEQ_PER_CALL = 8192
+
+STATUS = {0: "ORL_OK", 1: "ORL_E_INVALID_ARG", 2: "ORL_E_SHAPE", 3: "ORL_E_ALIGN", 4: "ORL_E_DTYPE",
+          5: "ORL_E_TOKEN_RANGE", 6: "ORL_E_MASK", 7: "ORL_E_NONFINITE", 8: "ORL_E_NUMERIC_GUARD",
+          9: "ORL_E_EMPTY_BATCH", 10: "ORL_E_GROUP_SPLIT", 11: "ORL_E_CUDA", 12: "ORL_E_NCCL",
+          13: "ORL_E_STATE"}
+ST = {v: k for k, v in STATUS.items()}
+DTYPE = {torch.bfloat16: 0, torch.float32: 1}
+KL = {"k1": 1, "k2": 2, "k3": 3}
+ADV = {"gae": 0, "grpo": 1, "rpp": 2, "rpp_baseline": 3}
+
+
+class Logits(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("V", ctypes.c_int64), ("stride_b", ctypes.c_int64), ("stride_t", ctypes.c_int64)]
+
+
+class Rows(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("seq_offset", ctypes.c_int64),
+                ("tokens", ctypes.c_void_p), ("lengths", ctypes.c_void_p)]
+
+
+class PpoCfg(ctypes.Structure):
+    _fields_ = [("eps_low", ctypes.c_double), ("eps_high", ctypes.c_double),
+                ("eps_value", ctypes.c_double), ("c1", ctypes.c_double), ("c2", ctypes.c_double),
+                ("beta_loss", ctypes.c_double), ("kl_loss_est", ctypes.c_int32),
+                ("kl_in_loss", ctypes.c_int32), ("ratio_guard", ctypes.c_double)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in (
+        "n_tokens", "policy_loss", "value_loss", "entropy", "kl", "approx_kl_old", "clip_frac",
+        "value_clip_frac", "ratio_mean", "total_loss", "adv_mean", "adv_std")] + [
+        ("n_guard", ctypes.c_int64), ("n_nonfinite", ctypes.c_int64), ("n_token_range", ctypes.c_int64),
+        ("whiten_warn", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "pad_"}
+
+
+_P, _I64, _I32, _F32, _F64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float, ctypes.c_double
+_lib.orl_version.restype = ctypes.c_int
+_lib.orl_get_unique_id.argtypes = [ctypes.c_char_p]
+_lib.orl_create.argtypes = [_I32, _I32, _I32, ctypes.c_char_p, ctypes.POINTER(_P)]
+_lib.orl_destroy.argtypes = [_P]
+_lib.orl_last_error.argtypes = [_P]
+_lib.orl_last_error.restype = ctypes.c_char_p
+_lib.orl_launch_count.argtypes = [_P]
+_lib.orl_launch_count.restype = ctypes.c_uint64
+_lib.orl_begin_iteration.argtypes = [_P, _P]
+_lib.orl_logprobs.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32, _P, _P, _P, _P,
+                              _P, _I32, _F64, _P, _P, _P, _P]
+_lib.orl_advantages.argtypes = [_P, _I64, _I64, _P, _I32, _F64, _F64, _I32, _P, _P, _P, _P, _P, _P, _P]
+_lib.orl_whiten_stats.argtypes = [_P, _I32, _P]
+_lib.orl_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
+                              ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+_lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
+_lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
+_lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
+for _f in ("orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
+           "orl_advantages", "orl_whiten_stats", "orl_ppo_loss", "orl_finalize",
+           "orl_export_partials", "orl_import_partials"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+
+class OrlError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class PPOConfig:
+    eps_low: float = 0.2
+    eps_high: float = 0.2
+    eps_value: float = 0.2
+    c1: float = 0.5
+    c2: float = 0.0
+    beta_loss: float = 0.0
+    kl_loss_est: str = "k2"
+    kl_in_loss: bool = False
+    ratio_guard: float = 30.0
+
+    def c(self) -> PpoCfg:
+        return PpoCfg(self.eps_low, self.eps_high, self.eps_value, self.c1, self.c2, self.beta_loss,
+                      KL[self.kl_loss_est], int(bool(self.kl_in_loss)), self.ratio_guard)
+
+
+def version() -> int:
+    return _lib.orl_version()
+
+
+def orl_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
+    st = _lib.orl_get_unique_id(buf)
+    if st:
+        raise OrlError(st, _lib.orl_last_error(None).decode())
+    return buf.raw
+
+
+class Context:
+    """Owns an orl_ctx (NCCL communicator, fp64 accumulators, error counters)."""
+
+    def __init__(self, device: int = 0, world: int = 1, rank: int = 0, unique_id: bytes | None = None):
+        h = ctypes.c_void_p()
+        st = _lib.orl_create(int(device), int(world), int(rank), unique_id, ctypes.byref(h))
+        if st:
+            raise OrlError(st, _lib.orl_last_error(None).decode())
+        self.h, self.device, self.world, self.rank = h, device, world, rank
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.orl_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st: int, allow=()):
+        if st and st not in allow:
+            raise OrlError(st, _lib.orl_last_error(self.h).decode())
+        return st
+
+    @property
+    def launch_count(self) -> int:
+        return int(_lib.orl_launch_count(self.h))
+
+
+# ----------------------------------------------------------------------------- C-named calls
+def _rows(tokens, lengths, B, T, seq_offset):
+    return Rows(int(B), int(T), int(seq_offset), tokens.data_ptr(), lengths.data_ptr())
+
+
+def _logits(x):
+    if x.dtype not in DTYPE:
+        raise TypeError(f"logits dtype {x.dtype} (bf16 or fp32 expected)")
+    if x.dim() != 3 or x.stride(2) != 1:
+        raise ValueError("logits must be a [B,T,V] view with unit stride along V")
+    return Logits(x.data_ptr(), DTYPE[x.dtype], 0, x.shape[2], x.stride(0), x.stride(1))
+
+
+def orl_begin_iteration(ctx: Context, stream=None):
+    return ctx.check(_lib.orl_begin_iteration(ctx.h, _stream(stream)))
+
+
+def orl_logprobs(ctx: Context, tokens, lengths, logits, logp, *, seq_offset=0, inv_temp=1.0,
+                 entropy=None, lse=None, gathered=None, partner_logp=None, kl_est="k1",
+                 beta_reward=0.0, seq_reward=None, kl=None, shaped_reward=None, stream=None):
+    """S1 (+S2/S3 with partner_logp) on the micro-batch logits[0:B] = sequences
+    [seq_offset, seq_offset+B) of the rank batch; per-token arrays are [B_total, T]."""
+    B, T = logits.shape[0], tokens.shape[1]
+    rows, lg = _rows(tokens, lengths, B, T, seq_offset), _logits(logits)
+    st = _lib.orl_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), _ptr(logp),
+                           _ptr(entropy), _ptr(lse), _ptr(gathered), _ptr(partner_logp),
+                           KL.get(kl_est, kl_est), float(beta_reward), _ptr(seq_reward), _ptr(kl),
+                           _ptr(shaped_reward), _stream(stream))
+    return ctx.check(st)
+
+
+def orl_advantages(ctx: Context, lengths, adv, *, kind="gae", gamma=1.0, lam=0.95, group_size=1,
+                   shaped_reward=None, values=None, seq_reward=None, ret=None, group_keep=None,
+                   stream=None):
+    B, T = adv.shape
+    st = _lib.orl_advantages(ctx.h, B, T, _ptr(lengths), ADV.get(kind, kind), float(gamma), float(lam),
+                             int(group_size), _ptr(shaped_reward), _ptr(values), _ptr(seq_reward),
+                             _ptr(adv), _ptr(ret), _ptr(group_keep), _stream(stream))
+    return ctx.check(st)
+
+
+def orl_whiten_stats(ctx: Context, whiten: bool, stream=None):
+    return ctx.check(_lib.orl_whiten_stats(ctx.h, int(bool(whiten)), _stream(stream)))
+
+
+def orl_ppo_loss(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
+                 seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
+                 entropy=None, dloss_dlogp=None, dloss_dv=None, stream=None):
+    B, T = logits.shape[0], tokens.shape[1]
+    rows, lg, c = _rows(tokens, lengths, B, T, seq_offset), _logits(logits), cfg.c()
+    st = _lib.orl_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
+                           _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
+                           _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(dloss_dlogp),
+                           _ptr(dloss_dv), _stream(stream))
+    return ctx.check(st)
+
+
+DATA_ERRORS = (ST["ORL_E_TOKEN_RANGE"], ST["ORL_E_MASK"], ST["ORL_E_NONFINITE"],
+               ST["ORL_E_NUMERIC_GUARD"], ST["ORL_E_EMPTY_BATCH"])
+
+
+def orl_finalize(ctx: Context, cfg: PPOConfig, dev_out=None, stream=None, raise_on_data_error=False):
+    """Returns (status_name, stats dict).  Data errors are returned, not raised,
+    unless raise_on_data_error."""
+    out, c = Stats(), cfg.c()
+    st = _lib.orl_finalize(ctx.h, ctypes.byref(c), ctypes.byref(out), _ptr(dev_out), _stream(stream))
+    ctx.check(st, allow=() if raise_on_data_error else DATA_ERRORS)
+    return STATUS[st], out.as_dict()
+
+
+def orl_export_partials(ctx: Context, which: int, stream=None):
+    import numpy as np
+    n = 4 if which == 0 else STATS_N
+    buf = np.zeros(n, dtype=np.float64)
+    ctx.check(_lib.orl_export_partials(ctx.h, int(which), buf.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
+    return buf
+
+
+def orl_import_partials(ctx: Context, which: int, host_all, stream=None):
+    import numpy as np
+    arr = np.ascontiguousarray(host_all, dtype=np.float64)
+    world = arr.shape[0]
+    ctx.check(_lib.orl_import_partials(ctx.h, int(which), arr.ctypes.data_as(ctypes.c_void_p), world,
+                                       _stream(stream)))

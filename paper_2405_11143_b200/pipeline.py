@@ -1,0 +1,113 @@
+"""Host orchestration of one PPO/RLVR iteration on one rank through liborl.
+
+Call order follows PAPER.md App. C: old-policy log-probs
+ -> reference log-probs + KL-shaped reward -> advantages
+ -> global normalisation (collective C1) -> actor pass with the
+PPO loss -> statistics (collective C2).  Only launches and buffer
+bookkeeping live here; the arithmetic is in liborl.so.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import torch
+
+from . import orl as _orl
+
+
+@dataclass
+class PathConfig:
+    adv_kind: str = "gae"
+    gamma: float = 1.0
+    lam: float = 0.95
+    group_size: int = 1
+    whiten: bool = True
+    kl_mode: str = "reward"          # "reward": beta k(old,ref) shapes r'; "loss": beta k(new,ref) in the loss
+    kl_est_reward: str = "k1"
+    beta_reward: float = 0.01
+    inv_temp: float = 1.0
+    use_ref: bool = True
+    ppo: _orl.PPOConfig = field(default_factory=_orl.PPOConfig)
+
+    @classmethod
+    def from_synth(cls, c: dict) -> "PathConfig":
+        kl_mode = c.get("kl_mode", "reward")
+        return cls(adv_kind=c["adv_kind"], gamma=c["gamma"], lam=c["lam"], group_size=c.get("group_size", 1),
+                   whiten=c["whiten"], kl_mode=kl_mode, kl_est_reward=c.get("kl_est_reward", "k1"),
+                   beta_reward=c.get("beta_reward", 0.0) if kl_mode == "reward" else 0.0,
+                   ppo=_orl.PPOConfig(eps_low=c["eps_low"], eps_high=c["eps_high"], eps_value=c["eps_v"],
+                                      c1=c["c1"], c2=c["c2"], beta_loss=c.get("beta_loss", 0.0),
+                                      kl_loss_est=c.get("kl_est_loss", "k2"), kl_in_loss=kl_mode == "loss"))
+
+    @property
+    def critic(self) -> bool:
+        return self.adv_kind == "gae"
+
+
+class Buffers:
+    """Per-token [B,T] fp32 outputs of the rank-local batch (device)."""
+
+    def __init__(self, B: int, T: int, device, group_size: int = 1, grads: bool = True):
+        f = lambda: torch.zeros(B, T, dtype=torch.float32, device=device)  # noqa: E731
+        self.logp_old, self.logp_ref, self.kl, self.shaped = f(), f(), f(), f()
+        self.adv, self.ret, self.logp_new, self.entropy = f(), f(), f(), f()
+        self.dlogp = f() if grads else None
+        self.dv = f() if grads else None
+        self.keep = torch.zeros(max(1, B // max(1, group_size)), dtype=torch.uint8, device=device)
+        self.stats_dev = torch.zeros(_orl.STATS_N, dtype=torch.float64, device=device)
+
+
+LogitsSource = Callable[[str, int, int], torch.Tensor]   # (role, seq_start, seq_end) -> [e-s, T, V]
+
+
+def microbatches(B: int, mb: int):
+    return [(s, min(B, s + mb)) for s in range(0, B, mb)]
+
+
+def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers, logits: LogitsSource,
+                  mb: int, stream: Optional[torch.cuda.Stream] = None, finalize: bool = True,
+                  on_k1: Optional[Callable[[str], object]] = None):
+    """One iteration on this rank.  `batch` holds device tensors tokens [B,T] int32,
+    lengths [B] int32, seq_reward [B] f32 and (critic) values_old / values_new [B,T].
+    `on_k1(tag)` (optional) is called around every K1 launch for timing hooks."""
+    tok, L = batch["tokens"], batch["lengths"]
+    B, T = tok.shape
+    mbs = microbatches(B, mb)
+    hook = on_k1 or (lambda tag: None)
+    _orl.orl_begin_iteration(ctx, stream)
+    for s, e in mbs:                                   # S1, old policy
+        h = hook("old")
+        _orl.orl_logprobs(ctx, tok, L, logits("old", s, e), bufs.logp_old, seq_offset=s,
+                          inv_temp=cfg.inv_temp, stream=stream)
+        if h: h()
+    if cfg.use_ref:
+        for s, e in mbs:                               # S1+S2+S3, reference
+            h = hook("ref")
+            _orl.orl_logprobs(ctx, tok, L, logits("ref", s, e), bufs.logp_ref, seq_offset=s,
+                              inv_temp=cfg.inv_temp, partner_logp=bufs.logp_old, kl_est=cfg.kl_est_reward,
+                              beta_reward=cfg.beta_reward if cfg.kl_mode == "reward" else 0.0,
+                              seq_reward=batch["seq_reward"], kl=bufs.kl, shaped_reward=bufs.shaped,
+                              stream=stream)
+            if h: h()
+    else:
+        raise NotImplementedError("the paper's PPO loop always has a reference model (P:193)")
+    _orl.orl_advantages(ctx, L, bufs.adv, kind=cfg.adv_kind, gamma=cfg.gamma, lam=cfg.lam,   # S4/S4'/S5
+                        group_size=cfg.group_size, shaped_reward=bufs.shaped,
+                        values=batch.get("values_old") if cfg.critic else None,
+                        seq_reward=batch["seq_reward"], ret=bufs.ret,
+                        group_keep=bufs.keep if cfg.adv_kind in ("grpo", "rpp_baseline") else None,
+                        stream=stream)
+    _orl.orl_whiten_stats(ctx, cfg.whiten and cfg.adv_kind != "grpo", stream)         # S6 + C1
+    critic = cfg.critic and batch.get("values_new") is not None
+    for s, e in mbs:                                   # S1 + S7..S9, actor
+        h = hook("new")
+        _orl.orl_ppo_loss(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.logp_old, bufs.adv, bufs.logp_new,
+                          seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
+                          ret=bufs.ret if critic else None, v_new=batch["values_new"] if critic else None,
+                          v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
+                          dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None, stream=stream)
+        if h: h()
+    if not finalize:
+        return None
+    return _orl.orl_finalize(ctx, cfg.ppo, dev_out=bufs.stats_dev, stream=stream)  # S10 + C2

@@ -1,0 +1,98 @@
+"""CPU checks of the C-ABI boundary: liborl.so builds for sm_100a, loads, exports
+every entry point include/orl.h declares, the ctypes structs match the C
+layouts, host-side argument validation works without a GPU, and the product
+never links or imports the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "orl.h")
+PKG = os.path.join(ROOT, "paper_2405_11143_b200")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2405_11143_b200 import build
+
+    path = build.build()
+    return ctypes.CDLL(path), path
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:orl_status|int|const char \*|uint64_t)\s*\**\s*(orl_\w+)\s*\(",
+                                 text, re.M)))
+
+
+def test_header_declares_the_survey_calls():
+    names = declared_functions()
+    for n in ("orl_get_unique_id", "orl_create", "orl_destroy", "orl_last_error", "orl_logprobs",
+              "orl_advantages", "orl_whiten_stats", "orl_ppo_loss", "orl_finalize"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    so, path = lib
+    names = declared_functions()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(so, n), f"{n} not exported by {path}"
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (orl_\w+)", out))
+    assert set(names) <= exported
+    assert "oracle_" not in out, "liborl.so must not contain oracle code"
+
+
+def test_library_is_sm100a(lib):
+    _, path = lib
+    out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+    assert "UBLKCP" in sass or "UTMALDG" in sass, "TMA bulk copies missing from SASS"
+    assert "FFMA2" in sass and "MUFU.EX2" in sass
+
+
+def test_struct_layouts_match_c(lib, tmp_path):
+    from paper_2405_11143_b200 import orl
+    src = tmp_path / "sz.c"
+    src.write_text('#include "orl.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(void){'
+                   'printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(orl_logits), sizeof(orl_rows), sizeof(orl_ppo_cfg),'
+                   ' sizeof(orl_stats), offsetof(orl_ppo_cfg, kl_loss_est), offsetof(orl_stats, n_guard),'
+                   ' offsetof(orl_ppo_cfg, ratio_guard));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    want = [ctypes.sizeof(orl.Logits), ctypes.sizeof(orl.Rows), ctypes.sizeof(orl.PpoCfg),
+            ctypes.sizeof(orl.Stats), orl.PpoCfg.kl_loss_est.offset, orl.Stats.n_guard.offset,
+            orl.PpoCfg.ratio_guard.offset]
+    assert got == want
+
+
+def test_host_validation_without_gpu(lib):
+    so, _ = lib
+    so.orl_last_error.restype = ctypes.c_char_p
+    so.orl_last_error.argtypes = [ctypes.c_void_p]
+    assert so.orl_version() == 1
+    assert so.orl_begin_iteration(None, None) == 1          # ORL_E_INVALID_ARG, before any CUDA call
+    assert b"ctx" in so.orl_last_error(None)
+    assert so.orl_whiten_stats(None, 1, None) == 1
+    out = ctypes.c_void_p()
+    assert so.orl_create(0, 2, 5, None, ctypes.byref(out)) == 1   # rank >= world
+    assert so.orl_create(0, 2, 0, None, ctypes.byref(out)) == 1   # world > 1 needs an id
+    assert so.orl_destroy(None) == 0
+    assert so.orl_launch_count(None) == 0
+
+
+def test_product_never_imports_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import oracle|from oracle|#include .*oracle)", text, re.M), f
+    text = open(os.path.join(ROOT, "oracle", "orl_oracle.c")).read()
+    includes = re.findall(r"^#include\s*[<\"]([^>\"]+)", text, re.M)
+    assert includes and all(i in ("math.h", "stdint.h", "stdlib.h", "string.h") for i in includes), includes

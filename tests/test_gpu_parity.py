@@ -1,0 +1,432 @@
+"""GPU parity: liborl.so (through the C ABI) vs the fp64 oracle on the same
+seeded synthetic inputs.  Every test here needs a B200.
+
+Stage isolation: each downstream stage is compared with the
+oracle stage fed the GPU's own fp32 upstream outputs; the whole chain from
+logits is also compared end to end on the tiny fp32 config.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2405_11143_b200 import synth
+from tests import parity
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2405_11143_b200 import orl
+    from paper_2405_11143_b200.pipeline import Buffers, PathConfig, run_iteration
+
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = orl.Context(0)
+    yield c
+    c.close()
+
+
+def _to_dev(batch):
+    return {k: (v.to(DEV) if isinstance(v, torch.Tensor) else v) for k, v in batch.items()}
+
+
+def _run(ctx, batch_dev, cfg, mb, grads=True):
+    B, T = batch_dev["tokens"].shape
+    bufs = Buffers(B, T, DEV, cfg.group_size, grads=grads)
+    src = lambda role, s, e: batch_dev[f"logits_{role}"][s:e]  # noqa: E731
+    status, st = run_iteration(ctx, batch_dev, cfg, bufs, src, mb=mb)
+    torch.cuda.synchronize()
+    return status, st, bufs
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _isolated_oracle(npb, bufs, ocfg):
+    """Oracle downstream of S1, fed the GPU's fp32 log-probs / entropy."""
+    sh = dict(npb)
+    sh["logp_old"] = _np(bufs.logp_old).astype(np.float64)
+    sh["logp_ref"] = _np(bufs.logp_ref).astype(np.float64)
+    sh["logp_new"] = _np(bufs.logp_new).astype(np.float64)
+    sh["entropy_new"] = _np(bufs.entropy).astype(np.float64)
+    return oracle.pipeline([sh], ocfg)
+
+
+def _check_downstream(bufs, o, glob, st, mask, cfg_name, ppo_tol=parity.REL, raw_shaped=None):
+    parity.check_rel("kl", _np(bufs.kl), o["kl"], mask)
+    # RPP-baseline: the GPU shapes with the raw R_b and K3 subtracts mu_g at t = L_b - 1
+    # (orl.h orl_advantages); the oracle shapes R_b - mu_g.  Compare the raw shaping then.
+    parity.check_rel("shaped_reward", _np(bufs.shaped), o["shaped_reward"] if raw_shaped is None else raw_shaped,
+                     mask)
+    parity.check_rel("adv", _np(bufs.adv), o["adv"], mask)
+    if o.get("ret") is not None:
+        parity.check_rel("ret", _np(bufs.ret), o["ret"], mask)
+    parity.check_rel("dloss_dlogp", _np(bufs.dlogp), o["dlogp"], mask)
+    if bufs.dv is not None:
+        parity.check_rel("dloss_dv", _np(bufs.dv), o["dv"], mask)
+    # clip decisions bit-exact (outside a 1e-6 tie band around the clip edges)
+    lp_n, lp_o = _np(bufs.logp_new).astype(np.float64), _np(bufs.logp_old).astype(np.float64)
+    rho = np.exp(lp_n - lp_o)
+    gpu_clipped = (_np(bufs.dlogp) == 0.0) & mask
+    ora_clipped = o["clipped"].astype(bool) & mask
+    tie = (np.abs(rho - 0.8) < 1e-6) | (np.abs(rho - 1.2) < 1e-6) | (np.abs(rho - 1.28) < 1e-6)
+    zero_adv = np.abs(o["adv_w"]) < 1e-30
+    sel = mask & ~tie & ~zero_adv
+    if not np.any(o["dlogp"][mask & ora_clipped] != 0):       # no KL term in the gradient
+        assert np.array_equal(gpu_clipped[sel], ora_clipped[sel]), f"{cfg_name}: clip decisions differ"
+    gs, os_ = st, glob["stats"]
+    assert gs["n_tokens"] == os_["n_tokens"]
+    ntie = np.count_nonzero(tie & mask)
+    for k in ("clip_frac", "value_clip_frac"):
+        assert abs(gs[k] - os_[k]) <= 1e-12 + ntie / max(1, mask.sum()), (k, gs[k], os_[k])
+    # scale floors: the mean |per-token term| of each statistic
+    mabs = lambda a: float(np.mean(np.abs(a[mask]))) if mask.any() else 0.0  # noqa: E731
+    floors = dict(policy_loss=mabs(o["obj"]), value_loss=mabs(o["vl"]), entropy=mabs(o["entropy"]),
+                  kl=1e-6, approx_kl_old=1e-6, ratio_mean=1.0)
+    floors["total_loss"] = sum(floors[k] for k in ("policy_loss", "value_loss", "entropy"))
+    for k, fl in floors.items():
+        g_, o_ = gs[k], os_[k]
+        assert abs(g_ - o_) <= ppo_tol * max(abs(o_), fl), (k, g_, o_, fl)
+    if os_["n_tokens"] >= 2 and gs["adv_std"]:
+        for g_, o_ in ((gs["adv_mean"], glob["adv_mean"]), (gs["adv_std"], glob["adv_std"])):
+            assert abs(g_ - o_) <= 1e-6 * max(1.0, abs(o_)), (g_, o_)
+
+
+# --------------------------------------------------------------------------- tiny, end to end
+@pytest.mark.parametrize("kind", ["gae", "rpp", "rpp_baseline", "grpo"])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_tiny_end_to_end_and_isolated(ctx, kind, seed):
+    c = dict(synth.CONFIGS["tiny"])
+    B = 8
+    c.update(adv_kind=kind, group_size=2 if kind in ("grpo", "rpp_baseline") else 1)
+    if kind == "grpo":
+        c.update(kl_mode="loss", kl_est_loss="k2", beta_loss=0.05, whiten=False, eps_v=0.0, c1=0.0)
+    if kind.startswith("rpp"):
+        c.update(eps_v=0.0, c1=0.0)
+    batch = synth.make_batch(seed, B, c["T"], c["V"], "f32", "stress", "tiny", c["rewards"])
+    cfg = PathConfig.from_synth(c)
+    status, st, bufs = _run(ctx, _to_dev(batch), cfg, mb=3)
+    assert status == "ORL_OK", status
+    npb = synth.batch_to_numpy(batch)
+    m = parity.valid_mask(npb["lengths"], c["T"])
+    # end to end from the fp32 logits
+    out, glob = oracle.pipeline([npb], c)
+    o = out[0]
+    parity.check_abs("logp_old", _np(bufs.logp_old), o["logp_old"], m)
+    parity.check_abs("logp_ref", _np(bufs.logp_ref), o["logp_ref"], m)
+    parity.check_abs("logp_new", _np(bufs.logp_new), o["logp_new"], m)
+    parity.check_abs("entropy", _np(bufs.entropy), o["entropy"], m)
+    parity.check_rel("adv(e2e)", _np(bufs.adv), o["adv"], m, rel=1e-4)
+    # stage isolation at the 1e-5 bar
+    out_i, glob_i = _isolated_oracle(npb, bufs, c)
+    raw = None
+    if kind == "rpp_baseline":
+        raw = oracle.shape_rewards(npb["lengths"], _np(bufs.logp_old), _np(bufs.logp_ref), c["kl_est_reward"],
+                                   c["beta_reward"], npb["seq_reward"])[1]
+    _check_downstream(bufs, out_i[0], glob_i, st, m, f"tiny-{kind}", raw_shaped=raw)
+    if kind in ("grpo", "rpp_baseline"):
+        keep = oracle.group_advantages(npb["seq_reward"], 2)[1]
+        assert np.array_equal(_np(bufs.keep)[: B // 2], keep)
+
+
+def test_tiny_gathered_bit_exact_and_lse(ctx):
+    c = synth.CONFIGS["tiny"]
+    batch = synth.make_batch(5, 8, 16, 32, "f32", "stress", "tiny")
+    g = _to_dev(batch)
+    B, T = 8, 16
+    logp, ent, lse, gat = (torch.full((B, T), 7.0, device=DEV) for _ in range(4))
+    orl.orl_begin_iteration(ctx)
+    orl.orl_logprobs(ctx, g["tokens"], g["lengths"], g["logits_old"], logp, entropy=ent, lse=lse,
+                     gathered=gat, inv_temp=1 / 0.7)
+    torch.cuda.synchronize()
+    npb = synth.batch_to_numpy(batch)
+    o = oracle.logprobs(npb["logits_old"], npb["tokens"], npb["lengths"], 1 / 0.7)
+    m = parity.valid_mask(npb["lengths"], T)
+    assert np.array_equal(_np(gat)[m], o["gathered"][m].astype(np.float32))
+    parity.check_abs("lse", _np(lse), o["lse"], m)
+    parity.check_abs("logp", _np(logp), o["logp"], m)
+    parity.check_abs("entropy", _np(ent), o["entropy"], m)
+
+
+# --------------------------------------------------------------------------- bf16 mid size
+def _gpu_batch(seed, B, T, V, lengths="mixed", rewards="normal", group_size=1, mode="realistic"):
+    L = synth.lengths_for(B, T, seed, lengths)
+    tok = synth.tokens_for(B, T, V, seed)
+    bufs = tuple(torch.empty(B, T, V, dtype=torch.bfloat16, device=DEV) for _ in range(3))
+    synth.fill_logits_(bufs, tok, seed, 0, mode)
+    R = synth.rewards_for(B, seed, rewards, group_size)
+    v_old, v_new = synth.values_for(B, T, seed)
+    return dict(logits_old=bufs[0], logits_ref=bufs[1], logits_new=bufs[2], tokens=tok.to(DEV),
+                lengths=L.to(DEV), seq_reward=R.to(DEV), values_old=v_old.to(DEV), values_new=v_new.to(DEV))
+
+
+@pytest.mark.parametrize("mode", ["realistic", "stress"])
+def test_mid_bf16_llama_vocab(ctx, mode):
+    c = dict(synth.CONFIGS["llama8b"])
+    B, T, V = 4, 256, c["V"]
+    g = _gpu_batch(11, B, T, V, "mixed", mode=mode)
+    cfg = PathConfig.from_synth(c)
+    status, st, bufs = _run(ctx, g, cfg, mb=3)
+    assert status == "ORL_OK"
+    npb = synth.batch_to_numpy({k: v for k, v in g.items()})
+    m = parity.valid_mask(npb["lengths"], T)
+    for role, buf in (("old", bufs.logp_old), ("ref", bufs.logp_ref), ("new", bufs.logp_new)):
+        o = oracle.logprobs(npb[f"logits_{role}"], npb["tokens"], npb["lengths"])
+        parity.check_abs(f"logp_{role}", _np(buf), o["logp"], m)
+        if role == "new":
+            parity.check_abs("entropy", _np(bufs.entropy), o["entropy"], m)
+    out_i, glob_i = _isolated_oracle(npb, bufs, c)
+    _check_downstream(bufs, out_i[0], glob_i, st, m, f"mid-{mode}")
+
+
+# --------------------------------------------------------------------------- full sizes, sampled
+def _sampled_rows_check(g, bufs, n_rows=48, seed=0):
+    """S1 at the full V on rows sampled across the batch, one by one."""
+    L = _np(g["lengths"])
+    B, T = g["tokens"].shape
+    rng = np.random.default_rng(seed)
+    valid = [(b, t) for b in range(B) for t in [0, int(L[b]) - 1, int(rng.integers(0, max(1, L[b])))] if L[b] > 0]
+    pick = [valid[i] for i in rng.choice(len(valid), size=min(n_rows, len(valid)), replace=False)]
+    tok = _np(g["tokens"])
+    for role, buf in (("old", bufs.logp_old), ("ref", bufs.logp_ref), ("new", bufs.logp_new)):
+        rows = torch.stack([g[f"logits_{role}"][b, t] for b, t in pick]).unsqueeze(1)
+        x = synth.to_numpy_logits(rows)
+        o = oracle.logprobs(x, np.array([[tok[b, t]] for b, t in pick], np.int32), np.ones(len(pick), np.int32))
+        gv = np.array([[_np(buf)[b, t]] for b, t in pick])
+        parity.check_abs(f"logp_{role}@full", gv, o["logp"], np.ones_like(gv, bool))
+        if role == "new":
+            gh = np.array([[_np(bufs.entropy)[b, t]] for b, t in pick])
+            parity.check_abs("entropy@full", gh, o["entropy"], np.ones_like(gh, bool))
+
+
+@pytest.mark.parametrize("name,B", [("llama8b", 128), ("longcot", 8), ("grpo", 16), ("rpp8", 16)])
+def test_full_size_sampled(ctx, name, B):
+    """BASELINE.json configs at their full T and V (llama8b also at its full B), in the
+    launch configuration bench.py times (same micro-batch size)."""
+    c = dict(synth.CONFIGS[name])
+    T, V = c["T"], c["V"]
+    free = torch.cuda.mem_get_info()[0]
+    need = 3 * B * T * V * 2 * 1.05
+    if need > free:
+        pytest.skip(f"needs {need / 1e9:.0f} GB")
+    g = _gpu_batch(1234, B, T, V, "full" if name == "llama8b" else "mixed", c["rewards"], c["group_size"])
+    cfg = PathConfig.from_synth(c)
+    status, st, bufs = _run(ctx, g, cfg, mb=min(c["mb"], B))
+    assert status == "ORL_OK", status
+    _sampled_rows_check(g, bufs)
+    # downstream stages on the whole batch, oracle fed the GPU's fp32 upstream
+    npb = {k: (v.detach().cpu().numpy() if isinstance(v, torch.Tensor) and not k.startswith("logits_") else v)
+           for k, v in g.items() if not k.startswith("logits_")}
+    m = parity.valid_mask(npb["lengths"], T)
+    out_i, glob_i = _isolated_oracle(npb, bufs, c)
+    _check_downstream(bufs, out_i[0], glob_i, st, m, name)
+    del g
+    torch.cuda.empty_cache()
+
+
+# --------------------------------------------------------------------------- edge cases / errors
+def test_generic_path_unaligned_vocab(ctx):
+    """V = 50257 bf16 rows are not 16-byte multiples -> generic (non-TMA) kernel."""
+    B, T, V = 3, 40, 50257
+    g = _gpu_batch(3, B, T, V, "mixed")
+    cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V))
+    status, st, bufs = _run(ctx, g, cfg, mb=2)
+    assert status == "ORL_OK"
+    npb = synth.batch_to_numpy(g)
+    m = parity.valid_mask(npb["lengths"], T)
+    o = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"])
+    parity.check_abs("logp_new", _np(bufs.logp_new), o["logp"], m)
+    parity.check_abs("entropy", _np(bufs.entropy), o["entropy"], m)
+
+
+def test_forced_generic_matches_tma(ctx, monkeypatch):
+    B, T, V = 2, 64, 4096
+    g = _gpu_batch(4, B, T, V, "mixed")
+    cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V))
+    _, st1, b1 = _run(ctx, g, cfg, mb=2)
+    monkeypatch.setenv("ORL_FORCE_GENERIC", "1")
+    _, st2, b2 = _run(ctx, g, cfg, mb=2)
+    m = parity.valid_mask(_np(g["lengths"]), T)
+    np.testing.assert_allclose(_np(b1.logp_new)[m], _np(b2.logp_new)[m], atol=2e-6)
+    np.testing.assert_allclose(_np(b1.entropy)[m], _np(b2.entropy)[m], atol=2e-5)
+
+
+def test_strided_response_aligned_view(ctx):
+    """Logits of full sequences (prompt + response), sliced at prompt_len - 1 (Z1)."""
+    B, P, T, V = 3, 5, 24, 1024
+    full = torch.randn(B, P + T, V, device=DEV).to(torch.bfloat16)
+    view = full[:, P - 1:P - 1 + T, :]
+    tok = synth.tokens_for(B, T, V, 9).to(DEV)
+    L = torch.tensor([24, 10, 1], dtype=torch.int32, device=DEV)
+    logp = torch.zeros(B, T, device=DEV)
+    orl.orl_begin_iteration(ctx)
+    orl.orl_logprobs(ctx, tok, L, view, logp)
+    torch.cuda.synchronize()
+    o = oracle.logprobs(synth.to_numpy_logits(view), _np(tok), _np(L))
+    parity.check_abs("logp(view)", _np(logp), o["logp"], parity.valid_mask(_np(L), T))
+
+
+def test_neg_inf_entries_and_errors(ctx):
+    B, T, V = 2, 8, 2048
+    x = torch.randn(B, T, V, device=DEV) * 2
+    x[0, 1, 100:700] = float("-inf")             # allowed (Z26)
+    x[0, 2, :] = float("-inf")                   # whole row -inf: non-finite
+    x[1, 3, 5] = float("nan")                    # NaN logit: non-finite
+    xb = x.to(torch.bfloat16)
+    tok = synth.tokens_for(B, T, V, 2).to(DEV)
+    tok[0, 1] = 3                                # target not at a -inf entry
+    tok[1, 5] = V + 7                            # out of vocabulary
+    L = torch.tensor([8, 8], dtype=torch.int32, device=DEV)
+    logp, ent = torch.zeros(B, T, device=DEV), torch.zeros(B, T, device=DEV)
+    orl.orl_begin_iteration(ctx)
+    orl.orl_logprobs(ctx, tok, L, xb, logp, entropy=ent)
+    torch.cuda.synchronize()
+    o = oracle.logprobs(synth.to_numpy_logits(xb), _np(tok), _np(L))
+    lp, en = _np(logp), _np(ent)
+    ok = np.ones((B, T), bool)
+    ok[0, 2] = ok[1, 3] = ok[1, 5] = False
+    parity.check_abs("logp", np.where(ok, lp, 0), np.where(ok, o["logp"], 0), ok)
+    parity.check_abs("entropy", np.where(ok, en, 0), np.where(ok, o["entropy"], 0), ok)
+    assert np.isnan(lp[0, 2]) and np.isnan(lp[1, 3]) and np.isnan(lp[1, 5])
+    status, st = orl.orl_finalize(ctx, orl.PPOConfig())
+    assert status == "ORL_E_TOKEN_RANGE"
+    assert st["n_token_range"] == 1 and st["n_nonfinite"] == 2
+
+
+def test_ratio_guard_and_empty_batch(ctx):
+    B, T, V = 2, 4, 256
+    x = torch.randn(B, T, V, device=DEV)
+    tok = synth.tokens_for(B, T, V, 1).to(DEV)
+    L = torch.tensor([4, 0], dtype=torch.int32, device=DEV)
+    z = lambda: torch.zeros(B, T, device=DEV)  # noqa: E731
+    lo, adv, lpn = z(), z(), z()
+    lo[0, 2] = -60.0                              # |logp_new - logp_old| > 30
+    orl.orl_begin_iteration(ctx)
+    orl.orl_advantages(ctx, L, adv, kind="rpp", gamma=1.0, shaped_reward=z())
+    orl.orl_whiten_stats(ctx, False)
+    orl.orl_ppo_loss(ctx, tok, L, x, orl.PPOConfig(), lo, adv, lpn)
+    status, st = orl.orl_finalize(ctx, orl.PPOConfig())
+    assert status == "ORL_E_NUMERIC_GUARD" and st["n_guard"] == 1 and st["n_tokens"] == 4
+    L0 = torch.zeros(B, dtype=torch.int32, device=DEV)
+    orl.orl_begin_iteration(ctx)
+    orl.orl_advantages(ctx, L0, adv, kind="rpp", gamma=1.0, shaped_reward=z())
+    orl.orl_whiten_stats(ctx, True)
+    orl.orl_ppo_loss(ctx, tok, L0, x, orl.PPOConfig(), lo, adv, lpn)
+    status, st = orl.orl_finalize(ctx, orl.PPOConfig())
+    assert status == "ORL_E_EMPTY_BATCH" and st["whiten_warn"] == 1
+    assert torch.all(lpn == 0) and torch.all(adv == 0)
+
+
+def test_host_argument_errors(ctx):
+    B, T, V = 2, 4, 64
+    x = torch.randn(B, T, V, device=DEV)
+    tok = torch.zeros(B, T, dtype=torch.int32, device=DEV)
+    L = torch.full((B,), T, dtype=torch.int32, device=DEV)
+    lp = torch.zeros(B, T, device=DEV)
+    with pytest.raises(orl.OrlError) as e:
+        orl.orl_logprobs(ctx, tok, L, x, lp, inv_temp=0.0)
+    assert e.value.name == "ORL_E_INVALID_ARG"
+    with pytest.raises(orl.OrlError) as e:
+        orl.orl_logprobs(ctx, tok, L, x, lp, kl=lp)
+    assert e.value.name == "ORL_E_INVALID_ARG"
+    with pytest.raises(orl.OrlError) as e:
+        orl.orl_advantages(ctx, L, lp, kind="grpo", group_size=3, seq_reward=L.float())
+    assert e.value.name == "ORL_E_GROUP_SPLIT"
+    orl.orl_begin_iteration(ctx)
+    with pytest.raises(orl.OrlError) as e:
+        orl.orl_ppo_loss(ctx, tok, L, x, orl.PPOConfig(), lp, lp, lp)
+    assert e.value.name == "ORL_E_STATE"
+    with pytest.raises(TypeError):
+        orl.orl_logprobs(ctx, tok, L, x.to(torch.float16), lp)
+
+    class Misaligned:                 # a per-token array 2 bytes off a 4-byte boundary
+        def data_ptr(self):
+            return lp.data_ptr() + 2
+
+    with pytest.raises(orl.OrlError) as e:
+        orl.orl_logprobs(ctx, tok, L, x, Misaligned())
+    assert e.value.name == "ORL_E_ALIGN"
+
+
+# --------------------------------------------------------------------------- determinism / DP
+def test_run_to_run_bit_reproducible(ctx):
+    c = dict(synth.CONFIGS["llama8b"])
+    g = _gpu_batch(21, 6, 128, 8192, "mixed")
+    cfg = PathConfig.from_synth(c)
+    _, s1, b1 = _run(ctx, g, cfg, mb=4)
+    _, s2, b2 = _run(ctx, g, cfg, mb=4)
+    assert s1 == s2
+    for k in ("logp_old", "logp_ref", "logp_new", "entropy", "adv", "ret", "dlogp"):
+        assert torch.equal(getattr(b1, k), getattr(b2, k)), k
+
+
+@pytest.mark.parametrize("kind,n", [("gae", 2), ("rpp", 4), ("grpo", 2)])
+def test_shard_emulation_matches_single_rank(kind, n):
+    """n virtual ranks on one GPU, partials exchanged through the collective
+    boundary hooks (the exact device merges NCCL feeds), vs one rank."""
+    B, T, V = 8, 64, 2048
+    c = dict(synth.CONFIGS["llama8b"], adv_kind=kind, group_size=2 if kind == "grpo" else 1)
+    if kind == "grpo":
+        c.update(kl_mode="loss", beta_loss=0.01, whiten=False, eps_v=0.0, c1=0.0)
+    cfg = PathConfig.from_synth(c)
+    g = _gpu_batch(31, B, T, V, "mixed", "group_bernoulli" if kind == "grpo" else "normal", 2)
+    one = orl.Context(0)
+    _, st1, b1 = _run(one, g, cfg, mb=3)
+    bounds = synth.split_bounds(B, n, c["group_size"])
+    ctxs = [orl.Context(0) for _ in bounds]
+    shard_bufs = []
+    for cx, (s, e) in zip(ctxs, bounds):
+        gs = {k: v[s:e] for k, v in g.items()}
+        bb = Buffers(e - s, T, DEV, c["group_size"])
+        src = lambda role, a, z, gs=gs: gs[f"logits_{role}"][a:z]  # noqa: E731
+        # experience half up to the advantages
+        orl.orl_begin_iteration(cx)
+        for a, z in [(a, min(e - s, a + 3)) for a in range(0, e - s, 3)]:
+            orl.orl_logprobs(cx, gs["tokens"], gs["lengths"], src("old", a, z), bb.logp_old, seq_offset=a)
+        for a, z in [(a, min(e - s, a + 3)) for a in range(0, e - s, 3)]:
+            orl.orl_logprobs(cx, gs["tokens"], gs["lengths"], src("ref", a, z), bb.logp_ref, seq_offset=a,
+                             partner_logp=bb.logp_old, kl_est=cfg.kl_est_reward,
+                             beta_reward=cfg.beta_reward, seq_reward=gs["seq_reward"], kl=bb.kl,
+                             shaped_reward=bb.shaped)
+        orl.orl_advantages(cx, gs["lengths"], bb.adv, kind=kind, gamma=cfg.gamma, lam=cfg.lam,
+                           group_size=cfg.group_size, shaped_reward=bb.shaped,
+                           values=gs["values_old"] if cfg.critic else None, seq_reward=gs["seq_reward"],
+                           ret=bb.ret)
+        shard_bufs.append((gs, bb, src))
+    wparts = np.stack([orl.orl_export_partials(cx, 0) for cx in ctxs])
+    for cx in ctxs:
+        orl.orl_import_partials(cx, 0, wparts)
+        orl.orl_whiten_stats(cx, cfg.whiten and kind != "grpo")
+    for cx, (gs, bb, src) in zip(ctxs, shard_bufs):
+        Bs = gs["tokens"].shape[0]
+        for a, z in [(a, min(Bs, a + 3)) for a in range(0, Bs, 3)]:
+            crit = cfg.critic
+            orl.orl_ppo_loss(cx, gs["tokens"], gs["lengths"], src("new", a, z), cfg.ppo, bb.logp_old, bb.adv,
+                             bb.logp_new, seq_offset=a, logp_ref=bb.logp_ref, ret=bb.ret if crit else None,
+                             v_new=gs["values_new"] if crit else None, v_old=gs["values_old"] if crit else None,
+                             entropy=bb.entropy, dloss_dlogp=bb.dlogp)
+    sparts = np.stack([orl.orl_export_partials(cx, 1) for cx in ctxs])
+    res = []
+    for cx in ctxs:
+        orl.orl_import_partials(cx, 1, sparts)
+        res.append(orl.orl_finalize(cx, cfg.ppo))
+    for status, st in res:
+        assert status == "ORL_OK"
+        assert st == res[0][1]                      # every rank bit-identical
+        for k, v in st1.items():
+            if isinstance(v, float):
+                assert abs(st[k] - v) <= 1e-12 * max(1.0, abs(v)), (k, st[k], v)
+    for (s, e), (gs, bb, _) in zip(bounds, shard_bufs):
+        assert torch.equal(bb.logp_new, b1.logp_new[s:e])
+        assert torch.equal(bb.adv, b1.adv[s:e])
+        torch.testing.assert_close(bb.dlogp, b1.dlogp[s:e], rtol=1e-6, atol=1e-12)
+    for cx in ctxs + [one]:
+        cx.close()

@@ -278,6 +278,141 @@ __device__ void finish_partials(const K1Params &p, double (*wacc)[kNumPartials],
     if (lt == 0) *p.ticket = 0u;
 }
 
+// ---------------------------------------------------------------- chunk math
+// Per-thread streaming state: running reference m (log2 units) and packed
+// (even, odd) accumulators s = sum 2^t, u = sum 2^t t with t = x c - m.
+struct ThreadAcc {
+    float m;
+    uint64_t sA, sB, uA, uB;
+};
+
+__device__ __forceinline__ uint64_t bf16x2_to_f32x2(uint32_t w) {
+    uint64_t r;
+    asm("{\n\t.reg .b32 lo, hi;\n\tshl.b32 lo, %1, 16;\n\tand.b32 hi, %1, 0xffff0000;\n\t"
+        "mov.b64 %0, {lo, hi};\n\t}" : "=l"(r) : "r"(w));
+    return r;
+}
+
+// Number of element pairs held in 16 raw 32-bit words.
+template <typename Tin> struct Words;
+template <> struct Words<uint16_t> { static constexpr int kPairs = 16; };
+template <> struct Words<float> { static constexpr int kPairs = 8; };
+
+template <typename Tin>
+__device__ __forceinline__ uint64_t pair_at(const uint32_t (&w)[16], int q) {
+    if (sizeof(Tin) == 2) return bf16x2_to_f32x2(w[q]);
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(w[2 * q]), "r"(w[2 * q + 1]));
+    return r;
+}
+
+// Accumulate every pair of the chunk against the current m (no max, no clamp).
+template <typename Tin, bool ENT>
+__device__ __forceinline__ void acc_words(ThreadAcc &a, const uint32_t (&w)[16], uint64_t c2p) {
+    const uint64_t nm = pack2(-a.m, -a.m);
+#pragma unroll
+    for (int q = 0; q < Words<Tin>::kPairs; ++q) {
+        const uint64_t tt = ffma2(pair_at<Tin>(w, q), c2p, nm);
+        float t0, t1;
+        unpack2(tt, t0, t1);
+        const uint64_t e = pack2(ex2(t0), ex2(t1));
+        if (q & 1) {
+            a.sB = fadd2(a.sB, e);
+            if (ENT) a.uB = ffma2(e, tt, a.uB);
+        } else {
+            a.sA = fadd2(a.sA, e);
+            if (ENT) a.uA = ffma2(e, tt, a.uA);
+        }
+    }
+}
+
+// Exact path: clamp -inf (NaN kept), chunk max, rescale, accumulate.  Used for
+// the first chunk of every row and to redo a chunk whose fast pass overflowed
+// (an element more than 64 log2-units above m), produced a non-finite moment
+// (-inf logits in the entropy moment) or saw NaN.
+template <typename Tin, bool ENT>
+__device__ __forceinline__ void exact_words(ThreadAcc &a, uint32_t (&w)[16], float c2, uint64_t c2p) {
+    float cm;
+    if (sizeof(Tin) == 2) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) w[q] = hmax2_nan(w[q], kNegClampBf16x2);
+        uint32_t mx[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx[q] = hmax2_nan(w[q], w[q + 8]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = hmax2_nan(mx[q], mx[q + 4]);
+        mx[0] = hmax2_nan(hmax2_nan(mx[0], mx[2]), hmax2_nan(mx[1], mx[3]));
+        cm = fmax_nan(bf16lo(mx[0]), bf16hi(mx[0]));
+    } else {
+        cm = kNegClampF32;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const float f = fmax_nan(__uint_as_float(w[q]), kNegClampF32);
+            w[q] = __float_as_uint(f);
+            cm = fmax_nan(cm, f);
+        }
+    }
+    const float mn = fmax_nan(a.m, cm * c2);
+    const float d = a.m - mn;
+    const float r = ex2(d);
+    const uint64_t d2 = pack2(d, d), r2 = pack2(r, r);
+    if (ENT) {
+        a.uA = fmul2(r2, ffma2(d2, a.sA, a.uA));
+        a.uB = fmul2(r2, ffma2(d2, a.sB, a.uB));
+    }
+    a.sA = fmul2(r2, a.sA);
+    a.sB = fmul2(r2, a.sB);
+    a.m = mn;
+    acc_words<Tin, ENT>(a, w, c2p);
+}
+
+// True if the fast pass must be redone exactly.
+template <bool ENT>
+__device__ __forceinline__ bool needs_redo(const ThreadAcc &a) {
+    float s0, s1, s2, s3;
+    unpack2(fadd2(a.sA, a.sB), s0, s1);
+    s2 = s0 + s1;
+    bool bad = !(s2 < 1.8446744e19f);  // 2^64; also NaN / inf
+    if (ENT) {
+        unpack2(fadd2(a.uA, a.uB), s0, s1);
+        s3 = s0 + s1;
+        bad |= !(fabsf(s3) < 3.0e38f);
+    }
+    return bad;
+}
+
+// Load this thread's 4 x 16 B of the chunk (ragged tail padded with a finite
+// very negative logit, so padding gives 2^t = 0 and 2^t t = 0).
+template <typename Tin, bool FULL>
+__device__ __forceinline__ void load_words(uint32_t (&w)[16], const uint8_t *sb, int ct, int nvec) {
+    const uint32_t pad = sizeof(Tin) == 2 ? kNegClampBf16x2 : __float_as_uint(kNegClampF32);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int vi = ct + k * kConsumers;
+        uint4 v;
+        if (FULL || vi < nvec) v = lds128(sb + vi * 16);
+        else v = make_uint4(pad, pad, pad, pad);
+        w[4 * k + 0] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+    }
+}
+
+template <typename Tin, bool ENT, bool FULL>
+__device__ __forceinline__ void process_chunk(ThreadAcc &a, const uint8_t *sb, int ct, int nvec, bool first,
+                                              float c2, uint64_t c2p) {
+    uint32_t w[16];
+    load_words<Tin, FULL>(w, sb, ct, nvec);
+    if (first) {
+        exact_words<Tin, ENT>(a, w, c2, c2p);
+        return;
+    }
+    const ThreadAcc saved = a;
+    acc_words<Tin, ENT>(a, w, c2p);
+    if (needs_redo<ENT>(a)) {
+        a = saved;
+        exact_words<Tin, ENT>(a, w, c2, c2p);
+    }
+}
+
 // ---------------------------------------------------------------- TMA kernel
 template <typename Tin, int MODE>
 __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
@@ -332,7 +467,6 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
     if (MODE == kModeLoss) {
         wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
     }
-    constexpr int EPV = 16 / sizeof(Tin);  // elements per 16-byte vector
     const int nside = MODE == kModeLoss ? 6 : 2;
 
     int stage = 0;
@@ -359,111 +493,42 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
         if (epi && lane < nside) side = load_side(p, MODE, lane, gi, b);
 
         const uint64_t c2p = pack2(p.c2, p.c2);
-        float m = kMInit;
-        uint64_t sA = 0, sB = 0, uA = 0, uB = 0;  // packed (even, odd) accumulators
+        ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
         float tgt = 0.f;
         bool have_tgt = false;
+        // which chunk / thread / element holds the target logit
+        const bool y_ok = (y >= 0) && ((int64_t)y < p.V);
+        const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin);
+        const int64_t tchunk = y_ok ? ybyte / kChunk : -1;
+        const int tin = (int)(ybyte % kChunk);
+        const bool towner = ((tin >> 4) % kConsumers) == ct;
+        const bool ent = MODE == kModeLoss || p.entropy != nullptr;
 
-        for (int64_t off = 0; off < row_bytes; off += kChunk) {
+        int64_t ci = 0;
+        for (int64_t off = 0; off < row_bytes; off += kChunk, ++ci) {
             const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
-            const int nvec = bytes >> 4;
             mbar_wait(&S.full[stage], phase);
             const uint8_t *sb = S.stage[stage];
-            // target capture (raw value, before clamping)
-            {
-                const int64_t first = off / sizeof(Tin);
-                const int64_t loc = (int64_t)y - first;
-                if (loc >= 0 && loc < bytes / (int)sizeof(Tin)) {
-                    const int vec = (int)(loc / EPV);
-                    if ((vec % kConsumers) == ct) {
-                        if (sizeof(Tin) == 2)
-                            tgt = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(sb)[loc]) << 16);
-                        else
-                            tgt = reinterpret_cast<const float *>(sb)[loc];
-                        have_tgt = true;
-                    }
-                }
+            if (ci == tchunk && towner) {   // raw target value, before any clamping
+                tgt = sizeof(Tin) == 2
+                          ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(sb + tin)) << 16)
+                          : *reinterpret_cast<const float *>(sb + tin);
+                have_tgt = true;
             }
-            if (sizeof(Tin) == 2) {
-                uint32_t w[16];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    uint4 v = make_uint4(kNegClampBf16x2, kNegClampBf16x2, kNegClampBf16x2, kNegClampBf16x2);
-                    if (vi < nvec) v = lds128(sb + vi * 16);
-                    w[4 * k + 0] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
-                }
-#pragma unroll
-                for (int q = 0; q < 16; ++q) w[q] = hmax2_nan(w[q], kNegClampBf16x2);
-                uint32_t mx[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) mx[q] = hmax2_nan(w[q], w[q + 8]);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) mx[q] = hmax2_nan(mx[q], mx[q + 4]);
-                mx[0] = hmax2_nan(hmax2_nan(mx[0], mx[2]), hmax2_nan(mx[1], mx[3]));
-                const float cm = fmax_nan(bf16lo(mx[0]), bf16hi(mx[0])) * p.c2;
-                const float mn = fmax_nan(m, cm);
-                const float d = m - mn;
-                const float r = ex2(d);
-                const uint64_t d2 = pack2(d, d), r2 = pack2(r, r);
-                uA = fmul2(r2, ffma2(d2, sA, uA));
-                uB = fmul2(r2, ffma2(d2, sB, uB));
-                sA = fmul2(r2, sA);
-                sB = fmul2(r2, sB);
-                m = mn;
-                const uint64_t nm = pack2(-m, -m);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const uint64_t x = pack2(bf16lo(w[q]), bf16hi(w[q]));
-                    const uint64_t tt = ffma2(x, c2p, nm);
-                    float t0, t1;
-                    unpack2(tt, t0, t1);
-                    const uint64_t e = pack2(ex2(t0), ex2(t1));
-                    if (q & 1) { sB = fadd2(sB, e); uB = ffma2(e, tt, uB); }
-                    else       { sA = fadd2(sA, e); uA = ffma2(e, tt, uA); }
-                }
+            const bool first = off == 0;
+            if (bytes == kChunk) {
+                if (ent) process_chunk<Tin, true, true>(acc, sb, ct, kChunk >> 4, first, p.c2, c2p);
+                else process_chunk<Tin, false, true>(acc, sb, ct, kChunk >> 4, first, p.c2, c2p);
             } else {
-                float f[16];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    uint4 v = make_uint4(__float_as_uint(kNegClampF32), __float_as_uint(kNegClampF32),
-                                         __float_as_uint(kNegClampF32), __float_as_uint(kNegClampF32));
-                    if (vi < nvec) v = lds128(sb + vi * 16);
-                    f[4 * k + 0] = __uint_as_float(v.x); f[4 * k + 1] = __uint_as_float(v.y);
-                    f[4 * k + 2] = __uint_as_float(v.z); f[4 * k + 3] = __uint_as_float(v.w);
-                }
-                float cmx = kNegClampF32;
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    f[q] = fmax_nan(f[q], kNegClampF32);
-                    cmx = fmax_nan(cmx, f[q]);
-                }
-                const float mn = fmax_nan(m, cmx * p.c2);
-                const float d = m - mn;
-                const float r = ex2(d);
-                const uint64_t d2 = pack2(d, d), r2 = pack2(r, r);
-                uA = fmul2(r2, ffma2(d2, sA, uA));
-                uB = fmul2(r2, ffma2(d2, sB, uB));
-                sA = fmul2(r2, sA);
-                sB = fmul2(r2, sB);
-                m = mn;
-                const uint64_t nm = pack2(-m, -m);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const uint64_t x = pack2(f[2 * q], f[2 * q + 1]);
-                    const uint64_t tt = ffma2(x, c2p, nm);
-                    float t0, t1;
-                    unpack2(tt, t0, t1);
-                    const uint64_t e = pack2(ex2(t0), ex2(t1));
-                    if (q & 1) { sB = fadd2(sB, e); uB = ffma2(e, tt, uB); }
-                    else       { sA = fadd2(sA, e); uA = ffma2(e, tt, uA); }
-                }
+                if (ent) process_chunk<Tin, true, false>(acc, sb, ct, bytes >> 4, first, p.c2, c2p);
+                else process_chunk<Tin, false, false>(acc, sb, ct, bytes >> 4, first, p.c2, c2p);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
         }
+        const float m = acc.m;
+        const uint64_t sA = acc.sA, sB = acc.sB, uA = acc.uA, uB = acc.uB;
 
         // ---- row end: thread -> warp -> slot ----
         float s0, s1, s2, s3, u0, u1, u2, u3;

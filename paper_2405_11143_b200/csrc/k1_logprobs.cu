@@ -38,17 +38,22 @@ namespace orl {
 
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kThreads = kConsumers + 32;
+constexpr int kProducerWarp = kConsumerWarps;      // warp 8: TMA issue
+constexpr int kEpilogueWarp = kConsumerWarps + 1;  // warp 9: merge + fp64 epilogue
+constexpr int kThreads = kConsumers + 64;
 constexpr int kChunk = 16384;  // bytes per TMA stage
 constexpr int kStages = 6;
-constexpr int kSlots = 4;
+constexpr int kSlots = 3;      // row-partial ring (consumers -> epilogue warp)
+constexpr int kRowInfo = 8;    // row-info ring (producer -> consumers), >= kStages + 1
 constexpr int kVecPerThread = kChunk / 16 / kConsumers;  // 4 x 16 B per thread per chunk
 static_assert(kVecPerThread == 4, "chunk processing is written for 4 vectors per thread");
+static_assert(kRowInfo >= kStages + 1, "row-info ring must outrun the stage ring");
 
+// Every consumer thread's online state for one row, plus the target logit.
 struct RowSlot {
-    float m[kConsumerWarps], s[kConsumerWarps], u[kConsumerWarps];
+    float m[kConsumers], s[kConsumers], u[kConsumers];
     float target;
-    float pad[7];
+    float pad[31];
 };
 
 struct __align__(128) K1Smem {
@@ -57,9 +62,9 @@ struct __align__(128) K1Smem {
     uint64_t empty[kStages];
     uint64_t row_full[kSlots];
     uint64_t row_empty[kSlots];
+    int32_t row_y[kRowInfo];
     RowSlot slot[kSlots];
-    double wacc[kConsumerWarps][kNumPartials];
-    int32_t misc[4];
+    double wacc[kNumPartials];
 };
 
 size_t k1_tma_smem_bytes(int B) { return sizeof(K1Smem) + sizeof(int32_t) * (size_t)(B + 32); }
@@ -413,6 +418,26 @@ __device__ __forceinline__ void process_chunk(ThreadAcc &a, const uint8_t *sb, i
     }
 }
 
+// Warp-level variant for the TMA kernel (the epilogue warp owns the partials).
+__device__ void finish_partials_warp(const K1Params &p, const double *wacc, int lane) {
+    if (lane < kNumPartials) p.ws[(size_t)lane * p.ws_stride + blockIdx.x] = wacc[lane];
+    __threadfence();
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) last = (atomicAdd(p.ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    for (int c = 0; c < kNumPartials; ++c) {
+        double v = 0.0;
+        for (int q = lane; q < (int)gridDim.x; q += 32) v += __ldcg(&p.ws[(size_t)c * p.ws_stride + q]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) p.acc[c] += v;
+    }
+    if (lane == 0) *p.ticket = 0u;
+}
+
 // ---------------------------------------------------------------- TMA kernel
 template <typename Tin, int MODE>
 __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
@@ -433,83 +458,111 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
         }
         fence_mbar_init();
     }
-    if (tid < kConsumerWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
+    if (tid < kNumPartials) S.wacc[tid] = 0.0;
     build_prefix(p, cum, warp_tot);  // contains __syncthreads
     const int64_t N = cum[p.B - 1];
     const int64_t row_bytes = p.row_bytes;
 
-    if (warp == kConsumerWarps) {
-        // ===================== producer: one elected lane issues TMA ==========
+    if (warp == kProducerWarp) {
+        // ===================== producer: one lane issues the TMA bulk copies ======
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t j = blockIdx.x; j < N; j += gridDim.x) {
-                int b, t;
+            int64_t j = blockIdx.x;
+            int b = 0, t = 0, y = 0;
+            if (j < N) {
                 locate_row(cum, p.B, j, b, t);
+                y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
+            }
+            for (int rl = 0; j < N; j += gridDim.x, ++rl) {
+                const int64_t jn = j + gridDim.x;  // prefetch the next row's token id
+                int bn = 0, tn = 0, yn = 0;
+                if (jn < N) {
+                    locate_row(cum, p.B, jn, bn, tn);
+                    yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
+                }
                 const char *src = p.base + ((int64_t)b * p.stride_b + (int64_t)t * p.stride_t) * p.elt;
                 for (int64_t off = 0; off < row_bytes; off += kChunk) {
                     const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
                     mbar_wait(&S.empty[stage], phase ^ 1u);
+                    if (off == 0) S.row_y[rl % kRowInfo] = y;  // published by the arrive below
                     mbar_arrive_expect_tx(&S.full[stage], bytes);
                     tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
                     if (++stage == kStages) { stage = 0; phase ^= 1u; }
                 }
+                b = bn; t = tn; y = yn;
             }
         }
-        return;  // the producer warp takes no part in the consumer barriers
+        return;
     }
 
-    // ========================= consumers ======================================
+    if (warp == kEpilogueWarp) {
+        // ===================== epilogue: merge 256 partials, fp64 per-row math ===
+        double wh[4] = {0.0, 0.0, 0.0, 0.0};
+        if (MODE == kModeLoss) {
+            wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
+        }
+        const int nside = MODE == kModeLoss ? 6 : 2;
+        for (int64_t j = blockIdx.x, rl = 0; j < N; j += gridDim.x, ++rl) {
+            int b, t;
+            locate_row(cum, p.B, j, b, t);
+            const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
+            const int y = __ldg(p.tokens + gi);
+            float side = 0.f;
+            if (lane < nside) side = load_side(p, MODE, lane, gi, b);
+            const int slot = (int)(rl % kSlots);
+            mbar_wait(&S.row_full[slot], (uint32_t)(rl / kSlots) & 1u);
+            const RowSlot &R = S.slot[slot];
+            Online st{R.m[lane], R.s[lane], R.u[lane]};
+#pragma unroll
+            for (int w = 1; w < kConsumerWarps; ++w)
+                st = online_merge(st, Online{R.m[lane + 32 * w], R.s[lane + 32 * w], R.u[lane + 32 * w]});
+            st = warp_merge(st);
+            const float target = R.target;
+            float sv[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&S.row_empty[slot]);
+                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc);
+            }
+            __syncwarp();
+        }
+        if (MODE == kModeLoss) finish_partials_warp(p, S.wacc, lane);
+        return;
+    }
+
+    // ========================= consumers (warps 0..7) ============================
     const int ct = tid;  // 0..255
     zero_masked(p, cum, ct, kConsumers, MODE);
-    double wh[4] = {0.0, 0.0, 0.0, 0.0};
-    if (MODE == kModeLoss) {
-        wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
-    }
-    const int nside = MODE == kModeLoss ? 6 : 2;
-
+    const bool ent = MODE == kModeLoss || p.entropy != nullptr;
+    const uint64_t c2p = pack2(p.c2, p.c2);
     int stage = 0;
     uint32_t phase = 0;
-    int64_t j = blockIdx.x;
-    int b = 0, t = 0, y = 0;
-    if (j < N) {
-        locate_row(cum, p.B, j, b, t);
-        y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
-    }
-    for (int rl = 0; j < N; j += gridDim.x, ++rl) {
-        // prefetch the next row's token id
-        const int64_t jn = j + gridDim.x;
-        int bn = 0, tn = 0, yn = 0;
-        if (jn < N) {
-            locate_row(cum, p.B, jn, bn, tn);
-            yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
-        }
-        const bool epi = (rl % kConsumerWarps) == warp;
-        const int slot = rl % kSlots;
-        const uint32_t slot_par = (uint32_t)(rl / kSlots) & 1u;
-        const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
-        float side = 0.f;
-        if (epi && lane < nside) side = load_side(p, MODE, lane, gi, b);
-
-        const uint64_t c2p = pack2(p.c2, p.c2);
+    for (int64_t j = blockIdx.x, rl = 0; j < N; j += gridDim.x, ++rl) {
         ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
         float tgt = 0.f;
         bool have_tgt = false;
-        // which chunk / thread / element holds the target logit
-        const bool y_ok = (y >= 0) && ((int64_t)y < p.V);
-        const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin);
-        const int64_t tchunk = y_ok ? ybyte / kChunk : -1;
-        const int tin = (int)(ybyte % kChunk);
-        const bool towner = ((tin >> 4) % kConsumers) == ct;
-        const bool ent = MODE == kModeLoss || p.entropy != nullptr;
-
+        int64_t tchunk = -1;
+        int tin = 0;
+        bool towner = false;
         int64_t ci = 0;
         for (int64_t off = 0; off < row_bytes; off += kChunk, ++ci) {
             const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
             mbar_wait(&S.full[stage], phase);
+            if (off == 0) {  // which chunk / thread holds the target logit
+                const int y = S.row_y[rl % kRowInfo];
+                const bool y_ok = (y >= 0) && ((int64_t)y < p.V);
+                const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin);
+                tchunk = y_ok ? ybyte / kChunk : -1;
+                tin = (int)(ybyte % kChunk);
+                towner = ((tin >> 4) % kConsumers) == ct;
+            }
             const uint8_t *sb = S.stage[stage];
-            if (ci == tchunk && towner) {   // raw target value, before any clamping
+            if (ci == tchunk && towner) {  // raw target value, before any clamping
                 tgt = sizeof(Tin) == 2
                           ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(sb + tin)) << 16)
                           : *reinterpret_cast<const float *>(sb + tin);
@@ -527,47 +580,20 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
         }
-        const float m = acc.m;
-        const uint64_t sA = acc.sA, sB = acc.sB, uA = acc.uA, uB = acc.uB;
-
-        // ---- row end: thread -> warp -> slot ----
-        float s0, s1, s2, s3, u0, u1, u2, u3;
-        unpack2(sA, s0, s1);
-        unpack2(sB, s2, s3);
-        unpack2(uA, u0, u1);
-        unpack2(uB, u2, u3);
-        Online st{m, (s0 + s1) + (s2 + s3), (u0 + u1) + (u2 + u3)};
-        st = warp_merge(st);
-        mbar_wait(&S.row_empty[slot], slot_par ^ 1u);
-        if (lane == 0) {
-            S.slot[slot].m[warp] = st.m;
-            S.slot[slot].s[warp] = st.s;
-            S.slot[slot].u[warp] = st.u;
-        }
-        if (have_tgt) S.slot[slot].target = tgt;
+        // ---- row end: publish this thread's state to the row slot ----
+        float s0, s1, s2, s3;
+        unpack2(fadd2(acc.sA, acc.sB), s0, s1);
+        unpack2(fadd2(acc.uA, acc.uB), s2, s3);
+        const int slot = (int)(rl % kSlots);
+        mbar_wait(&S.row_empty[slot], ((uint32_t)(rl / kSlots) & 1u) ^ 1u);
+        RowSlot &R = S.slot[slot];
+        R.m[ct] = acc.m;
+        R.s[ct] = s0 + s1;
+        R.u[ct] = s2 + s3;
+        if (have_tgt) R.target = tgt;
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.row_full[slot]);
-
-        if (epi) {
-            float sv[6];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
-            mbar_wait(&S.row_full[slot], slot_par);
-            Online tot{S.slot[slot].m[0], S.slot[slot].s[0], S.slot[slot].u[0]};
-#pragma unroll
-            for (int w = 1; w < kConsumerWarps; ++w)
-                tot = online_merge(tot, Online{S.slot[slot].m[w], S.slot[slot].s[w], S.slot[slot].u[w]});
-            const float target = S.slot[slot].target;
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&S.row_empty[slot]);
-                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-                row_epilogue<MODE>(p, b, t, L, y, tot, target, sv, wh, S.wacc[warp]);
-            }
-        }
-        b = bn; t = tn; y = yn;
     }
-    if (MODE == kModeLoss) finish_partials(p, S.wacc, kConsumerWarps, ct, kConsumers, 1);
 }
 
 // ---------------------------------------------------------------- generic kernel

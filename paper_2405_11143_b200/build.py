@@ -39,8 +39,11 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile liborl.so.  `defines` (e.g. ["ORL_K1_STAGES=8"]) and `out` build a
+    tuning variant under another name (tools/k1_tune.py)."""
+    lib = out or LIB
+    if not force and not defines and not needs_build():
         return LIB
     nccl = nccl_root()
     nvcc = os.environ.get("NVCC", "nvcc")
@@ -48,13 +51,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
            *sources(), "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
            "-Xlinker", "-rpath", "-Xlinker", os.path.join(nccl, "lib"),
-           "-o", LIB + ".tmp"]
+           *[f"-D{d}" for d in defines], "-o", lib + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

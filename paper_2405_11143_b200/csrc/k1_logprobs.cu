@@ -36,17 +36,39 @@
 
 namespace orl {
 
-constexpr int kConsumerWarps = 8;
+// Launch shape (tunable at build time; defaults are the measured best, DESIGN 5.1).
+#ifndef ORL_K1_CONSUMER_WARPS
+#define ORL_K1_CONSUMER_WARPS 16
+#endif
+#ifndef ORL_K1_CHUNK
+#define ORL_K1_CHUNK 32768
+#endif
+#ifndef ORL_K1_STAGES
+#define ORL_K1_STAGES 6
+#endif
+#ifndef ORL_K1_MINBLOCKS
+#define ORL_K1_MINBLOCKS 1
+#endif
+#ifndef ORL_K1_EPI_WARPS
+#define ORL_K1_EPI_WARPS 2
+#endif
+constexpr int kConsumerWarps = ORL_K1_CONSUMER_WARPS;
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kProducerWarp = kConsumerWarps;      // warp 8: TMA issue
-constexpr int kEpilogueWarp = kConsumerWarps + 1;  // warp 9: merge + fp64 epilogue
-constexpr int kThreads = kConsumers + 64;
-constexpr int kChunk = 16384;  // bytes per TMA stage
-constexpr int kStages = 6;
-constexpr int kSlots = 3;      // row-partial ring (consumers -> epilogue warp)
-constexpr int kRowInfo = 8;    // row-info ring (producer -> consumers), >= kStages + 1
-constexpr int kVecPerThread = kChunk / 16 / kConsumers;  // 4 x 16 B per thread per chunk
-static_assert(kVecPerThread == 4, "chunk processing is written for 4 vectors per thread");
+constexpr int kProducerWarp = kConsumerWarps;      // TMA issue
+constexpr int kEpilogueWarp = kConsumerWarps + 1;  // first of the merge + fp64 epilogue warps
+constexpr int kEpiWarps = ORL_K1_EPI_WARPS;         // rows alternate between them
+constexpr int kThreads = kConsumers + 32 + 32 * kEpiWarps;
+constexpr int kChunk = ORL_K1_CHUNK;  // bytes per TMA stage
+constexpr int kStages = ORL_K1_STAGES;
+// Row-partial ring (consumers -> epilogue warps).  Row rl uses slot rl % kSlots
+// and epilogue warp rl % kEpiWarps; kSlots is a multiple of kEpiWarps so every
+// slot is always drained by the same warp, in order (parity waits stay exact).
+constexpr int kSlots = kEpiWarps * (kEpiWarps == 1 ? 3 : 2);
+constexpr int kRowInfo = 16;   // row-info ring (producer -> consumers), >= kStages + 1
+constexpr int kVecPerThread = kChunk / 16 / kConsumers;  // 16-byte vectors per thread per chunk
+constexpr int kW = 4 * kVecPerThread;                    // 32-bit words per thread per chunk
+static_assert(kVecPerThread >= 1 && kChunk % (16 * kConsumers) == 0, "chunk must split evenly");
+static_assert((kW & (kW - 1)) == 0, "words per thread must be a power of two");
 static_assert(kRowInfo >= kStages + 1, "row-info ring must outrun the stage ring");
 
 // Every consumer thread's online state for one row, plus the target logit.
@@ -64,7 +86,7 @@ struct __align__(128) K1Smem {
     uint64_t row_empty[kSlots];
     int32_t row_y[kRowInfo];
     RowSlot slot[kSlots];
-    double wacc[kNumPartials];
+    double wacc[kEpiWarps][kNumPartials];
 };
 
 size_t k1_tma_smem_bytes(int B) { return sizeof(K1Smem) + sizeof(int32_t) * (size_t)(B + 32); }
@@ -300,11 +322,11 @@ __device__ __forceinline__ uint64_t bf16x2_to_f32x2(uint32_t w) {
 
 // Number of element pairs held in 16 raw 32-bit words.
 template <typename Tin> struct Words;
-template <> struct Words<uint16_t> { static constexpr int kPairs = 16; };
-template <> struct Words<float> { static constexpr int kPairs = 8; };
+template <> struct Words<uint16_t> { static constexpr int kPairs = kW; };
+template <> struct Words<float> { static constexpr int kPairs = kW / 2; };
 
 template <typename Tin>
-__device__ __forceinline__ uint64_t pair_at(const uint32_t (&w)[16], int q) {
+__device__ __forceinline__ uint64_t pair_at(const uint32_t (&w)[kW], int q) {
     if (sizeof(Tin) == 2) return bf16x2_to_f32x2(w[q]);
     uint64_t r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(w[2 * q]), "r"(w[2 * q + 1]));
@@ -312,15 +334,21 @@ __device__ __forceinline__ uint64_t pair_at(const uint32_t (&w)[16], int q) {
 }
 
 // Accumulate every pair of the chunk against the current m (no max, no clamp).
-template <typename Tin, bool ENT>
-__device__ __forceinline__ void acc_words(ThreadAcc &a, const uint32_t (&w)[16], uint64_t c2p) {
+// POLY = k > 0: every k-th pair takes the FMA-pipe polynomial instead of MUFU.
+template <typename Tin, bool ENT, int POLY>
+__device__ __forceinline__ void acc_words(ThreadAcc &a, const uint32_t (&w)[kW], uint64_t c2p) {
     const uint64_t nm = pack2(-a.m, -a.m);
 #pragma unroll
     for (int q = 0; q < Words<Tin>::kPairs; ++q) {
         const uint64_t tt = ffma2(pair_at<Tin>(w, q), c2p, nm);
-        float t0, t1;
-        unpack2(tt, t0, t1);
-        const uint64_t e = pack2(ex2(t0), ex2(t1));
+        uint64_t e;
+        if (POLY > 0 && (q % POLY) == POLY - 1) {
+            e = poly_ex2x2(tt);
+        } else {
+            float t0, t1;
+            unpack2(tt, t0, t1);
+            e = pack2(ex2(t0), ex2(t1));
+        }
         if (q & 1) {
             a.sB = fadd2(a.sB, e);
             if (ENT) a.uB = ffma2(e, tt, a.uB);
@@ -336,22 +364,23 @@ __device__ __forceinline__ void acc_words(ThreadAcc &a, const uint32_t (&w)[16],
 // (an element more than 64 log2-units above m), produced a non-finite moment
 // (-inf logits in the entropy moment) or saw NaN.
 template <typename Tin, bool ENT>
-__device__ __forceinline__ void exact_words(ThreadAcc &a, uint32_t (&w)[16], float c2, uint64_t c2p) {
+__device__ __forceinline__ void exact_words(ThreadAcc &a, uint32_t (&w)[kW], float c2, uint64_t c2p) {
     float cm;
     if (sizeof(Tin) == 2) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) w[q] = hmax2_nan(w[q], kNegClampBf16x2);
-        uint32_t mx[8];
+        for (int q = 0; q < kW; ++q) w[q] = hmax2_nan(w[q], kNegClampBf16x2);
+        uint32_t mx[kW];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mx[q] = hmax2_nan(w[q], w[q + 8]);
+        for (int q = 0; q < kW; ++q) mx[q] = w[q];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) mx[q] = hmax2_nan(mx[q], mx[q + 4]);
-        mx[0] = hmax2_nan(hmax2_nan(mx[0], mx[2]), hmax2_nan(mx[1], mx[3]));
+        for (int h = kW / 2; h >= 1; h >>= 1)
+#pragma unroll
+            for (int q = 0; q < h; ++q) mx[q] = hmax2_nan(mx[q], mx[q + h]);
         cm = fmax_nan(bf16lo(mx[0]), bf16hi(mx[0]));
     } else {
         cm = kNegClampF32;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < kW; ++q) {
             const float f = fmax_nan(__uint_as_float(w[q]), kNegClampF32);
             w[q] = __float_as_uint(f);
             cm = fmax_nan(cm, f);
@@ -368,7 +397,7 @@ __device__ __forceinline__ void exact_words(ThreadAcc &a, uint32_t (&w)[16], flo
     a.sA = fmul2(r2, a.sA);
     a.sB = fmul2(r2, a.sB);
     a.m = mn;
-    acc_words<Tin, ENT>(a, w, c2p);
+    acc_words<Tin, ENT, 0>(a, w, c2p);
 }
 
 // True if the fast pass must be redone exactly.
@@ -389,10 +418,10 @@ __device__ __forceinline__ bool needs_redo(const ThreadAcc &a) {
 // Load this thread's 4 x 16 B of the chunk (ragged tail padded with a finite
 // very negative logit, so padding gives 2^t = 0 and 2^t t = 0).
 template <typename Tin, bool FULL>
-__device__ __forceinline__ void load_words(uint32_t (&w)[16], const uint8_t *sb, int ct, int nvec) {
+__device__ __forceinline__ void load_words(uint32_t (&w)[kW], const uint8_t *sb, int ct, int nvec) {
     const uint32_t pad = sizeof(Tin) == 2 ? kNegClampBf16x2 : __float_as_uint(kNegClampF32);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kVecPerThread; ++k) {
         const int vi = ct + k * kConsumers;
         uint4 v;
         if (FULL || vi < nvec) v = lds128(sb + vi * 16);
@@ -401,17 +430,15 @@ __device__ __forceinline__ void load_words(uint32_t (&w)[16], const uint8_t *sb,
     }
 }
 
-template <typename Tin, bool ENT, bool FULL>
-__device__ __forceinline__ void process_chunk(ThreadAcc &a, const uint8_t *sb, int ct, int nvec, bool first,
-                                              float c2, uint64_t c2p) {
-    uint32_t w[16];
-    load_words<Tin, FULL>(w, sb, ct, nvec);
+template <typename Tin, bool ENT, int POLY>
+__device__ __forceinline__ void process_words(ThreadAcc &a, uint32_t (&w)[kW], bool first, float c2,
+                                              uint64_t c2p) {
     if (first) {
         exact_words<Tin, ENT>(a, w, c2, c2p);
         return;
     }
     const ThreadAcc saved = a;
-    acc_words<Tin, ENT>(a, w, c2p);
+    acc_words<Tin, ENT, POLY>(a, w, c2p);
     if (needs_redo<ENT>(a)) {
         a = saved;
         exact_words<Tin, ENT>(a, w, c2, c2p);
@@ -419,8 +446,10 @@ __device__ __forceinline__ void process_chunk(ThreadAcc &a, const uint8_t *sb, i
 }
 
 // Warp-level variant for the TMA kernel (the epilogue warp owns the partials).
-__device__ void finish_partials_warp(const K1Params &p, const double *wacc, int lane) {
-    if (lane < kNumPartials) p.ws[(size_t)lane * p.ws_stride + blockIdx.x] = wacc[lane];
+__device__ void finish_partials_warp(const K1Params &p, const double (&wacc)[kNumPartials], int lane) {
+#pragma unroll
+    for (int c = 0; c < kNumPartials; ++c)
+        if (lane == c) p.ws[(size_t)c * p.ws_stride + blockIdx.x] = wacc[c];
     __threadfence();
     __syncwarp();
     unsigned last = 0;
@@ -439,8 +468,8 @@ __device__ void finish_partials_warp(const K1Params &p, const double *wacc, int 
 }
 
 // ---------------------------------------------------------------- TMA kernel
-template <typename Tin, int MODE>
-__global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
+template <typename Tin, int MODE, int POLY>
+__global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(const K1Params p) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     K1Smem &S = *reinterpret_cast<K1Smem *>(smem_raw);
     int32_t *cum = reinterpret_cast<int32_t *>(smem_raw + sizeof(K1Smem));
@@ -458,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
         }
         fence_mbar_init();
     }
-    if (tid < kNumPartials) S.wacc[tid] = 0.0;
+    if (tid < kEpiWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
     build_prefix(p, cum, warp_tot);  // contains __syncthreads
     const int64_t N = cum[p.B - 1];
     const int64_t row_bytes = p.row_bytes;
@@ -497,14 +526,16 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
         return;
     }
 
-    if (warp == kEpilogueWarp) {
-        // ===================== epilogue: merge 256 partials, fp64 per-row math ===
+    if (warp >= kEpilogueWarp) {
+        // ===================== epilogue: merge the partials, fp64 per-row math ===
+        const int ew = warp - kEpilogueWarp;  // rows rl with rl % kEpiWarps == ew
         double wh[4] = {0.0, 0.0, 0.0, 0.0};
         if (MODE == kModeLoss) {
             wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
         }
         const int nside = MODE == kModeLoss ? 6 : 2;
-        for (int64_t j = blockIdx.x, rl = 0; j < N; j += gridDim.x, ++rl) {
+        for (int64_t j = blockIdx.x + (int64_t)ew * gridDim.x, rl = ew; j < N;
+             j += (int64_t)kEpiWarps * gridDim.x, rl += kEpiWarps) {
             int b, t;
             locate_row(cum, p.B, j, b, t);
             const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
@@ -527,11 +558,23 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
             if (lane == 0) {
                 mbar_arrive(&S.row_empty[slot]);
                 const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc);
+                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew]);
             }
             __syncwarp();
         }
-        if (MODE == kModeLoss) finish_partials_warp(p, S.wacc, lane);
+        if (MODE == kModeLoss) {
+            if (kEpiWarps > 1) named_bar_sync(1, 32 * kEpiWarps);
+            if (ew == 0) {
+                double tot[kNumPartials];
+#pragma unroll
+                for (int c = 0; c < kNumPartials; ++c) {
+                    double v = 0.0;
+                    for (int e = 0; e < kEpiWarps; ++e) v += S.wacc[e][c];   // fixed order
+                    tot[c] = v;
+                }
+                finish_partials_warp(p, tot, lane);
+            }
+        }
         return;
     }
 
@@ -568,17 +611,17 @@ __global__ void __launch_bounds__(kThreads, 2) k1_tma_kernel(const K1Params p) {
                           : *reinterpret_cast<const float *>(sb + tin);
                 have_tgt = true;
             }
-            const bool first = off == 0;
-            if (bytes == kChunk) {
-                if (ent) process_chunk<Tin, true, true>(acc, sb, ct, kChunk >> 4, first, p.c2, c2p);
-                else process_chunk<Tin, false, true>(acc, sb, ct, kChunk >> 4, first, p.c2, c2p);
-            } else {
-                if (ent) process_chunk<Tin, true, false>(acc, sb, ct, bytes >> 4, first, p.c2, c2p);
-                else process_chunk<Tin, false, false>(acc, sb, ct, bytes >> 4, first, p.c2, c2p);
-            }
+            // copy this thread's 64 B to registers and hand the stage back to the
+            // producer before computing, so the ring keeps ~all stages in flight
+            uint32_t w[kW];
+            if (bytes == kChunk) load_words<Tin, true>(w, sb, ct, kChunk >> 4);
+            else load_words<Tin, false>(w, sb, ct, bytes >> 4);
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
+            const bool first = off == 0;
+            if (ent) process_words<Tin, true, POLY>(acc, w, first, p.c2, c2p);
+            else process_words<Tin, false, POLY>(acc, w, first, p.c2, c2p);
         }
         // ---- row end: publish this thread's state to the row slot ----
         float s0, s1, s2, s3;
@@ -671,34 +714,42 @@ __global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
 }
 
 // ---------------------------------------------------------------- launcher
+template <typename Tin, int MODE, int POLY>
+static cudaError_t launch_tma(const K1Params &p, int num_sms, cudaStream_t s) {
+    const int64_t N_upper = (int64_t)p.B * p.T;  // rows are counted on device; size by the bound
+    const size_t smem = k1_tma_smem_bytes(p.B);
+    auto kern = k1_tma_kernel<Tin, MODE, POLY>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t grid = (int64_t)num_sms * per_sm;
+    if (grid > N_upper) grid = N_upper;
+    if (grid > p.ws_stride) grid = p.ws_stride;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, kThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <typename Tin, int MODE>
 static cudaError_t launch_typed(const K1Params &p, bool tma, int num_sms, cudaStream_t s) {
-    const int64_t N_upper = (int64_t)p.B * p.T;  // rows are counted on device; size by the bound
+    const int64_t N_upper = (int64_t)p.B * p.T;
     if (tma) {
-        const size_t smem = k1_tma_smem_bytes(p.B);
-        cudaError_t e = cudaFuncSetAttribute(k1_tma_kernel<Tin, MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_tma_kernel<Tin, MODE>, kThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (per_sm < 1) return cudaErrorInvalidConfiguration;
-        int64_t grid = (int64_t)num_sms * per_sm;
-        if (grid > N_upper) grid = N_upper;
-        if (grid > p.ws_stride) grid = p.ws_stride;
-        if (grid < 1) grid = 1;
-        k1_tma_kernel<Tin, MODE><<<(unsigned)grid, kThreads, smem, s>>>(p);
-    } else {
-        const size_t smem = sizeof(int32_t) * (size_t)(p.B + 32);
-        cudaError_t e = cudaFuncSetAttribute(k1_generic_kernel<Tin, MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int64_t grid = (int64_t)num_sms * 4;
-        if (grid > N_upper) grid = N_upper;
-        if (grid > p.ws_stride) grid = p.ws_stride;
-        if (grid < 1) grid = 1;
-        k1_generic_kernel<Tin, MODE><<<(unsigned)grid, 256, smem, s>>>(p);
+        if (p.poly == 4) return launch_tma<Tin, MODE, 4>(p, num_sms, s);
+        if (p.poly == 8) return launch_tma<Tin, MODE, 8>(p, num_sms, s);
+        return launch_tma<Tin, MODE, 0>(p, num_sms, s);
     }
+    const size_t smem = sizeof(int32_t) * (size_t)(p.B + 32);
+    cudaError_t e = cudaFuncSetAttribute(k1_generic_kernel<Tin, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (int64_t)num_sms * 4;
+    if (grid > N_upper) grid = N_upper;
+    if (grid > p.ws_stride) grid = p.ws_stride;
+    if (grid < 1) grid = 1;
+    k1_generic_kernel<Tin, MODE><<<(unsigned)grid, 256, smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ static_assert(sizeof(ncclUniqueId) == ORL_UNIQUE_ID_BYTES, "unique id size");
 
 namespace {
 constexpr int kMaxWorld = 256;
+constexpr int kDefaultPoly = 0;
 thread_local std::string g_thread_err;
 }  // namespace
 
@@ -133,6 +134,10 @@ static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const o
     p.row_bytes = lg->V * p.elt;
     p.inv_temp = inv_temp;
     p.c2 = inv_temp * 1.4426950408889634f;
+    {
+        const char *e = getenv("ORL_K1_POLY");   // tuning knob: 0, 4 or 8
+        p.poly = e ? atoi(e) : kDefaultPoly;
+    }
     p.B = (int)rows->B;
     p.T = (int)rows->T;
     p.seq_offset = rows->seq_offset;

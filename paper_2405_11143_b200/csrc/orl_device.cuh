@@ -63,6 +63,34 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// 2^t for a packed pair on the FMA/ALU pipes (no MUFU): t clamped to
+// [-126, 127], Cody-Waite split t = j + f with j = rint(t) (magic-number
+// add), degree-5 polynomial for 2^f on [-1/2, 1/2] (max rel. error 2.3e-7 in
+// fp32 Horner, ~MUFU.EX2 accuracy), exponent added with one LEA per lane.
+// Used for a fixed fraction of the elements to offload the MUFU pipe.
+__device__ __forceinline__ uint64_t poly_ex2x2(uint64_t tt) {
+    float t0, t1;
+    unpack2(tt, t0, t1);
+    t0 = fminf(fmaxf(t0, -126.f), 127.f);
+    t1 = fminf(fmaxf(t1, -126.f), 127.f);
+    const uint64_t tc = pack2(t0, t1);
+    const uint64_t mag = pack2(12582912.f, 12582912.f);   // 1.5 * 2^23
+    const uint64_t r = fadd2(tc, mag);                     // low mantissa bits = rint(t)
+    const uint64_t jf = fadd2(r, pack2(-12582912.f, -12582912.f));
+    const uint64_t f = ffma2(jf, pack2(-1.f, -1.f), tc);  // t - j in [-1/2, 1/2]
+    uint64_t q = ffma2(pack2(1.3276358e-3f, 1.3276358e-3f), f, pack2(9.6755093e-3f, 9.6755093e-3f));
+    q = ffma2(q, f, pack2(5.5507135e-2f, 5.5507135e-2f));
+    q = ffma2(q, f, pack2(2.4022120e-1f, 2.4022120e-1f));
+    q = ffma2(q, f, pack2(6.9314694e-1f, 6.9314694e-1f));
+    q = ffma2(q, f, pack2(1.0000001f, 1.0000001f));
+    float q0, q1, r0, r1;
+    unpack2(q, q0, q1);
+    unpack2(r, r0, r1);
+    const uint32_t o0 = __float_as_uint(q0) + (__float_as_uint(r0) << 23);
+    const uint32_t o1 = __float_as_uint(q1) + (__float_as_uint(r1) << 23);
+    return pack2(__uint_as_float(o0), __uint_as_float(o1));
+}
+
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 

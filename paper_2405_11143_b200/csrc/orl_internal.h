@@ -26,6 +26,7 @@ struct K1Params {
     int elt;            // 2 (bf16) or 4 (fp32)
     float inv_temp;
     float c2;           // inv_temp * log2(e)
+    int poly;           // MUFU offload: every poly-th element pair uses the FMA-pipe exp2 (0 = off)
     int B, T;
     int64_t seq_offset;
     const int32_t *tokens, *lengths;

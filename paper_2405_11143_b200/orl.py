@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liborl.so")
+LIB_PATH = os.environ.get("ORL_LIB_PATH") or os.path.join(_PKG, "liborl.so")   # override: tuning builds
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2405_11143_b200.build` "
                       "(or __graft_entry__.build()); there is no CPU fallback")

@@ -1,0 +1,38 @@
+"""Build K1 launch-shape variants (here) and benchmark them (on the GPU box).
+
+    python tools/k1_tune.py build      # nvcc variants into build/tune/
+    python tools/k1_tune.py run        # k1_bench.py for each variant
+"""
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+VARIANTS = {
+    "w8_c16k_s6_b2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=16384", "ORL_K1_STAGES=6", "ORL_K1_MINBLOCKS=2"],
+    "w8_c8k_s12_b2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=8192", "ORL_K1_STAGES=12", "ORL_K1_MINBLOCKS=2"],
+    "w16_c32k_s6_b1": ["ORL_K1_CONSUMER_WARPS=16", "ORL_K1_CHUNK=32768", "ORL_K1_STAGES=6", "ORL_K1_MINBLOCKS=1"],
+    "w4_c8k_s12_b2": ["ORL_K1_CONSUMER_WARPS=4", "ORL_K1_CHUNK=8192", "ORL_K1_STAGES=12", "ORL_K1_MINBLOCKS=2"],
+    "w8_c8k_s10_b2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=8192", "ORL_K1_STAGES=10", "ORL_K1_MINBLOCKS=2"],
+    "w16_c16k_s12_b1": ["ORL_K1_CONSUMER_WARPS=16", "ORL_K1_CHUNK=16384", "ORL_K1_STAGES=12", "ORL_K1_MINBLOCKS=1"],
+}
+OUT = os.path.join(ROOT, "build", "tune")
+
+if sys.argv[1] == "build":
+    from paper_2405_11143_b200 import build
+    os.makedirs(OUT, exist_ok=True)
+    names = sys.argv[2:] or list(VARIANTS)
+    with ThreadPoolExecutor(len(names)) as ex:
+        list(ex.map(lambda n: build.build(force=True, defines=VARIANTS[n], out=os.path.join(OUT, f"liborl_{n}.so")), names))
+    print("built", names)
+else:
+    for n in VARIANTS:
+        so = os.path.join(OUT, f"liborl_{n}.so")
+        if not os.path.exists(so):
+            continue
+        env = dict(os.environ, ORL_LIB_PATH=so)
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "k1_bench.py"), "--kinds", "logp,logp+H,loss"],
+                             env=env, capture_output=True, text=True)
+        print(f"== {n}\n{out.stdout}{out.stderr[-500:] if out.returncode else ''}", flush=True)

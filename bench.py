@@ -209,18 +209,28 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     src = lambda role, s, e: logits[role][s:e]  # noqa: E731
     n_tok_rank = int(L.clamp(max=T).sum().item())
+    n_mb = len(range(0, B, mb))
 
-    # per-K1-launch event timing on the launching stream
-    events = []
+    # K1 timing on the launching stream: one event before the first launch of each
+    # pass (old / ref / actor) and one after its last launch, so the interval is the
+    # wall time of that pass's back-to-back K1 launches (PDL lets consecutive K1
+    # launches overlap their tail/prologue, so per-launch intervals would overlap).
+    events = []      # (tag, n_launches, start_event, end_event)
+    cur = {}
 
     def hook(tag):
-        a = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        if cur.get("tag") != tag:
+            a = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cur.update(tag=tag, start=a, n=0)
 
         def done():
-            b = torch.cuda.Event(enable_timing=True)
-            b.record(stream)
-            events.append((tag, a, b))
+            cur["n"] += 1
+            if cur["n"] == n_mb:
+                b = torch.cuda.Event(enable_timing=True)
+                b.record(stream)
+                events.append((tag, cur["n"], cur["start"], b))
+                cur.clear()
         return done
 
     def step(timing):
@@ -257,12 +267,12 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (K1) --------------------------------
     side = {"old": 8, "ref": 8 + 12, "new": 8 + 24 + 16}   # side bytes per token (DESIGN 5.1)
-    k1_ms = sum(a.elapsed_time(b) for _, a, b in events)
+    k1_ms = sum(a.elapsed_time(b) for _, _, a, b in events)
     k1_bytes = 0
-    for tag, _, _ in events:
-        k1_bytes += (mb * T) * (V * elt + side[tag])
+    for tag, n, _, _ in events:
+        k1_bytes += n * (mb * T) * (V * elt + side[tag])
     k1_bytes = k1_bytes * (n_tok_rank / (B * T))           # only valid rows are read
-    n_k1 = len(events)
+    n_k1 = sum(n for _, n, _, _ in events)
     achieved = k1_bytes / (k1_ms / 1e3) / 1e9
     peak, peak_src = _peaks()
     traffic = None

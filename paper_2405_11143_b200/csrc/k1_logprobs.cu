@@ -445,7 +445,10 @@ __device__ __forceinline__ void process_words(ThreadAcc &a, uint32_t (&w)[kW], b
     }
 }
 
-// Warp-level variant for the TMA kernel (the epilogue warp owns the partials).
+// Warp-level variant for the TMA kernel (epilogue warp 0 owns the partials).
+// The last CTA loads every CTA's partials at once (all loads in flight), then
+// sums each column in a fixed order: lane-strided CTA order, then a fixed
+// xor-shuffle tree.
 __device__ void finish_partials_warp(const K1Params &p, const double (&wacc)[kNumPartials], int lane) {
 #pragma unroll
     for (int c = 0; c < kNumPartials; ++c)
@@ -457,14 +460,26 @@ __device__ void finish_partials_warp(const K1Params &p, const double (&wacc)[kNu
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return;
     __threadfence();
-    for (int c = 0; c < kNumPartials; ++c) {
-        double v = 0.0;
-        for (int q = lane; q < (int)gridDim.x; q += 32) v += __ldcg(&p.ws[(size_t)c * p.ws_stride + q]);
+    double v[kNumPartials];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) p.acc[c] += v;
+    for (int c = 0; c < kNumPartials; ++c) v[c] = 0.0;
+    for (int q = lane; q < (int)gridDim.x; q += 32) {
+        double x[kNumPartials];
+#pragma unroll
+        for (int c = 0; c < kNumPartials; ++c) x[c] = __ldcg(&p.ws[(size_t)c * p.ws_stride + q]);
+#pragma unroll
+        for (int c = 0; c < kNumPartials; ++c) v[c] += x[c];
     }
-    if (lane == 0) *p.ticket = 0u;
+#pragma unroll
+    for (int c = 0; c < kNumPartials; ++c) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < kNumPartials; ++c) p.acc[c] += v[c];
+        *p.ticket = 0u;
+    }
 }
 
 // ---------------------------------------------------------------- TMA kernel
@@ -488,6 +503,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         fence_mbar_init();
     }
     if (tid < kEpiWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
+    // Programmatic dependent launch: let the next kernel in the stream start
+    // as our CTAs retire (it fills the SMs of this launch's tail).  Only the
+    // epilogue warps touch memory other kernels write or read, and they wait
+    // for the preceding grid first (griddepcontrol.wait below).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     build_prefix(p, cum, warp_tot);  // contains __syncthreads
     const int64_t N = cum[p.B - 1];
     const int64_t row_bytes = p.row_bytes;
@@ -529,6 +549,8 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     if (warp >= kEpilogueWarp) {
         // ===================== epilogue: merge the partials, fp64 per-row math ===
         const int ew = warp - kEpilogueWarp;  // rows rl with rl % kEpiWarps == ew
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        zero_masked(p, cum, lane + 32 * ew, 32 * kEpiWarps, MODE);
         double wh[4] = {0.0, 0.0, 0.0, 0.0};
         if (MODE == kModeLoss) {
             wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
@@ -579,8 +601,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     }
 
     // ========================= consumers (warps 0..7) ============================
-    const int ct = tid;  // 0..255
-    zero_masked(p, cum, ct, kConsumers, MODE);
+    const int ct = tid;  // 0..kConsumers-1
     const bool ent = MODE == kModeLoss || p.entropy != nullptr;
     const uint64_t c2p = pack2(p.c2, p.c2);
     int stage = 0;
@@ -729,8 +750,17 @@ static cudaError_t launch_tma(const K1Params &p, int num_sms, cudaStream_t s) {
     if (grid > N_upper) grid = N_upper;
     if (grid > p.ws_stride) grid = p.ws_stride;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kThreads, smem, s>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 template <typename Tin, int MODE>

@@ -434,8 +434,21 @@ template <typename Tin, bool ENT, int POLY>
 __device__ __forceinline__ void process_words(ThreadAcc &a, uint32_t (&w)[kW], bool first, float c2,
                                               uint64_t c2p) {
     if (first) {
-        exact_words<Tin, ENT>(a, w, c2, c2p);
-        return;
+        // Row start: seed m with the max of this thread's first 16-byte vector
+        // (cheap); the fast pass below redoes the chunk exactly if anything in
+        // it lies more than 64 log2-units above that seed.
+        float cm;
+        if (sizeof(Tin) == 2) {
+            const uint32_t m01 = hmax2_nan(hmax2_nan(w[0], kNegClampBf16x2), w[1]);
+            const uint32_t m23 = hmax2_nan(w[2], w[3]);
+            const uint32_t mx = hmax2_nan(m01, m23);
+            cm = fmax_nan(bf16lo(mx), bf16hi(mx));
+        } else {
+            cm = fmax_nan(fmax_nan(__uint_as_float(w[0]), __uint_as_float(w[1])),
+                          fmax_nan(__uint_as_float(w[2]), __uint_as_float(w[3])));
+            cm = fmax_nan(cm, kNegClampF32);
+        }
+        a.m = fmax_nan(cm * c2, kMInit);
     }
     const ThreadAcc saved = a;
     acc_words<Tin, ENT, POLY>(a, w, c2p);

@@ -121,8 +121,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
         "r"(bytes)
         : "memory");
 }
-// Wait until the phase with parity `parity` of `bar` has completed.
+// Wait until the phase with parity `parity` of `bar` has completed.  The
+// suspend-time hint lets the hardware park the warp until the phase flips
+// instead of re-polling (fewer issue slots and less power while starved).
+#ifndef ORL_MBAR_SUSPEND_NS
+#define ORL_MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if ORL_MBAR_SUSPEND_NS > 0
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(ORL_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
@@ -130,6 +144,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol;

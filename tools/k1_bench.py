@@ -1,15 +1,23 @@
 """K1-only microbenchmark: GB/s of orl_logprobs / orl_ppo_loss on resident bf16 logits.
 
-    python tools/k1_bench.py [--V 128256] [--rows 8192] [--iters 20]
+    python tools/k1_bench.py [--V 128256] [--iters 30] [--warm-seconds 0] [--repeat 1]
+    python tools/k1_bench.py --libs a.so,b.so ...   # interleave several liborl builds
+
+With --warm-seconds the GPU first runs the loss kernel back to back for that
+long (reaching its power/thermal steady state), then every (lib, kind) pair is
+timed `--repeat` times, interleaved, and the median is reported with the SM
+clock sampled during the run.
 """
 import argparse
+import ctypes
 import os
+import statistics
+import subprocess
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
-
-from paper_2405_11143_b200 import orl, synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--V", type=int, default=128256)
@@ -18,7 +26,24 @@ ap.add_argument("--mb", type=int, default=8)
 ap.add_argument("--nbuf", type=int, default=6)
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--kinds", default="logp,logp+H,loss,sum,copy")
+ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--warm-seconds", type=float, default=0.0)
+ap.add_argument("--libs", default="")
 a = ap.parse_args()
+
+libs = a.libs.split(",") if a.libs else [os.environ.get("ORL_LIB_PATH", "")]
+mods = []
+for path in libs:
+    # load each build as a separate binding module instance
+    if path:
+        os.environ["ORL_LIB_PATH"] = path
+    import importlib
+    import paper_2405_11143_b200.orl as orl_mod
+    orl_mod = importlib.reload(orl_mod)
+    mods.append((os.path.basename(path) or "liborl.so", orl_mod))
+
+from paper_2405_11143_b200 import synth  # noqa: E402
+
 dev = torch.device("cuda:0")
 B, T, V = a.mb * a.nbuf, a.T, a.V
 x = torch.randn(B, T, V, device=dev, dtype=torch.bfloat16)
@@ -26,14 +51,18 @@ tok = synth.tokens_for(B, T, V, 0).to(dev)
 L = torch.full((B,), T, dtype=torch.int32, device=dev)
 z = lambda: torch.zeros(B, T, device=dev)  # noqa: E731
 lp, ent, lo, adv, lpn, dl = z(), z(), z(), z(), z(), z()
-ctx = orl.Context(0)
-orl.orl_begin_iteration(ctx)
-orl.orl_advantages(ctx, L, adv, kind="rpp", shaped_reward=z())
-orl.orl_whiten_stats(ctx, True)
-cfg = orl.PPOConfig()
+y = torch.empty_like(x[: a.mb])
+ctxs = {}
+for name, orl in mods:
+    ctx = orl.Context(0)
+    orl.orl_begin_iteration(ctx)
+    orl.orl_advantages(ctx, L, adv, kind="rpp", shaped_reward=z())
+    orl.orl_whiten_stats(ctx, True)
+    ctxs[name] = (orl, ctx, orl.PPOConfig())
 
 
-def run(kind, i):
+def run(name, kind, i):
+    orl, ctx, cfg = ctxs[name]
     s = (i % a.nbuf) * a.mb
     xv = x[s:s + a.mb]
     if kind == "sum":            # torch reference: read-only streaming reduction
@@ -48,17 +77,38 @@ def run(kind, i):
         orl.orl_ppo_loss(ctx, tok, L, xv, cfg, lo, adv, lpn, seq_offset=s, entropy=ent, dloss_dlogp=dl)
 
 
-y = torch.empty_like(x[: a.mb])
-for kind in a.kinds.split(","):
-    for i in range(5):
-        run(kind, i)
-    torch.cuda.synchronize()
+def timed(name, kind):
+    for i in range(3):
+        run(name, kind, i)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(a.iters):
-        run(kind, i)
+        run(name, kind, i)
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.iters
+    return e0.elapsed_time(e1) / a.iters
+
+
+smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,temperature.gpu", "--format=csv,noheader,nounits",
+                        "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+if a.warm_seconds > 0:
+    t0 = time.time()
+    first = next(iter(ctxs))
+    while time.time() - t0 < a.warm_seconds:
+        timed(first, "loss")
+res = {}
+for r in range(a.repeat):
+    for name in ctxs:
+        for kind in a.kinds.split(","):
+            res.setdefault((name, kind), []).append(timed(name, kind))
+smi.terminate()
+out, _ = smi.communicate()
+clk = [float(l.split(",")[0]) for l in out.strip().splitlines() if l.strip()]
+pw = [float(l.split(",")[1]) for l in out.strip().splitlines() if l.strip()]
+for (name, kind), v in res.items():
+    ms = statistics.median(v)
     gb = a.mb * T * V * 2 / 1e9 * (2 if kind == "copy" else 1)
-    print(f"{kind:8s} V={V} rows={a.mb * T}: {ms * 1e3:8.1f} us/launch  {gb / ms * 1e3:8.1f} GB/s")
+    print(f"{name:28s} {kind:7s} V={V}: {ms * 1e3:8.1f} us/launch  {gb / ms * 1e3:8.1f} GB/s  "
+          f"(min {min(v) * 1e3:.1f} max {max(v) * 1e3:.1f})")
+if clk:
+    print(f"SM clock median {statistics.median(clk):.0f} MHz (min {min(clk):.0f}), power median {statistics.median(pw):.0f} W")

@@ -11,12 +11,11 @@ from concurrent.futures import ThreadPoolExecutor
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "w8_c16k_s6_b2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=16384", "ORL_K1_STAGES=6", "ORL_K1_MINBLOCKS=2"],
-    "w8_c8k_s12_b2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=8192", "ORL_K1_STAGES=12", "ORL_K1_MINBLOCKS=2"],
-    "w16_c32k_s6_b1": ["ORL_K1_CONSUMER_WARPS=16", "ORL_K1_CHUNK=32768", "ORL_K1_STAGES=6", "ORL_K1_MINBLOCKS=1"],
-    "w4_c8k_s12_b2": ["ORL_K1_CONSUMER_WARPS=4", "ORL_K1_CHUNK=8192", "ORL_K1_STAGES=12", "ORL_K1_MINBLOCKS=2"],
-    "w8_c8k_s10_b2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=8192", "ORL_K1_STAGES=10", "ORL_K1_MINBLOCKS=2"],
-    "w16_c16k_s12_b1": ["ORL_K1_CONSUMER_WARPS=16", "ORL_K1_CHUNK=16384", "ORL_K1_STAGES=12", "ORL_K1_MINBLOCKS=1"],
+    "default": [],
+    "c64k_s3": ["ORL_K1_CHUNK=65536", "ORL_K1_STAGES=3"],
+    "c32k_s5": ["ORL_K1_STAGES=5"],
+    "c64k_s3_susp": ["ORL_K1_CHUNK=65536", "ORL_K1_STAGES=3", "ORL_MBAR_SUSPEND_NS=10000"],
+    "c32k_s6_susp": ["ORL_MBAR_SUSPEND_NS=10000"],
 }
 OUT = os.path.join(ROOT, "build", "tune")
 

@@ -290,6 +290,11 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": int(k1_bytes / max(n_k1, 1)), "k1_share_of_step": round(k1_ms / (ms * args.steps), 4),
             "peak_source": peak_src}
 
+    # ---- NEXT-1: the backward pass dL/dlogits (separate leg, not in `value`) ----
+    next1 = None
+    if not args.no_next1 and world == 1:
+        next1 = run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok_rank)
+
     # ---- e2e: host buffers, H2D/D2H inside the timed region --------------------
     e2e = None
     if not args.no_e2e:
@@ -316,11 +321,54 @@ def run_ours(args):
                            "l2": "inputs larger than L2 (3 x %.1f GB logits per rank vs 126 MB L2)" % (B * T * V * elt / 1e9)},
                 "status": status, "stats": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in st.items()},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
+                "next1_logits_grad": next1,
                 "per_gpu_tokens_per_s": round(value / world, 1)}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok):
+    """Time the NEXT-1 backward pass (orl_logits_grad) over every micro-batch of
+    the actor logits: reads V*2 B and writes V*2 B per token.  Uses the per-token
+    lse / entropy / dloss_dlogp the timed steps left in `bufs`."""
+    from paper_2405_11143_b200 import orl
+
+    B, T, V = batch["tokens"].shape[0], c["T"], c["V"]
+    free = torch.cuda.mem_get_info()[0]
+    need = B * T * V * 2
+    if need > free - (4 << 30):
+        return {"skipped": f"needs {need / 1e9:.1f} GB for dlogits"}
+    dl = torch.empty(B, T, V, dtype=logits["new"].dtype, device=dev)
+    tok, L = batch["tokens"], batch["lengths"]
+
+    def once():
+        for s in range(0, B, mb):
+            e = min(B, s + mb)
+            orl.orl_logits_grad(ctx, tok, L, logits["new"][s:e], cfg.ppo, bufs.lse, bufs.entropy, bufs.dlogp,
+                                dl[s:e], seq_offset=s, inv_temp=cfg.inv_temp, stream=stream)
+
+    for _ in range(2):
+        once()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(3, args.steps // 4)
+    a.record(stream)
+    for _ in range(reps):
+        once()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    byts = n_tok * V * 2 * 2
+    peak, _ = _peaks()
+    del dl
+    torch.cuda.empty_cache()
+    return {"tokens_per_s": round(n_tok / (ms / 1e3), 1), "ms_per_pass": round(ms, 4),
+            "roofline": {"bound": "hbm", "achieved": round(byts / (ms / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(byts / (ms / 1e3) / 1e9 / peak, 4),
+                         "bytes": "V*2 read + V*2 written per valid token"},
+            "kernel": "k5_tma_kernel", "launches": len(range(0, B, mb)), "reps": reps}
 
 
 def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank):
@@ -414,6 +462,7 @@ def main():
     ap.add_argument("--ref-seqs", type=int, default=4, help="oracle sample size (sequences)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-next1", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

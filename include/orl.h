@@ -261,7 +261,30 @@ orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *ac
                         float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
                         const float *logp_ref, const float *adv, const float *ret,
                         const float *v_new, const float *v_old, float *logp_new,
-                        float *entropy, float *dloss_dlogp, float *dloss_dv, void *stream);
+                        float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
+                        void *stream);
+/* (lse, optional: the log-partition of the scaled actor logits, saved for
+ * orl_logits_grad.) */
+
+/* ---- NEXT-1: gradient w.r.t. the actor logits -------------------------- */
+
+/* One streaming pass over the actor logits of a micro-batch that writes
+ *   dL/dx_v = inv_temp * ( w (delta_{v,y} - p_v) + (c2/N) p_v (ln p_v + H) )
+ * for every valid row, where L is the minimised total of orl_finalize (Z12),
+ * p = softmax(inv_temp x), w = dloss_dlogp, and lse (the log-partition), H
+ * (entropy) and w are the per-token outputs the actor pass saved
+ * (orl_ppo_loss); N is the global token count of orl_whiten_stats and c2 is
+ * cfg->c2.  P:197 "gradient computation"; SURVEY 8(f) NEXT-1.
+ * dlogits (device) has the actor's dtype and V, element strides
+ * (out_stride_b, out_stride_t) relative to the micro-batch's first sequence,
+ * and must not alias any logits still being read.  zero_masked = 1 also
+ * writes zeros into the rows with t >= L_b.  Outputs are rounded to the
+ * logits dtype (bf16: round-to-nearest-even). */
+orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
+                           float inv_temp, const orl_ppo_cfg *cfg, const float *lse,
+                           const float *entropy, const float *dloss_dlogp, void *dlogits,
+                           int64_t out_stride_b, int64_t out_stride_t, int zero_masked,
+                           void *stream);
 
 /* ---- S10 + C2: statistics ---------------------------------------------- */
 

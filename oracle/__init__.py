@@ -76,6 +76,8 @@ def _load():
                                         f64, f64, f64, f64, f64, i32, i32, f64, f64,
                                         P, P, P, P, P, P]
         lib.oracle_ppo_loss.restype = None
+        lib.oracle_logits_grad_row.argtypes = [P, i64, i64, f64, f64, f64, P]
+        lib.oracle_logits_grad_row.restype = None
         lib.oracle_stats.argtypes = [P, f64, f64, f64, i32, P]
         lib.oracle_stats.restype = i32
         _lib = lib
@@ -115,6 +117,8 @@ def logprobs(logits, tokens, lengths, inv_temp=1.0, bf16=None):
     lib = _load()
     if bf16 is None:
         bf16 = logits.dtype == np.uint16
+    dt = 0 if bf16 else (2 if logits.dtype == np.float64 else 1)
+    assert dt != 1 or logits.dtype == np.float32, logits.dtype
     item = logits.itemsize
     assert logits.strides[2] == item, "V must be unit stride"
     B, T, V = logits.shape
@@ -123,7 +127,7 @@ def logprobs(logits, tokens, lengths, inv_temp=1.0, bf16=None):
     outs = {k: np.zeros((B, T)) for k in ("logp", "entropy", "lse", "gathered")}
     cnt = np.zeros(2, dtype=np.int64)
     base = logits.__array_interface__["data"][0]
-    lib.oracle_logprobs(ctypes.c_void_p(base), 0 if bf16 else 1, B, T, V, sb, st,
+    lib.oracle_logprobs(ctypes.c_void_p(base), dt, B, T, V, sb, st,
                         _p(tokens), _p(lengths), float(inv_temp),
                         _p(outs["logp"]), _p(outs["entropy"]), _p(outs["lse"]),
                         _p(outs["gathered"]), cnt.ctypes.data, cnt.ctypes.data + 8)
@@ -265,6 +269,30 @@ def stats(sums, c1=0.0, c2=0.0, beta_loss=0.0, kl_in_loss=False):
     d["n_guard"] = int(sums[9])
     d["n_nonfinite"] = int(sums[10])
     return d
+
+
+# --------------------------------------------------------------------------- NEXT-1
+def logits_grad_row(x, y, inv_temp, w, a):
+    """dL/dx of one valid row (raw logits x, fp64): NEXT-1."""
+    lib = _load()
+    x = _f64(x)
+    g = np.zeros(x.size)
+    lib.oracle_logits_grad_row(_p(x), x.size, int(y), float(inv_temp), float(w), float(a), _p(g))
+    return g
+
+
+def logits_grad(logits, tokens, lengths, dlogp, inv_temp, c2, n_global):
+    """[B,T,V] dL/dlogits (zeros on masked rows); `logits` as for logprobs()."""
+    B, T, V = logits.shape
+    out = np.zeros((B, T, V))
+    a = c2 / n_global
+    for b in range(B):
+        for t in range(int(lengths[b])):
+            row = logits[b, t]
+            x = (row.astype(np.uint32) << 16).view(np.float32).astype(np.float64) \
+                if row.dtype == np.uint16 else row.astype(np.float64)
+            out[b, t] = logits_grad_row(x, tokens[b, t], inv_temp, dlogp[b, t], a)
+    return out
 
 
 from .pipeline import pipeline  # noqa: E402  (composition of the stages above)

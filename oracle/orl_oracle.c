@@ -28,6 +28,7 @@
 
 #define ORACLE_DTYPE_BF16 0
 #define ORACLE_DTYPE_F32 1
+#define ORACLE_DTYPE_F64 2 /* test inputs (finite differences) */
 
 /* bf16 -> fp64 is exact: a bf16 is the top 16 bits of an IEEE fp32. */
 static double bf16_bits_to_double(uint16_t h)
@@ -42,6 +43,8 @@ static double load_logit(const void *logits, int dtype, int64_t off)
 {
     if (dtype == ORACLE_DTYPE_BF16)
         return bf16_bits_to_double(((const uint16_t *)logits)[off]);
+    if (dtype == ORACLE_DTYPE_F64)
+        return ((const double *)logits)[off];
     return (double)((const float *)logits)[off];
 }
 
@@ -448,4 +451,31 @@ int oracle_stats(const double *sums, double c1, double c2, double beta_loss,
     out[8] = sums[8] / N;
     out[9] = out[1] + c1 * out[2] - c2 * out[3] + (kl_in_loss ? beta_loss * out[4] : 0.0);
     return 0;
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-1  gradient of the minimised total (Z12) w.r.t. the actor's raw
+ *     logits, for one valid row ("gradient computation"):
+ *       z = inv_temp x,  p = softmax(z),  ln p_v = z_v - lse,
+ *       H = -sum_v p_v ln p_v,
+ *       dL/dz_v = w (delta_vy - p_v) + a p_v (ln p_v + H),   a = c2/N
+ *       dL/dx_v = inv_temp dL/dz_v
+ *     w = dL/dlogp_new (the per-token derivative of oracle_ppo_loss).  The
+ *     entropy part is the derivative of -c2 mean(H); the policy and KL-loss
+ *     parts reach the logits only through logp_new = z_y - lse.
+ * ---------------------------------------------------------------------- */
+void oracle_logits_grad_row(const double *x, int64_t V, int64_t y, double inv_temp, double w,
+                            double a, double *grad)
+{
+    double *z = (double *)calloc((size_t)(V > 0 ? V : 1), sizeof(double));
+    for (int64_t v = 0; v < V; ++v) z[v] = inv_temp * x[v];
+    double lse, logp, H;
+    oracle_row_logsoftmax(z, V, y, &lse, &logp, &H);
+    for (int64_t v = 0; v < V; ++v) {
+        double lp = z[v] - lse;
+        double p = exp(lp);
+        double dz = w * ((v == y ? 1.0 : 0.0) - p) + a * p * (lp + H);
+        grad[v] = inv_temp * dz;
+    }
+    free(z);
 }

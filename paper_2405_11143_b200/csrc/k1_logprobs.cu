@@ -615,7 +615,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 
     // ========================= consumers (warps 0..7) ============================
     const int ct = tid;  // 0..kConsumers-1
+#ifdef ORL_K1_ALWAYS_ENT
+    const bool ent = true;
+#else
     const bool ent = MODE == kModeLoss || p.entropy != nullptr;
+#endif
     const uint64_t c2p = pack2(p.c2, p.c2);
     int stage = 0;
     uint32_t phase = 0;

@@ -1,0 +1,339 @@
+// k5_logits_grad.cu -- K5 (NEXT-1): gradient of the minimised PPO total w.r.t.
+// the actor's raw logits, one streaming pass (read logits, write dlogits).
+//
+//   z = inv_temp x,  p = softmax(z),  H = -sum_v p_v ln p_v,  logp_y = z_y - lse
+//   dL/dz_v = w (delta_vy - p_v) + a p_v (ln p_v + H),   a = c2 / N
+//   dL/dx_v = inv_temp dL/dz_v
+// with w = dL/dlogp_new from the actor pass (orl_ppo_loss's dloss_dlogp) and
+// lse, H saved by that pass ("gradient computation"; SURVEY
+// 8(f) NEXT-1).
+//
+// Same streaming skeleton as K1 (persistent CTA per SM, producer warp with a
+// 1-D TMA bulk-copy ring), but no row reduction: each consumer thread turns its
+// 16-byte vectors into gradient vectors and writes them with st.global.v4;
+// the per-row constants (y, lse, H, w) are published by the producer.  The
+// target element's delta term is patched by its owner thread afterwards.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "orl_device.cuh"
+#include "orl_internal.h"
+
+namespace orl {
+
+namespace k5 {
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;
+constexpr int kChunk = 32768;
+constexpr int kStages = 6;
+constexpr int kRowInfo = 16;
+constexpr int kVPT = kChunk / 16 / kConsumers;  // 4
+static_assert(kRowInfo >= kStages + 1, "row-info ring must outrun the stage ring");
+
+struct RowInfo {
+    int32_t y;
+    float l2;   // lse * log2(e)
+    float A1;   // inv_temp * a * ln2
+    float A0;   // inv_temp * (a H - w)
+    float wt;   // inv_temp * w   (the delta term at v = y)
+    int32_t pad[3];
+};
+
+struct __align__(128) Smem {
+    uint8_t stage[kStages][kChunk];
+    uint64_t full[kStages];
+    uint64_t empty[kStages];
+    RowInfo info[kRowInfo];
+};
+}  // namespace k5
+
+size_t k5_smem_bytes(int B) { return sizeof(k5::Smem) + sizeof(int32_t) * (size_t)(B + 32); }
+
+__device__ void k5_build_prefix(const K5Params &p, int32_t *cum, int32_t *warp_tot) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int per = (p.B + nthr - 1) / nthr;
+    const int beg = min(p.B, tid * per), end = min(p.B, beg + per);
+    int local = 0;
+    for (int b = beg; b < end; ++b) {
+        int L = p.lengths[p.seq_offset + b];
+        L = L < 0 ? 0 : (L > p.T ? p.T : L);
+        local += L;
+        cum[b] = local;
+    }
+    const int lane = tid & 31, warp = tid >> 5;
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int w = 0; w < (nthr + 31) / 32; ++w) {
+            int v = warp_tot[w];
+            warp_tot[w] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    const int excl = warp_tot[warp] + incl - local;
+    for (int b = beg; b < end; ++b) cum[b] += excl;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void stg128(void *p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t f32x2_to_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// Row constants from the saved forward quantities.
+__device__ __forceinline__ k5::RowInfo row_info(const K5Params &p, int64_t gi, int y, float a) {
+    k5::RowInfo r;
+    const float lse = __ldg(p.lse + gi), H = __ldg(p.entropy + gi), w = __ldg(p.dlogp + gi);
+    r.y = y;
+    r.l2 = lse * kLog2e;
+    r.A1 = p.inv_temp * a * (float)kLn2;
+    r.A0 = p.inv_temp * (a * H - w);
+    r.wt = p.inv_temp * w;
+    return r;
+}
+
+template <typename Tin>
+__global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params p) {
+    using namespace k5;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw + sizeof(Smem));
+    int32_t *warp_tot = cum + p.B;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    k5_build_prefix(p, cum, warp_tot);
+    const int64_t N = cum[p.B - 1];
+    const int64_t row_bytes = p.V * (int64_t)sizeof(Tin);
+    // The saved per-token inputs come from the actor pass (a previous kernel).
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const float a = (float)(p.c2 / p.whiten[0]);   // c2 / N_global
+
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t j = blockIdx.x, rl = 0; j < N; j += gridDim.x, ++rl) {
+                int b, t;
+                locate_row(cum, p.B, j, b, t);
+                const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
+                const RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), a);
+                const char *src = p.base + ((int64_t)b * p.stride_b + (int64_t)t * p.stride_t) * sizeof(Tin);
+                for (int64_t off = 0; off < row_bytes; off += kChunk) {
+                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
+                    mbar_wait(&S.empty[stage], phase ^ 1u);
+                    if (off == 0) S.info[rl % kRowInfo] = ri;
+                    mbar_arrive_expect_tx(&S.full[stage], bytes);
+                    tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+        return;
+    }
+
+    const int ct = tid;
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint64_t c2p = pack2(p.c2x, p.c2x);
+    for (int64_t j = blockIdx.x, rl = 0; j < N; j += gridDim.x, ++rl) {
+        int b, t;
+        locate_row(cum, p.B, j, b, t);
+        Tin *orow = reinterpret_cast<Tin *>(p.out) + (int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t;
+        RowInfo ri;
+        uint64_t nl2 = 0, A1p = 0, A0p = 0;
+        for (int64_t off = 0; off < row_bytes; off += kChunk) {
+            const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
+            const int nvec = bytes >> 4;
+            mbar_wait(&S.full[stage], phase);
+            if (off == 0) {
+                ri = S.info[rl % kRowInfo];
+                nl2 = pack2(-ri.l2, -ri.l2);
+                A1p = pack2(ri.A1, ri.A1);
+                A0p = pack2(ri.A0, ri.A0);
+            }
+            const uint8_t *sb = S.stage[stage];
+            // owner of the target element reads it before the stage is released
+            const int64_t ybyte = (int64_t)ri.y * (int64_t)sizeof(Tin);
+            const bool own_y = ri.y >= 0 && (int64_t)ri.y < p.V && ybyte >= off && ybyte < off + bytes &&
+                               (((int)(ybyte - off) >> 4) % kConsumers) == ct;
+            float xy = 0.f;
+            if (own_y) {
+                const uint8_t *q = sb + (ybyte - off);
+                xy = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(q)) << 16)
+                                      : *reinterpret_cast<const float *>(q);
+            }
+            uint4 v[kVPT];
+#pragma unroll
+            for (int k = 0; k < kVPT; ++k) {
+                const int vi = ct + k * kConsumers;
+                if (vi < nvec) v[k] = lds128(sb + vi * 16);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1u; }
+            char *obase = reinterpret_cast<char *>(orow) + off;
+#pragma unroll
+            for (int k = 0; k < kVPT; ++k) {
+                const int vi = ct + k * kConsumers;
+                if (vi >= nvec) continue;
+                const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                uint32_t o[4];
+                if (sizeof(Tin) == 2) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t x = pack2(bf16lo(w4[q]), bf16hi(w4[q]));
+                        const uint64_t t2 = ffma2(x, c2p, nl2);          // (z - lse) log2 e
+                        float t0, t1;
+                        unpack2(t2, t0, t1);
+                        const uint64_t pr = pack2(ex2(t0), ex2(t1));     // p
+                        const uint64_t g = fmul2(pr, ffma2(A1p, t2, A0p));
+                        float g0, g1;
+                        unpack2(g, g0, g1);
+                        o[q] = f32x2_to_bf16x2(g0, g1);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        uint64_t x;
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(w4[2 * q]), "r"(w4[2 * q + 1]));
+                        const uint64_t t2 = ffma2(x, c2p, nl2);
+                        float t0, t1;
+                        unpack2(t2, t0, t1);
+                        const uint64_t pr = pack2(ex2(t0), ex2(t1));
+                        const uint64_t g = fmul2(pr, ffma2(A1p, t2, A0p));
+                        float g0, g1;
+                        unpack2(g, g0, g1);
+                        o[2 * q] = __float_as_uint(g0);
+                        o[2 * q + 1] = __float_as_uint(g1);
+                    }
+                }
+                stg128(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+            }
+            // delta term at v = y: the owner of y's vector rewrites that element
+            if (own_y) {
+                const float t2 = fmaf(xy, p.c2x, -ri.l2);
+                const float g = ex2(t2) * fmaf(ri.A1, t2, ri.A0) + ri.wt;
+                if (sizeof(Tin) == 2) {
+                    const uint32_t hb = f32x2_to_bf16x2(g, 0.f) & 0xffffu;
+                    asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + ri.y), "h"((unsigned short)hb) : "memory");
+                } else {
+                    reinterpret_cast<float *>(orow)[ri.y] = g;
+                }
+            }
+        }
+    }
+    // zero the masked rows of the output block (t >= L_b)
+    if (p.zero_masked) {
+        const int64_t total = (int64_t)p.B * p.T;
+        for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
+            const int b = (int)(q / p.T), t = (int)(q % p.T);
+            const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+            if (t < L) continue;
+            char *orow = reinterpret_cast<char *>(p.out) +
+                         ((int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t) * (int64_t)sizeof(Tin);
+            for (int64_t o = (int64_t)ct * 16; o < row_bytes; o += (int64_t)kConsumers * 16)
+                stg128(orow + o, make_uint4(0u, 0u, 0u, 0u));
+        }
+    }
+}
+
+// Generic path (unaligned rows): one row per CTA iteration, scalar accesses.
+template <typename Tin>
+__global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw);
+    int32_t *warp_tot = cum + p.B;
+    k5_build_prefix(p, cum, warp_tot);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const float a = (float)(p.c2 / p.whiten[0]);
+    const int64_t total = (int64_t)p.B * p.T;
+    for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
+        const int b = (int)(q / p.T), t = (int)(q % p.T);
+        const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+        Tin *orow = reinterpret_cast<Tin *>(p.out) + (int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t;
+        const Tin *row = reinterpret_cast<const Tin *>(p.base) + (int64_t)b * p.stride_b + (int64_t)t * p.stride_t;
+        if (t >= L) {
+            if (p.zero_masked)
+                for (int64_t v = threadIdx.x; v < p.V; v += blockDim.x) orow[v] = Tin(0);
+            continue;
+        }
+        const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
+        const k5::RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), a);
+        for (int64_t v = threadIdx.x; v < p.V; v += blockDim.x) {
+            float x;
+            if (sizeof(Tin) == 2) x = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(row)[v]) << 16);
+            else x = reinterpret_cast<const float *>(row)[v];
+            const float t2 = fmaf(x, p.c2x, -ri.l2);
+            float g = ex2(t2) * fmaf(ri.A1, t2, ri.A0);
+            if (v == ri.y) g += ri.wt;
+            if (sizeof(Tin) == 2) {
+                const uint32_t hb = f32x2_to_bf16x2(g, 0.f) & 0xffffu;
+                reinterpret_cast<uint16_t *>(orow)[v] = (uint16_t)hb;
+            } else {
+                reinterpret_cast<float *>(orow)[v] = g;
+            }
+        }
+    }
+}
+
+template <typename Tin>
+static cudaError_t launch_k5_typed(const K5Params &p, bool tma, int num_sms, cudaStream_t s) {
+    const int64_t rows = (int64_t)p.B * p.T;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.stream = s;
+    if (tma) {
+        const size_t smem = k5_smem_bytes(p.B);
+        cudaError_t e = cudaFuncSetAttribute(k5_tma_kernel<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int64_t grid = num_sms;
+        if (grid > rows) grid = rows;
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(k5::kThreads);
+        cfg.dynamicSmemBytes = smem;
+        return cudaLaunchKernelEx(&cfg, k5_tma_kernel<Tin>, p);
+    }
+    const size_t smem = sizeof(int32_t) * (size_t)(p.B + 32);
+    cudaError_t e = cudaFuncSetAttribute(k5_generic_kernel<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (int64_t)num_sms * 4;
+    if (grid > rows) grid = rows;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    return cudaLaunchKernelEx(&cfg, k5_generic_kernel<Tin>, p);
+}
+
+cudaError_t launch_k5(const K5Params &p, bool tma, int num_sms, cudaStream_t s) {
+    return p.elt == 2 ? launch_k5_typed<uint16_t>(p, tma, num_sms, s) : launch_k5_typed<float>(p, tma, num_sms, s);
+}
+
+}  // namespace orl

@@ -383,7 +383,8 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
                                    float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
                                    const float *logp_ref, const float *adv, const float *ret,
                                    const float *v_new, const float *v_old, float *logp_new,
-                                   float *entropy, float *dloss_dlogp, float *dloss_dv, void *stream) {
+                                   float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
+                                   void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
     orl_status st = validate_rows_logits(ctx, rows, actor, inv_temp);
     if (st) return st;
@@ -394,7 +395,7 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
     if (dloss_dv && critic == 0) return fail(ctx, ORL_E_INVALID_ARG, "dloss_dv needs the critic arrays");
     if (!aligned4(logp_old) || !aligned4(logp_ref) || !aligned4(adv) || !aligned4(ret) || !aligned4(v_new) ||
         !aligned4(v_old) || !aligned4(logp_new) || !aligned4(entropy) || !aligned4(dloss_dlogp) ||
-        !aligned4(dloss_dv))
+        !aligned4(dloss_dv) || !aligned4(lse))
         return fail(ctx, ORL_E_ALIGN, "per-token arrays must be 4-byte aligned");
     if (!(cfg->eps_low >= 0.0 && cfg->eps_low < 1.0) || !(cfg->eps_high >= 0.0) ||
         !std::isfinite(cfg->eps_high) || !std::isfinite(cfg->eps_value) || !std::isfinite(cfg->c1) ||
@@ -409,6 +410,7 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
     fill_common(ctx, p, rows, actor, inv_temp);
     p.logp = logp_new;
     p.entropy = entropy;
+    p.lse = lse;
     p.logp_old = logp_old;
     p.logp_ref = logp_ref;
     p.adv = adv;
@@ -426,6 +428,56 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
     p.kl_loss_est = cfg->kl_loss_est;
     p.kl_in_loss = cfg->kl_in_loss;
     CUDA_TRY(ctx, launch_k1(p, tma_eligible(actor), kModeLoss, ctx->num_sms, as_stream(stream)));
+    ctx->launches += 1;
+    return ORL_OK;
+}
+
+// ------------------------------------------------------------------ NEXT-1
+extern "C" orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
+                                      float inv_temp, const orl_ppo_cfg *cfg, const float *lse,
+                                      const float *entropy, const float *dloss_dlogp, void *dlogits,
+                                      int64_t out_stride_b, int64_t out_stride_t, int zero_masked,
+                                      void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    orl_status st = validate_rows_logits(ctx, rows, actor, inv_temp);
+    if (st) return st;
+    if (!cfg || !lse || !entropy || !dloss_dlogp || !dlogits)
+        return fail(ctx, ORL_E_INVALID_ARG, "cfg, lse, entropy, dloss_dlogp and dlogits are required");
+    if (!aligned4(lse) || !aligned4(entropy) || !aligned4(dloss_dlogp))
+        return fail(ctx, ORL_E_ALIGN, "per-token arrays must be 4-byte aligned");
+    if (out_stride_t < actor->V || out_stride_b < 0)
+        return fail(ctx, ORL_E_SHAPE, "dlogits strides (%lld, %lld) invalid", (long long)out_stride_b,
+                    (long long)out_stride_t);
+    if (!std::isfinite(cfg->c2)) return fail(ctx, ORL_E_INVALID_ARG, "cfg->c2 not finite");
+    if (!ctx->have_whiten) return fail(ctx, ORL_E_STATE, "orl_logits_grad before orl_whiten_stats");
+    if ((st = set_device(ctx))) return st;
+    K5Params p;
+    std::memset(&p, 0, sizeof p);
+    p.base = static_cast<const char *>(actor->ptr);
+    p.out = dlogits;
+    p.V = actor->V;
+    p.stride_b = actor->stride_b;
+    p.stride_t = actor->stride_t;
+    p.out_stride_b = out_stride_b;
+    p.out_stride_t = out_stride_t;
+    p.elt = actor->dtype == ORL_BF16 ? 2 : 4;
+    p.inv_temp = inv_temp;
+    p.c2x = inv_temp * 1.4426950408889634f;
+    p.c2 = cfg->c2;
+    p.B = (int)rows->B;
+    p.T = (int)rows->T;
+    p.seq_offset = rows->seq_offset;
+    p.tokens = rows->tokens;
+    p.lengths = rows->lengths;
+    p.lse = lse;
+    p.entropy = entropy;
+    p.dlogp = dloss_dlogp;
+    p.whiten = ctx->d_whiten;
+    p.zero_masked = zero_masked ? 1 : 0;
+    const int64_t elt = p.elt;
+    const bool tma = tma_eligible(actor) && (reinterpret_cast<uintptr_t>(dlogits) % 16 == 0) &&
+                     ((out_stride_t * elt) % 16 == 0) && ((out_stride_b * elt) % 16 == 0);
+    CUDA_TRY(ctx, launch_k5(p, tma, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
     return ORL_OK;
 }

@@ -57,6 +57,25 @@ cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaSt
 // Shared-memory footprint of the TMA kernel for B sequences.
 size_t k1_tma_smem_bytes(int B);
 
+// K5 (NEXT-1): dL/dlogits streaming pass.
+struct K5Params {
+    const char *base;  // actor logits of the micro-batch's first sequence
+    void *out;         // dlogits, same dtype and V
+    int64_t V, stride_b, stride_t, out_stride_b, out_stride_t;  // elements
+    int elt;
+    float inv_temp;
+    float c2x;         // inv_temp * log2(e)
+    double c2;         // entropy coefficient of the total loss
+    int B, T;
+    int64_t seq_offset;
+    const int32_t *tokens, *lengths;
+    const float *lse, *entropy, *dlogp;  // saved by the actor pass
+    const double *whiten;                // device [4]: N_global first
+    int zero_masked;
+};
+cudaError_t launch_k5(const K5Params &p, bool tma, int num_sms, cudaStream_t s);
+size_t k5_smem_bytes(int B);
+
 struct K3Params {
     int B, T, kind, G;
     double gamma, lambda;

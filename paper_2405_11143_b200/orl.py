@@ -78,13 +78,15 @@ _lib.orl_logprobs.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), 
 _lib.orl_advantages.argtypes = [_P, _I64, _I64, _P, _I32, _F64, _F64, _I32, _P, _P, _P, _P, _P, _P, _P]
 _lib.orl_whiten_stats.argtypes = [_P, _I32, _P]
 _lib.orl_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
-                              ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+                              ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+_lib.orl_logits_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32, ctypes.POINTER(PpoCfg),
+                                 _P, _P, _P, _P, _I64, _I64, _I32, _P]
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
 for _f in ("orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
            "orl_advantages", "orl_whiten_stats", "orl_ppo_loss", "orl_finalize",
-           "orl_export_partials", "orl_import_partials"):
+           "orl_export_partials", "orl_import_partials", "orl_logits_grad"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -211,13 +213,26 @@ def orl_whiten_stats(ctx: Context, whiten: bool, stream=None):
 
 def orl_ppo_loss(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
                  seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
-                 entropy=None, dloss_dlogp=None, dloss_dv=None, stream=None):
+                 entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, stream=None):
     B, T = logits.shape[0], tokens.shape[1]
     rows, lg, c = _rows(tokens, lengths, B, T, seq_offset), _logits(logits), cfg.c()
     st = _lib.orl_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
                            _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
-                           _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(dloss_dlogp),
+                           _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
                            _ptr(dloss_dv), _stream(stream))
+    return ctx.check(st)
+
+
+def orl_logits_grad(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, lse, entropy, dloss_dlogp, dlogits, *,
+                    seq_offset=0, inv_temp=1.0, zero_masked=True, stream=None):
+    """NEXT-1: dL/dlogits of the micro-batch logits[0:B] into dlogits[0:B] (same dtype/shape view)."""
+    B, T = logits.shape[0], tokens.shape[1]
+    if dlogits.dtype != logits.dtype or dlogits.shape[2] != logits.shape[2] or dlogits.stride(2) != 1:
+        raise ValueError("dlogits must be a [B,T,V] view with the logits dtype and unit V stride")
+    rows, lg, c = _rows(tokens, lengths, B, T, seq_offset), _logits(logits), cfg.c()
+    st = _lib.orl_logits_grad(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
+                              _ptr(lse), _ptr(entropy), _ptr(dloss_dlogp), _ptr(dlogits), dlogits.stride(0),
+                              dlogits.stride(1), int(bool(zero_masked)), _stream(stream))
     return ctx.check(st)
 
 

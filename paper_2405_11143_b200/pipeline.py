@@ -52,6 +52,7 @@ class Buffers:
         f = lambda: torch.zeros(B, T, dtype=torch.float32, device=device)  # noqa: E731
         self.logp_old, self.logp_ref, self.kl, self.shaped = f(), f(), f(), f()
         self.adv, self.ret, self.logp_new, self.entropy = f(), f(), f(), f()
+        self.lse = f()
         self.dlogp = f() if grads else None
         self.dv = f() if grads else None
         self.keep = torch.zeros(max(1, B // max(1, group_size)), dtype=torch.uint8, device=device)
@@ -67,10 +68,13 @@ def microbatches(B: int, mb: int):
 
 def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers, logits: LogitsSource,
                   mb: int, stream: Optional[torch.cuda.Stream] = None, finalize: bool = True,
-                  on_k1: Optional[Callable[[str], object]] = None):
+                  on_k1: Optional[Callable[[str], object]] = None,
+                  grad_sink: Optional[Callable[[int, int], torch.Tensor]] = None):
     """One iteration on this rank.  `batch` holds device tensors tokens [B,T] int32,
     lengths [B] int32, seq_reward [B] f32 and (critic) values_old / values_new [B,T].
-    `on_k1(tag)` (optional) is called around every K1 launch for timing hooks."""
+    `on_k1(tag)` (optional) is called around every K1 launch for timing hooks.
+    `grad_sink(s, e)` (optional, NEXT-1) returns the [e-s, T, V] dlogits view the
+    backward pass (orl_logits_grad) writes for micro-batch [s, e)."""
     tok, L = batch["tokens"], batch["lengths"]
     B, T = tok.shape
     mbs = microbatches(B, mb)
@@ -106,8 +110,15 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
                           seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
                           ret=bufs.ret if critic else None, v_new=batch["values_new"] if critic else None,
                           v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
-                          dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None, stream=stream)
+                          lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
+                          stream=stream)
         if h: h()
+    if grad_sink is not None:                          # NEXT-1: dL/dlogits
+        for s, e in mbs:
+            h = hook("grad")
+            _orl.orl_logits_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.lse, bufs.entropy, bufs.dlogp,
+                                 grad_sink(s, e), seq_offset=s, inv_temp=cfg.inv_temp, stream=stream)
+            if h: h()
     if not finalize:
         return None
     return _orl.orl_finalize(ctx, cfg.ppo, dev_out=bufs.stats_dev, stream=stream)  # S10 + C2

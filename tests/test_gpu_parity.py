@@ -430,3 +430,49 @@ def test_shard_emulation_matches_single_rank(kind, n):
         torch.testing.assert_close(bb.dlogp, b1.dlogp[s:e], rtol=1e-6, atol=1e-12)
     for cx in ctxs + [one]:
         cx.close()
+
+
+# --------------------------------------------------------------------------- NEXT-1
+def _check_grad(g, o, mask_rows, rel, name, w, H, a, inv_temp):
+    """|gpu - oracle| <= rel |o| + 1e-5 S_row, S_row = inv_temp (|w| + a (1 + H)) bounds the
+    size of the two terms of dL/dz_v before they cancel (fp32 w, H, lse carry ~1e-7)."""
+    for (b, t) in zip(*np.nonzero(mask_rows)):
+        gr, orow = g[b, t].astype(np.float64), o[b, t]
+        S = inv_temp * (abs(w[b, t]) + a * (1.0 + abs(H[b, t])))
+        err = np.abs(gr - orow)
+        lim = rel * np.abs(orow) + 1e-5 * S
+        assert np.all(err <= lim), (name, b, t, float((err / lim).max()))
+        assert abs(gr.sum()) <= (1e-4 if rel < 1e-3 else 1e-2) * np.abs(gr).sum() + 1e-6 * S  # shift invariance
+    for (b, t) in zip(*np.nonzero(~mask_rows)):
+        assert np.all(g[b, t] == 0), (name, "masked row not zero")
+
+
+@pytest.mark.parametrize("dtype,V,inv_temp", [("f32", 32, 1.0), ("f32", 1000, 1 / 0.7), ("bf16", 4096, 1.0),
+                                               ("bf16", 50257, 1.0)])
+def test_next1_logits_grad_parity(ctx, dtype, V, inv_temp):
+    """dL/dlogits from the GPU backward pass vs the oracle's, fed the GPU's own
+    saved per-token quantities (dloss_dlogp) -- stage isolation."""
+    B, T = 4, 24
+    c = dict(synth.CONFIGS["llama8b"], c2=0.01, V=V, inv_temp=inv_temp)
+    if dtype == "f32":
+        batch = synth.make_batch(7, B, T, V, "f32", "stress", "tiny")
+        g = _to_dev(batch)
+    else:
+        g = _gpu_batch(7, B, T, V, "mixed", mode="stress")
+    cfg = PathConfig.from_synth(c)
+    cfg.inv_temp = inv_temp
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    dl = torch.full((B, T, V), 3.0, dtype=tdt, device=DEV)
+    bufs = Buffers(B, T, DEV)
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    status, st = run_iteration(ctx, g, cfg, bufs, src, mb=3, grad_sink=lambda s, e: dl[s:e])
+    torch.cuda.synchronize()
+    assert status == "ORL_OK"
+    npb = synth.batch_to_numpy(g)
+    m = parity.valid_mask(npb["lengths"], T)
+    o = oracle.logits_grad(npb["logits_new"], npb["tokens"], npb["lengths"], _np(bufs.dlogp).astype(np.float64),
+                           inv_temp, 0.01, float(m.sum()))
+    gg = dl.float().cpu().numpy()
+    H = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"], inv_temp)["entropy"]
+    _check_grad(gg, o, m, 2e-5 if dtype == "f32" else 8e-3, f"{dtype}-{V}", _np(bufs.dlogp), H,
+                0.01 / float(m.sum()), inv_temp)

@@ -471,3 +471,43 @@ def test_pipeline_shard_invariance(kind):
         for k, v in g1["stats"].items():
             if isinstance(v, float):
                 assert abs(v - gn["stats"][k]) <= 1e-12 * max(1.0, abs(v)), (k, v, gn["stats"][k])
+
+
+# ----------------------------------------------------------------------------- NEXT-1
+@pytest.mark.parametrize("k", ["k1", "k2", "k3"])
+def test_next1_logits_grad_finite_differences(k):
+    """dL/dlogits of the whole oracle chain (logprobs -> ppo_loss -> stats total)
+    by central differences in fp64, against oracle.logits_grad (NEXT-1)."""
+    B, T, V = 2, 3, 6
+    L = np.array([3, 2], np.int32)
+    x = rng.normal(0, 1.5, (B, T, V))
+    tok = rng.integers(0, V, (B, T)).astype(np.int32)
+    lo = rng.normal(-1.5, 0.3, (B, T))
+    lr = lo + rng.normal(0, 0.2, (B, T))
+    A = rng.normal(0, 1, (B, T))
+    inv_temp, c2, beta = 1 / 0.8, 0.05, 0.1
+
+    def total(xn):
+        o = oracle.logprobs(xn, tok, L, inv_temp)
+        res = oracle.ppo_loss(L, o["logp"], lo, A, logp_ref=lr, entropy=o["entropy"], eps_low=0.2,
+                              eps_high=0.28, beta_loss=beta, kl_est=k, kl_in_loss=True)
+        st = oracle.stats(res["sums"], c2=c2, beta_loss=beta, kl_in_loss=True)
+        return st["total_loss"], res
+
+    _, res = total(x)
+    g = oracle.logits_grad(x, tok, L, res["dlogp"], inv_temp, c2, float(L.sum()))
+    h = 1e-6
+    for b in range(B):
+        for t in range(T):
+            for v in range(V):
+                xp, xm = x.copy(), x.copy()
+                xp[b, t, v] += h
+                xm[b, t, v] -= h
+                fd = (total(xp)[0] - total(xm)[0]) / (2 * h)
+                assert abs(fd - g[b, t, v]) < 2e-8, (b, t, v, fd, g[b, t, v])
+                if t >= L[b]:
+                    assert g[b, t, v] == 0.0
+    # each valid row's gradient sums to 0 (softmax shift invariance)
+    for b in range(B):
+        for t in range(L[b]):
+            assert abs(g[b, t].sum()) < 1e-13

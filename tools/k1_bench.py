@@ -50,15 +50,18 @@ x = torch.randn(B, T, V, device=dev, dtype=torch.bfloat16)
 tok = synth.tokens_for(B, T, V, 0).to(dev)
 L = torch.full((B,), T, dtype=torch.int32, device=dev)
 z = lambda: torch.zeros(B, T, device=dev)  # noqa: E731
-lp, ent, lo, adv, lpn, dl = z(), z(), z(), z(), z(), z()
+lp, ent, lo, adv, lpn, dl, lse = z(), z(), z(), z(), z(), z(), z()
 y = torch.empty_like(x[: a.mb])
+dlog = torch.empty_like(x[: a.mb])
 ctxs = {}
 for name, orl in mods:
     ctx = orl.Context(0)
     orl.orl_begin_iteration(ctx)
     orl.orl_advantages(ctx, L, adv, kind="rpp", shaped_reward=z())
     orl.orl_whiten_stats(ctx, True)
-    ctxs[name] = (orl, ctx, orl.PPOConfig())
+    cfg = orl.PPOConfig(c2=0.01)
+    orl.orl_ppo_loss(ctx, tok, L, x[: a.mb], cfg, lo, adv, lpn, entropy=ent, lse=lse, dloss_dlogp=dl)
+    ctxs[name] = (orl, ctx, cfg)
 
 
 def run(name, kind, i):
@@ -69,6 +72,8 @@ def run(name, kind, i):
         return xv.sum(dtype=torch.float32)
     if kind == "copy":           # torch reference: the MEASURED_PEAKS copy (read + write bytes)
         return y.copy_(xv)
+    if kind == "grad":           # NEXT-1 backward: read logits + write dlogits
+        return orl.orl_logits_grad(ctx, tok, L, xv, cfg, lse, ent, dl, dlog, seq_offset=s)
     if kind == "logp":
         orl.orl_logprobs(ctx, tok, L, xv, lp, seq_offset=s)
     elif kind == "logp+H":
@@ -107,7 +112,7 @@ clk = [float(l.split(",")[0]) for l in out.strip().splitlines() if l.strip()]
 pw = [float(l.split(",")[1]) for l in out.strip().splitlines() if l.strip()]
 for (name, kind), v in res.items():
     ms = statistics.median(v)
-    gb = a.mb * T * V * 2 / 1e9 * (2 if kind == "copy" else 1)
+    gb = a.mb * T * V * 2 / 1e9 * (2 if kind in ("copy", "grad") else 1)
     print(f"{name:28s} {kind:7s} V={V}: {ms * 1e3:8.1f} us/launch  {gb / ms * 1e3:8.1f} GB/s  "
           f"(min {min(v) * 1e3:.1f} max {max(v) * 1e3:.1f})")
 if clk:

@@ -12,10 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "default": [],
-    "c64k_s3": ["ORL_K1_CHUNK=65536", "ORL_K1_STAGES=3"],
-    "c32k_s5": ["ORL_K1_STAGES=5"],
-    "c64k_s3_susp": ["ORL_K1_CHUNK=65536", "ORL_K1_STAGES=3", "ORL_MBAR_SUSPEND_NS=10000"],
-    "c32k_s6_susp": ["ORL_MBAR_SUSPEND_NS=10000"],
+    "always_ent": ["ORL_K1_ALWAYS_ENT=1"],
 }
 OUT = os.path.join(ROOT, "build", "tune")
 

@@ -297,6 +297,19 @@ orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits 
 orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
                         double *dev_out, void *stream);
 
+/* ---- NEXT-3: adaptive KL coefficient and early stop (host only) -------- */
+
+/* Host scalar update, no device work ("adaptive KL penalty
+ * coefficients" and "early stopping criteria based on KL divergence
+ * thresholds"):
+ *   beta <- beta * (1 + clip(observed_kl / target - 1, -0.5, 0.5) / horizon)
+ *   *early_stop = observed_kl > max_kl
+ * observed_kl is a statistic of orl_finalize chosen by the caller (e.g. kl for
+ * the reference KL, approx_kl_old for the old-policy KL).  Requires beta >= 0,
+ * target > 0, horizon > 0, finite observed_kl (ORL_E_INVALID_ARG otherwise). */
+orl_status orl_kl_controller_step(double *beta, double target, double horizon, double observed_kl,
+                                  double max_kl, int *early_stop);
+
 /* ---- collective boundary hooks (testing / custom transports) ----------- */
 
 /* which = 0: this rank's whitening partial (double[4]: count, mean, M2, 0),

@@ -78,6 +78,8 @@ def _load():
         lib.oracle_ppo_loss.restype = None
         lib.oracle_logits_grad_row.argtypes = [P, i64, i64, f64, f64, f64, P]
         lib.oracle_logits_grad_row.restype = None
+        lib.oracle_kl_controller_step.argtypes = [P, f64, f64, f64, f64]
+        lib.oracle_kl_controller_step.restype = i32
         lib.oracle_stats.argtypes = [P, f64, f64, f64, i32, P]
         lib.oracle_stats.restype = i32
         _lib = lib
@@ -293,6 +295,13 @@ def logits_grad(logits, tokens, lengths, dlogp, inv_temp, c2, n_global):
                 if row.dtype == np.uint16 else row.astype(np.float64)
             out[b, t] = logits_grad_row(x, tokens[b, t], inv_temp, dlogp[b, t], a)
     return out
+
+
+def kl_controller_step(beta, target, horizon, observed, max_kl):
+    """NEXT-3: (new beta, early_stop)."""
+    b = np.array([float(beta)])
+    stop = _load().oracle_kl_controller_step(_p(b), float(target), float(horizon), float(observed), float(max_kl))
+    return float(b[0]), bool(stop)
 
 
 from .pipeline import pipeline  # noqa: E402  (composition of the stages above)

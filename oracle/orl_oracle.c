@@ -479,3 +479,18 @@ void oracle_logits_grad_row(const double *x, int64_t V, int64_t y, double inv_te
     }
     free(z);
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT-3  adaptive KL coefficient and early stop:
+ *   beta <- beta (1 + clip(observed/target - 1, -0.5, 0.5) / horizon)
+ *   early_stop = observed > max_kl
+ * ---------------------------------------------------------------------- */
+int oracle_kl_controller_step(double *beta, double target, double horizon, double observed,
+                              double max_kl)
+{
+    double e = observed / target - 1.0;
+    if (e < -0.5) e = -0.5;
+    if (e > 0.5) e = 0.5;
+    *beta = *beta * (1.0 + e / horizon);
+    return observed > max_kl;
+}

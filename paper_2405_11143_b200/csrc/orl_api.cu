@@ -543,6 +543,20 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
     return ORL_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-3
+extern "C" orl_status orl_kl_controller_step(double *beta, double target, double horizon, double observed_kl,
+                                             double max_kl, int *early_stop) {
+    if (!beta || !early_stop) return fail(nullptr, ORL_E_INVALID_ARG, "beta/early_stop is NULL");
+    if (!(*beta >= 0.0) || !(target > 0.0) || !(horizon > 0.0) || !std::isfinite(observed_kl))
+        return fail(nullptr, ORL_E_INVALID_ARG, "kl controller: beta=%g target=%g horizon=%g observed=%g", *beta,
+                    target, horizon, observed_kl);
+    double e = observed_kl / target - 1.0;
+    e = e < -0.5 ? -0.5 : (e > 0.5 ? 0.5 : e);
+    *beta = *beta * (1.0 + e / horizon);
+    *early_stop = observed_kl > max_kl ? 1 : 0;
+    return ORL_OK;
+}
+
 // ------------------------------------------------------------------ hooks
 extern "C" orl_status orl_export_partials(orl_ctx *ctx, int which, double *host_out, void *stream) {
     if (!ctx || !host_out) return fail(ctx, ORL_E_INVALID_ARG, "ctx/host_out is NULL");

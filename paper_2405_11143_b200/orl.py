@@ -84,7 +84,8 @@ _lib.orl_logits_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
-for _f in ("orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
+_lib.orl_kl_controller_step.argtypes = [ctypes.POINTER(_F64), _F64, _F64, _F64, _F64, ctypes.POINTER(ctypes.c_int)]
+for _f in ("orl_kl_controller_step", "orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
            "orl_advantages", "orl_whiten_stats", "orl_ppo_loss", "orl_finalize",
            "orl_export_partials", "orl_import_partials", "orl_logits_grad"):
     getattr(_lib, _f).restype = ctypes.c_int
@@ -263,3 +264,13 @@ def orl_import_partials(ctx: Context, which: int, host_all, stream=None):
     world = arr.shape[0]
     ctx.check(_lib.orl_import_partials(ctx.h, int(which), arr.ctypes.data_as(ctypes.c_void_p), world,
                                        _stream(stream)))
+
+
+def orl_kl_controller_step(beta: float, target: float, horizon: float, observed_kl: float, max_kl: float):
+    """NEXT-3 (host only): returns (new beta, early_stop)."""
+    b, stop = ctypes.c_double(beta), ctypes.c_int(0)
+    st = _lib.orl_kl_controller_step(ctypes.byref(b), float(target), float(horizon), float(observed_kl),
+                                     float(max_kl), ctypes.byref(stop))
+    if st:
+        raise OrlError(st, _lib.orl_last_error(None).decode())
+    return b.value, bool(stop.value)

@@ -96,3 +96,18 @@ def test_product_never_imports_oracle():
     text = open(os.path.join(ROOT, "oracle", "orl_oracle.c")).read()
     includes = re.findall(r"^#include\s*[<\"]([^>\"]+)", text, re.M)
     assert includes and all(i in ("math.h", "stdint.h", "stdlib.h", "string.h") for i in includes), includes
+
+
+def test_next3_kl_controller_host_matches_oracle(lib):
+    """Host-only ABI call (no GPU) against the oracle on random inputs."""
+    import numpy as np
+    import oracle
+    from paper_2405_11143_b200 import orl
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        beta, target, horizon = rng.uniform(0, 1), rng.uniform(1e-3, 0.1), rng.uniform(1, 100)
+        obs, mx = rng.uniform(0, 0.3), rng.uniform(0, 0.3)
+        assert orl.orl_kl_controller_step(beta, target, horizon, obs, mx) == oracle.kl_controller_step(
+            beta, target, horizon, obs, mx)
+    with pytest.raises(orl.OrlError):
+        orl.orl_kl_controller_step(0.1, 0.0, 1.0, 0.1, 1.0)

@@ -511,3 +511,13 @@ def test_next1_logits_grad_finite_differences(k):
     for b in range(B):
         for t in range(L[b]):
             assert abs(g[b, t].sum()) < 1e-13
+
+
+# ----------------------------------------------------------------------------- NEXT-3
+def test_next3_kl_controller_spec_examples(golden):
+    for c in golden("spec_examples.json")["kl_controller"]:
+        b, stop = oracle.kl_controller_step(c["beta"], c["target"], c["horizon"], c["observed"], c["max_kl"])
+        assert abs(b - c["beta_out"]) < 1e-15 and stop == c["early_stop"]
+    # the proportional error is clipped to +-0.5: far-off observations move beta by 1 +- 0.5/horizon
+    assert oracle.kl_controller_step(1.0, 0.01, 2.0, 1e6, 1e9)[0] == 1.25
+    assert oracle.kl_controller_step(1.0, 0.01, 2.0, 0.0, 1e9)[0] == 0.75

@@ -89,7 +89,54 @@ struct __align__(128) K1Smem {
     double wacc[kEpiWarps][kNumPartials];
 };
 
-size_t k1_tma_smem_bytes(int B) { return sizeof(K1Smem) + sizeof(int32_t) * (size_t)(B + 32); }
+size_t k1_tma_smem_bytes(int B) {
+    return sizeof(K1Smem) + sizeof(int32_t) * (size_t)((B > kSmemPrefixMax ? 0 : B) + 32);
+}
+
+// Large micro-batches: the inclusive prefix of the clamped lengths is built once
+// in global memory by one CTA (the same block scan) and read by every CTA.
+__global__ void __launch_bounds__(1024) lengths_prefix_kernel(const int32_t *lengths, int B, int T, int32_t *cum,
+                                                              unsigned long long *err) {
+    __shared__ int32_t warp_tot[32];
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int per = (B + nthr - 1) / nthr;
+    const int beg = min(B, tid * per), end = min(B, beg + per);
+    int local = 0, bad = 0;
+    for (int b = beg; b < end; ++b) {
+        int L = lengths[b];
+        if (L < 0 || L > T) ++bad;
+        L = L < 0 ? 0 : (L > T ? T : L);
+        local += L;
+        cum[b] = local;
+    }
+    if (bad && err) atomicAdd(&err[2], (unsigned long long)bad);
+    const int lane = tid & 31, warp = tid >> 5;
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int w = 0; w < nthr / 32; ++w) {
+            int v = warp_tot[w];
+            warp_tot[w] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    const int excl = warp_tot[warp] + incl - local;
+    for (int b = beg; b < end; ++b) cum[b] += excl;
+}
+
+cudaError_t launch_lengths_prefix(const int32_t *lengths, int B, int T, int32_t *cum, unsigned long long *err,
+                                  cudaStream_t s) {
+    lengths_prefix_kernel<<<1, 1024, 0, s>>>(lengths, B, T, cum, err);
+    return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------- prologue
 // Inclusive prefix of the clamped lengths of the micro-batch into cum[0..B).
@@ -500,8 +547,8 @@ template <typename Tin, int MODE, int POLY>
 __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(const K1Params p) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     K1Smem &S = *reinterpret_cast<K1Smem *>(smem_raw);
-    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw + sizeof(K1Smem));
-    int32_t *warp_tot = cum + p.B;  // 32 ints after the prefix
+    int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw + sizeof(K1Smem));
+    int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);  // 32 ints after the prefix
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if (tid == 0) {
@@ -521,7 +568,12 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     // epilogue warps touch memory other kernels write or read, and they wait
     // for the preceding grid first (griddepcontrol.wait below).
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    build_prefix(p, cum, warp_tot);  // contains __syncthreads
+    const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
+    if (p.cum_global) {  // written by the prefix kernel just before us (PDL: wait for it)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        __syncthreads();
+    }
+    else build_prefix(p, cum_s, warp_tot);  // contains __syncthreads
     const int64_t N = cum[p.B - 1];
     const int64_t row_bytes = p.row_bytes;
 
@@ -686,11 +738,16 @@ __global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
     __shared__ double wacc[1][kNumPartials];
     __shared__ float sm_m[8], sm_s[8], sm_u[8];
     __shared__ float sm_tgt;
-    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw);
-    int32_t *warp_tot = cum + p.B;
+    int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw);
+    int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < kNumPartials) wacc[0][tid] = 0.0;
-    build_prefix(p, cum, warp_tot);
+    const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
+    if (p.cum_global) {  // written by the prefix kernel just before us (PDL: wait for it)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        __syncthreads();
+    }
+    else build_prefix(p, cum_s, warp_tot);
     const int64_t N = cum[p.B - 1];
     zero_masked(p, cum, tid, 256, MODE);
     double wh[4] = {0.0, 0.0, 0.0, 0.0};
@@ -788,7 +845,7 @@ static cudaError_t launch_typed(const K1Params &p, bool tma, int num_sms, cudaSt
         if (p.poly == 8) return launch_tma<Tin, MODE, 8>(p, num_sms, s);
         return launch_tma<Tin, MODE, 0>(p, num_sms, s);
     }
-    const size_t smem = sizeof(int32_t) * (size_t)(p.B + 32);
+    const size_t smem = sizeof(int32_t) * (size_t)((p.cum_global ? 0 : p.B) + 32);
     cudaError_t e = cudaFuncSetAttribute(k1_generic_kernel<Tin, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

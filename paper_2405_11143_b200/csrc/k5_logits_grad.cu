@@ -49,7 +49,9 @@ struct __align__(128) Smem {
 };
 }  // namespace k5
 
-size_t k5_smem_bytes(int B) { return sizeof(k5::Smem) + sizeof(int32_t) * (size_t)(B + 32); }
+size_t k5_smem_bytes(int B) {
+    return sizeof(k5::Smem) + sizeof(int32_t) * (size_t)((B > kSmemPrefixMax ? 0 : B) + 32);
+}
 
 __device__ void k5_build_prefix(const K5Params &p, int32_t *cum, int32_t *warp_tot) {
     const int tid = threadIdx.x, nthr = blockDim.x;
@@ -114,8 +116,8 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
     using namespace k5;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw + sizeof(Smem));
-    int32_t *warp_tot = cum + p.B;
+    int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw + sizeof(Smem));
+    int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -124,7 +126,12 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
         }
         fence_mbar_init();
     }
-    k5_build_prefix(p, cum, warp_tot);
+    const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
+    if (p.cum_global) {  // written by the prefix kernel just before us (PDL: wait for it)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        __syncthreads();
+    }
+    else k5_build_prefix(p, cum_s, warp_tot);
     const int64_t N = cum[p.B - 1];
     const int64_t row_bytes = p.V * (int64_t)sizeof(Tin);
     // The saved per-token inputs come from the actor pass (a previous kernel).
@@ -265,9 +272,14 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
 template <typename Tin>
 __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    int32_t *cum = reinterpret_cast<int32_t *>(smem_raw);
-    int32_t *warp_tot = cum + p.B;
-    k5_build_prefix(p, cum, warp_tot);
+    int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw);
+    int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);
+    const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
+    if (p.cum_global) {  // written by the prefix kernel just before us (PDL: wait for it)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        __syncthreads();
+    }
+    else k5_build_prefix(p, cum_s, warp_tot);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const float a = (float)(p.c2 / p.whiten[0]);
     const int64_t total = (int64_t)p.B * p.T;
@@ -321,7 +333,7 @@ static cudaError_t launch_k5_typed(const K5Params &p, bool tma, int num_sms, cud
         cfg.dynamicSmemBytes = smem;
         return cudaLaunchKernelEx(&cfg, k5_tma_kernel<Tin>, p);
     }
-    const size_t smem = sizeof(int32_t) * (size_t)(p.B + 32);
+    const size_t smem = sizeof(int32_t) * (size_t)((p.cum_global ? 0 : p.B) + 32);
     cudaError_t e = cudaFuncSetAttribute(k5_generic_kernel<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int64_t grid = (int64_t)num_sms * 4;

@@ -48,6 +48,8 @@ struct orl_ctx {
     double *d_gather_s = nullptr;      // [kMaxWorld][16]
     double *d_stats = nullptr;         // [16]
     double *h_stats = nullptr;         // pinned [16 + 4]
+    int32_t *d_cum = nullptr;          // length prefix of large micro-batches
+    int64_t cum_cap = 0;
     bool have_adv = false, have_whiten = false;
     int imported_w = 0, imported_s = 0;
     uint64_t launches = 0;
@@ -151,6 +153,24 @@ static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const o
     p.whiten = ctx->d_whiten;
 }
 
+// Large micro-batches (B > kSmemPrefixMax): build the length prefix in global memory.
+static orl_status prepare_prefix(orl_ctx *ctx, const orl_rows *rows, bool count_err, cudaStream_t s,
+                                 const int32_t **out) {
+    *out = nullptr;
+    if (rows->B <= kSmemPrefixMax) return ORL_OK;
+    if (rows->B > ctx->cum_cap) {
+        cudaFree(ctx->d_cum);
+        ctx->d_cum = nullptr;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->d_cum, (size_t)rows->B * sizeof(int32_t)));
+        ctx->cum_cap = rows->B;
+    }
+    CUDA_TRY(ctx, launch_lengths_prefix(rows->lengths + rows->seq_offset, (int)rows->B, (int)rows->T, ctx->d_cum,
+                                        count_err ? ctx->d_err : nullptr, s));
+    ctx->launches += 1;
+    *out = ctx->d_cum;
+    return ORL_OK;
+}
+
 // ------------------------------------------------------------------ context
 extern "C" int orl_version(void) { return ORL_VERSION; }
 
@@ -232,6 +252,7 @@ extern "C" orl_status orl_destroy(orl_ctx *ctx) {
     cudaFree(ctx->d_flags);
     cudaFree(ctx->d_gather_s);
     cudaFree(ctx->d_stats);
+    cudaFree(ctx->d_cum);
     if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
     delete ctx;
     return ORL_OK;
@@ -289,6 +310,7 @@ extern "C" orl_status orl_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl
     p.seq_reward = seq_reward;
     p.kl_out = kl;
     p.shaped = shaped_reward;
+    if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
     CUDA_TRY(ctx, launch_k1(p, tma_eligible(logits), kModeLogprob, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
     return ORL_OK;
@@ -427,6 +449,7 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
     p.ratio_guard = cfg->ratio_guard;
     p.kl_loss_est = cfg->kl_loss_est;
     p.kl_in_loss = cfg->kl_in_loss;
+    if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
     CUDA_TRY(ctx, launch_k1(p, tma_eligible(actor), kModeLoss, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
     return ORL_OK;
@@ -477,6 +500,7 @@ extern "C" orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const 
     const int64_t elt = p.elt;
     const bool tma = tma_eligible(actor) && (reinterpret_cast<uintptr_t>(dlogits) % 16 == 0) &&
                      ((out_stride_t * elt) % 16 == 0) && ((out_stride_b * elt) % 16 == 0);
+    if ((st = prepare_prefix(ctx, rows, false, as_stream(stream), &p.cum_global))) return st;
     CUDA_TRY(ctx, launch_k5(p, tma, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
     return ORL_OK;

@@ -43,6 +43,7 @@ struct K1Params {
     double eps_low, eps_high, eps_v, c1, beta_loss, ratio_guard;
     int kl_loss_est, kl_in_loss;
     const double *whiten;  // device [4]: N_global, mu, sigma, apply
+    const int32_t *cum_global;  // prefix of the micro-batch lengths (large B), else NULL
     // accounting
     double *ws;            // [kNumPartials][ws_stride] per-CTA partials
     int ws_stride;
@@ -54,6 +55,11 @@ struct K1Params {
 // Launch K1.  Returns the CUDA launch error.  `tma` selects the TMA bulk-copy
 // kernel (requires 16-byte aligned rows and row_bytes % 16 == 0).
 cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaStream_t s);
+// Micro-batches with more sequences than this keep the length prefix in global
+// memory (written by launch_lengths_prefix) instead of shared memory.
+constexpr int kSmemPrefixMax = 1024;
+cudaError_t launch_lengths_prefix(const int32_t *lengths, int B, int T, int32_t *cum,
+                                  unsigned long long *err, cudaStream_t s);
 // Shared-memory footprint of the TMA kernel for B sequences.
 size_t k1_tma_smem_bytes(int B);
 
@@ -71,6 +77,7 @@ struct K5Params {
     const int32_t *tokens, *lengths;
     const float *lse, *entropy, *dlogp;  // saved by the actor pass
     const double *whiten;                // device [4]: N_global first
+    const int32_t *cum_global;           // prefix of the micro-batch lengths (large B), else NULL
     int zero_masked;
 };
 cudaError_t launch_k5(const K5Params &p, bool tma, int num_sms, cudaStream_t s);

@@ -476,3 +476,25 @@ def test_next1_logits_grad_parity(ctx, dtype, V, inv_temp):
     H = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"], inv_temp)["entropy"]
     _check_grad(gg, o, m, 2e-5 if dtype == "f32" else 8e-3, f"{dtype}-{V}", _np(bufs.dlogp), H,
                 0.01 / float(m.sum()), inv_temp)
+
+
+def test_large_microbatch_global_prefix(ctx):
+    """B > 1024 sequences in one call: the length prefix lives in global memory."""
+    B, T, V = 1500, 3, 256
+    g = _gpu_batch(17, B, T, V, "mixed")
+    g["lengths"] = torch.randint(0, T + 1, (B,), dtype=torch.int32, device=DEV)
+    cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V, c2=0.01))
+    dl = torch.full((B, T, V), 5.0, dtype=torch.bfloat16, device=DEV)
+    bufs = Buffers(B, T, DEV)
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    status, st = run_iteration(ctx, g, cfg, bufs, src, mb=B, grad_sink=lambda s, e: dl[s:e])
+    torch.cuda.synchronize()
+    assert status == "ORL_OK"
+    npb = synth.batch_to_numpy(g)
+    m = parity.valid_mask(npb["lengths"], T)
+    o = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"])
+    parity.check_abs("logp_new", _np(bufs.logp_new), o["logp"], m)
+    parity.check_abs("entropy", _np(bufs.entropy), o["entropy"], m)
+    out_i, glob_i = _isolated_oracle(npb, bufs, dict(synth.CONFIGS["llama8b"], V=V, c2=0.01))
+    _check_downstream(bufs, out_i[0], glob_i, st, m, "largeB")
+    assert torch.all(dl.float()[~torch.from_numpy(m).to(DEV)] == 0)

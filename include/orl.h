@@ -169,9 +169,10 @@ int orl_version(void);
 orl_status orl_get_unique_id(unsigned char *id_out);
 
 /* Create a context on CUDA `device` for rank `rank` of `world` ranks.
- * world == 1: no communicator, `id` may be NULL.  world > 1: `id` (host,
- * ORL_UNIQUE_ID_BYTES) from orl_get_unique_id; collective (all ranks must
- * call).  The context owns the NCCL communicator, fp64 partial buffers,
+ * world == 1: `id` may be NULL (no communicator; the collectives reduce to
+ * local merges) or a unique id (a 1-rank NCCL communicator).  world > 1: `id`
+ * (host, ORL_UNIQUE_ID_BYTES) from orl_get_unique_id; collective (all ranks
+ * must call).  The context owns the NCCL communicator, fp64 partial buffers,
  * device error counters and a pinned host stats slot. */
 orl_status orl_create(int device, int world, int rank, const unsigned char *id, orl_ctx **out);
 

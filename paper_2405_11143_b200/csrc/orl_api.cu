@@ -226,7 +226,7 @@ extern "C" orl_status orl_create(int device, int world, int rank, const unsigned
          cudaMemset(ctx->d_flags, 0, 4 * sizeof(double)) == cudaSuccess &&
          cudaDeviceSynchronize() == cudaSuccess;
     if (!ok) return cleanup_fail(fail(nullptr, ORL_E_CUDA, "device init failed"));
-    if (world > 1) {
+    if (world > 1 || id) {  // world == 1 with an id: a 1-rank communicator (exercises the NCCL path)
         ncclUniqueId uid;
         std::memcpy(&uid, id, sizeof uid);
         ncclResult_t r = ncclCommInitRank(&ctx->comm, world, uid, rank);
@@ -388,7 +388,7 @@ extern "C" orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream) {
     } else {
         CUDA_TRY(ctx, launch_whiten_local(ctx->d_seq_part, (int)ctx->adv_B, ctx->d_gather_w + 4 * ctx->rank, s));
         ctx->launches += 1;
-        if (ctx->world > 1) {
+        if (ctx->comm) {
             NCCL_TRY(ctx, ncclAllGather(ctx->d_gather_w + 4 * ctx->rank, ctx->d_gather_w, 4, ncclDouble,
                                         ctx->comm, s));
         }
@@ -520,7 +520,7 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
     } else {
         CUDA_TRY(ctx, launch_stats_pack(ctx->d_acc, ctx->d_err, ctx->d_gather_s + kStatsSlots * ctx->rank, s));
         ctx->launches += 1;
-        if (ctx->world > 1)
+        if (ctx->comm)
             NCCL_TRY(ctx, ncclAllGather(ctx->d_gather_s + kStatsSlots * ctx->rank, ctx->d_gather_s,
                                         kStatsSlots, ncclDouble, ctx->comm, s));
     }

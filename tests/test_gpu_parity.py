@@ -498,3 +498,20 @@ def test_large_microbatch_global_prefix(ctx):
     out_i, glob_i = _isolated_oracle(npb, bufs, dict(synth.CONFIGS["llama8b"], V=V, c2=0.01))
     _check_downstream(bufs, out_i[0], glob_i, st, m, "largeB")
     assert torch.all(dl.float()[~torch.from_numpy(m).to(DEV)] == 0)
+
+
+def test_nccl_one_rank_communicator_matches_local():
+    """The NCCL all-gather path of C1/C2 (a 1-rank communicator) gives the same bits
+    as the local merge."""
+    B, T, V = 6, 64, 2048
+    c = dict(synth.CONFIGS["llama8b"], V=V)
+    cfg = PathConfig.from_synth(c)
+    g = _gpu_batch(41, B, T, V, "mixed")
+    a = orl.Context(0)
+    n = orl.Context(0, 1, 0, orl.orl_get_unique_id())
+    _, s1, b1 = _run(a, g, cfg, mb=4)
+    _, s2, b2 = _run(n, g, cfg, mb=4)
+    assert s1 == s2
+    assert torch.equal(b1.dlogp, b2.dlogp) and torch.equal(b1.adv, b2.adv)
+    a.close()
+    n.close()

@@ -117,6 +117,13 @@ typedef struct {
     int64_t seq_offset;     /* first sequence of the call in the rank batch   */
     const int32_t *tokens;  /* [B_total, T] sampled token ids y_{b,t}         */
     const int32_t *lengths; /* [B_total] response lengths L_b, 0 <= L_b <= T  */
+    /* Optional (NULL = padded logits).  Packed varlen logits (NEXT-2):
+     * [B_total + 1] token offsets with cu_seqlens[b+1] - cu_seqlens[b] >= L_b;
+     * logits row (b,t) of the call is element
+     * (cu_seqlens[seq_offset+b] - cu_seqlens[seq_offset] + t) * stride_t of the
+     * logits pointer (stride_b unused), and likewise for orl_logits_grad's
+     * output.  Per-token arrays stay [B_total, T]. */
+    const int32_t *cu_seqlens;
 } orl_rows;
 
 /* PPO loss configuration. */

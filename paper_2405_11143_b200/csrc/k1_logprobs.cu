@@ -596,7 +596,8 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                     locate_row(cum, p.B, jn, bn, tn);
                     yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
                 }
-                const char *src = p.base + ((int64_t)b * p.stride_b + (int64_t)t * p.stride_t) * p.elt;
+                const char *src =
+                    p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
                 for (int64_t off = 0; off < row_bytes; off += kChunk) {
                     const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
                     mbar_wait(&S.empty[stage], phase ^ 1u);
@@ -759,7 +760,8 @@ __global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
         locate_row(cum, p.B, j, b, t);
         const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
         const int y = __ldg(p.tokens + gi);
-        const Tin *row = reinterpret_cast<const Tin *>(p.base) + (int64_t)b * p.stride_b + (int64_t)t * p.stride_t;
+        const Tin *row = reinterpret_cast<const Tin *>(p.base) +
+                         logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t);
         Online st{kMInit, 0.f, 0.f};
         for (int64_t v0 = 0; v0 < p.V; v0 += 256 * 8) {
             float x[8];
@@ -841,8 +843,8 @@ template <typename Tin, int MODE>
 static cudaError_t launch_typed(const K1Params &p, bool tma, int num_sms, cudaStream_t s) {
     const int64_t N_upper = (int64_t)p.B * p.T;
     if (tma) {
-        if (p.poly == 4) return launch_tma<Tin, MODE, 4>(p, num_sms, s);
         if (p.poly == 8) return launch_tma<Tin, MODE, 8>(p, num_sms, s);
+        if (p.poly == 16) return launch_tma<Tin, MODE, 16>(p, num_sms, s);
         return launch_tma<Tin, MODE, 0>(p, num_sms, s);
     }
     const size_t smem = sizeof(int32_t) * (size_t)((p.cum_global ? 0 : p.B) + 32);

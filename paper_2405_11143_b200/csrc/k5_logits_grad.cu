@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                 locate_row(cum, p.B, j, b, t);
                 const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
                 const RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), a);
-                const char *src = p.base + ((int64_t)b * p.stride_b + (int64_t)t * p.stride_t) * sizeof(Tin);
+                const char *src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b,
+                                                             p.stride_t) * (int64_t)sizeof(Tin);
                 for (int64_t off = 0; off < row_bytes; off += kChunk) {
                     const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
                     mbar_wait(&S.empty[stage], phase ^ 1u);
@@ -169,7 +170,8 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
     for (int64_t j = blockIdx.x, rl = 0; j < N; j += gridDim.x, ++rl) {
         int b, t;
         locate_row(cum, p.B, j, b, t);
-        Tin *orow = reinterpret_cast<Tin *>(p.out) + (int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t;
+        Tin *orow = reinterpret_cast<Tin *>(p.out) +
+                    logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.out_stride_b, p.out_stride_t);
         RowInfo ri;
         uint64_t nl2 = 0, A1p = 0, A0p = 0;
         for (int64_t off = 0; off < row_bytes; off += kChunk) {
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
         }
     }
     // zero the masked rows of the output block (t >= L_b)
-    if (p.zero_masked) {
+    if (p.zero_masked && !p.cu_seqlens) {  // packed outputs have no masked rows
         const int64_t total = (int64_t)p.B * p.T;
         for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
             const int b = (int)(q / p.T), t = (int)(q % p.T);
@@ -286,13 +288,17 @@ __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
     for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
         const int b = (int)(q / p.T), t = (int)(q % p.T);
         const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-        Tin *orow = reinterpret_cast<Tin *>(p.out) + (int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t;
-        const Tin *row = reinterpret_cast<const Tin *>(p.base) + (int64_t)b * p.stride_b + (int64_t)t * p.stride_t;
         if (t >= L) {
+            if (p.cu_seqlens) continue;  // packed: no masked rows exist
+            Tin *orow = reinterpret_cast<Tin *>(p.out) + (int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t;
             if (p.zero_masked)
                 for (int64_t v = threadIdx.x; v < p.V; v += blockDim.x) orow[v] = Tin(0);
             continue;
         }
+        Tin *orow = reinterpret_cast<Tin *>(p.out) +
+                    logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.out_stride_b, p.out_stride_t);
+        const Tin *row = reinterpret_cast<const Tin *>(p.base) +
+                         logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t);
         const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
         const k5::RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), a);
         for (int64_t v = threadIdx.x; v < p.V; v += blockDim.x) {

@@ -112,8 +112,8 @@ static orl_status validate_rows_logits(orl_ctx *ctx, const orl_rows *rows, const
                     (long long)lg->stride_t, (long long)lg->V);
     if (!(inv_temp > 0.f) || !(inv_temp <= 1.0e4f))
         return fail(ctx, ORL_E_INVALID_ARG, "inv_temp=%g must be in (0, 1e4]", (double)inv_temp);
-    if (!aligned4(rows->tokens) || !aligned4(rows->lengths))
-        return fail(ctx, ORL_E_ALIGN, "tokens/lengths must be 4-byte aligned");
+    if (!aligned4(rows->tokens) || !aligned4(rows->lengths) || !aligned4(rows->cu_seqlens))
+        return fail(ctx, ORL_E_ALIGN, "tokens/lengths/cu_seqlens must be 4-byte aligned");
     return ORL_OK;
 }
 
@@ -145,6 +145,7 @@ static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const o
     p.seq_offset = rows->seq_offset;
     p.tokens = rows->tokens;
     p.lengths = rows->lengths;
+    p.cu_seqlens = rows->cu_seqlens;
     p.ws = ctx->d_ws;
     p.ws_stride = ctx->ws_stride;
     p.ticket = ctx->d_ticket;
@@ -492,6 +493,7 @@ extern "C" orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const 
     p.seq_offset = rows->seq_offset;
     p.tokens = rows->tokens;
     p.lengths = rows->lengths;
+    p.cu_seqlens = rows->cu_seqlens;
     p.lse = lse;
     p.entropy = entropy;
     p.dlogp = dloss_dlogp;

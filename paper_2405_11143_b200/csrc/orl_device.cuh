@@ -216,6 +216,14 @@ __device__ __forceinline__ double kl_grad(double d, int kind) {
     return 1.0 - exp(-d);
 }
 
+// Element offset of logits row (b, t) of a micro-batch: padded [B,T,V] views use
+// (stride_b, stride_t); packed varlen logits (cu_seqlens != NULL, token offsets
+// of the rank batch) put row (b,t) at (cu[so+b] - cu[so] + t) * stride_t.
+__device__ __forceinline__ int64_t logits_row_offset(const int32_t *cu, int64_t so, int b, int t, int64_t sb,
+                                                     int64_t st) {
+    return cu ? ((int64_t)(__ldg(cu + so + b) - __ldg(cu + so)) + t) * st : (int64_t)b * sb + (int64_t)t * st;
+}
+
 // Valid-row enumeration: the micro-batch's valid rows (t < L_b) in
 // (b,t) order, j = 0..N-1.  cum[b] = sum_{b'<=b} L_b' (inclusive).
 __device__ __forceinline__ void locate_row(const int32_t *cum, int B, int64_t j, int &b, int &t) {

@@ -30,6 +30,7 @@ struct K1Params {
     int B, T;
     int64_t seq_offset;
     const int32_t *tokens, *lengths;
+    const int32_t *cu_seqlens;  // packed varlen logits (NEXT-2), else NULL
     float *logp, *entropy, *lse, *gathered;
     // S2+S3 reward epilogue (reference pass)
     const float *partner;
@@ -75,6 +76,7 @@ struct K5Params {
     int B, T;
     int64_t seq_offset;
     const int32_t *tokens, *lengths;
+    const int32_t *cu_seqlens;           // packed varlen logits / dlogits, else NULL
     const float *lse, *entropy, *dlogp;  // saved by the actor pass
     const double *whiten;                // device [4]: N_global first
     const int32_t *cum_global;           // prefix of the micro-batch lengths (large B), else NULL

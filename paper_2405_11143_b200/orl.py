@@ -42,7 +42,7 @@ class Logits(ctypes.Structure):
 
 class Rows(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("seq_offset", ctypes.c_int64),
-                ("tokens", ctypes.c_void_p), ("lengths", ctypes.c_void_p)]
+                ("tokens", ctypes.c_void_p), ("lengths", ctypes.c_void_p), ("cu_seqlens", ctypes.c_void_p)]
 
 
 class PpoCfg(ctypes.Structure):
@@ -168,8 +168,15 @@ class Context:
 
 
 # ----------------------------------------------------------------------------- C-named calls
-def _rows(tokens, lengths, B, T, seq_offset):
-    return Rows(int(B), int(T), int(seq_offset), tokens.data_ptr(), lengths.data_ptr())
+def _rows(tokens, lengths, B, T, seq_offset, cu_seqlens=None):
+    return Rows(int(B), int(T), int(seq_offset), tokens.data_ptr(), lengths.data_ptr(),
+                None if cu_seqlens is None else cu_seqlens.data_ptr())
+
+
+def _packed(x, B):
+    """A packed [total, V] logits tensor seen as the [B, 1, V]-shaped descriptor the C
+    ABI wants (stride_b unused with cu_seqlens; stride_t = row pitch)."""
+    return Logits(x.data_ptr(), DTYPE[x.dtype], 0, x.shape[-1], 0, x.stride(-2))
 
 
 def _logits(x):
@@ -186,11 +193,16 @@ def orl_begin_iteration(ctx: Context, stream=None):
 
 def orl_logprobs(ctx: Context, tokens, lengths, logits, logp, *, seq_offset=0, inv_temp=1.0,
                  entropy=None, lse=None, gathered=None, partner_logp=None, kl_est="k1",
-                 beta_reward=0.0, seq_reward=None, kl=None, shaped_reward=None, stream=None):
+                 beta_reward=0.0, seq_reward=None, kl=None, shaped_reward=None, stream=None,
+                 cu_seqlens=None, n_seq=None):
     """S1 (+S2/S3 with partner_logp) on the micro-batch logits[0:B] = sequences
-    [seq_offset, seq_offset+B) of the rank batch; per-token arrays are [B_total, T]."""
-    B, T = logits.shape[0], tokens.shape[1]
-    rows, lg = _rows(tokens, lengths, B, T, seq_offset), _logits(logits)
+    [seq_offset, seq_offset+B) of the rank batch; per-token arrays are [B_total, T].
+    Packed varlen (NEXT-2): pass `cu_seqlens` and a [total, V] `logits` whose row 0 is
+    token cu_seqlens[seq_offset], plus `n_seq` (the B of the call)."""
+    T = tokens.shape[1]
+    B = n_seq if cu_seqlens is not None else logits.shape[0]
+    rows = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens)
+    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
     st = _lib.orl_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), _ptr(logp),
                            _ptr(entropy), _ptr(lse), _ptr(gathered), _ptr(partner_logp),
                            KL.get(kl_est, kl_est), float(beta_reward), _ptr(seq_reward), _ptr(kl),
@@ -214,9 +226,12 @@ def orl_whiten_stats(ctx: Context, whiten: bool, stream=None):
 
 def orl_ppo_loss(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
                  seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
-                 entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, stream=None):
-    B, T = logits.shape[0], tokens.shape[1]
-    rows, lg, c = _rows(tokens, lengths, B, T, seq_offset), _logits(logits), cfg.c()
+                 entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, stream=None,
+                 cu_seqlens=None, n_seq=None):
+    T = tokens.shape[1]
+    B = n_seq if cu_seqlens is not None else logits.shape[0]
+    rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
+    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
     st = _lib.orl_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
                            _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
                            _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
@@ -225,15 +240,19 @@ def orl_ppo_loss(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old
 
 
 def orl_logits_grad(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, lse, entropy, dloss_dlogp, dlogits, *,
-                    seq_offset=0, inv_temp=1.0, zero_masked=True, stream=None):
-    """NEXT-1: dL/dlogits of the micro-batch logits[0:B] into dlogits[0:B] (same dtype/shape view)."""
-    B, T = logits.shape[0], tokens.shape[1]
-    if dlogits.dtype != logits.dtype or dlogits.shape[2] != logits.shape[2] or dlogits.stride(2) != 1:
-        raise ValueError("dlogits must be a [B,T,V] view with the logits dtype and unit V stride")
-    rows, lg, c = _rows(tokens, lengths, B, T, seq_offset), _logits(logits), cfg.c()
+                    seq_offset=0, inv_temp=1.0, zero_masked=True, stream=None, cu_seqlens=None, n_seq=None):
+    """NEXT-1: dL/dlogits of the micro-batch logits[0:B] into dlogits[0:B] (same dtype/shape view;
+    packed [total, V] tensors with cu_seqlens)."""
+    T = tokens.shape[1]
+    B = n_seq if cu_seqlens is not None else logits.shape[0]
+    if dlogits.dtype != logits.dtype or dlogits.shape[-1] != logits.shape[-1] or dlogits.stride(-1) != 1:
+        raise ValueError("dlogits must be a view with the logits dtype, V and unit V stride")
+    rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
+    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
+    sb = 0 if cu_seqlens is not None else dlogits.stride(0)
     st = _lib.orl_logits_grad(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
-                              _ptr(lse), _ptr(entropy), _ptr(dloss_dlogp), _ptr(dlogits), dlogits.stride(0),
-                              dlogits.stride(1), int(bool(zero_masked)), _stream(stream))
+                              _ptr(lse), _ptr(entropy), _ptr(dloss_dlogp), _ptr(dlogits), sb,
+                              dlogits.stride(-2), int(bool(zero_masked)), _stream(stream))
     return ctx.check(st)
 
 

@@ -515,3 +515,51 @@ def test_nccl_one_rank_communicator_matches_local():
     assert torch.equal(b1.dlogp, b2.dlogp) and torch.equal(b1.adv, b2.adv)
     a.close()
     n.close()
+
+
+def test_next2_packed_varlen_matches_padded(ctx):
+    """Packed varlen logits ([total, V] + cu_seqlens, NEXT-2) give bit-identical per-token
+    outputs and dlogits to the padded [B, T, V] layout (rows are computed independently)."""
+    B, T, V = 5, 40, 4096
+    g = _gpu_batch(23, B, T, V, "mixed")
+    L = g["lengths"].long()
+    cu = torch.zeros(B + 1, dtype=torch.int32, device=DEV)
+    cu[1:] = torch.cumsum(L, 0).int()
+    packed = {r: torch.cat([g[f"logits_{r}"][b, : int(L[b])] for b in range(B)]) for r in ("old", "ref", "new")}
+    cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V, c2=0.01))
+    # padded reference run
+    dl_pad = torch.zeros(B, T, V, dtype=torch.bfloat16, device=DEV)
+    bp = Buffers(B, T, DEV)
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    status, st_pad = run_iteration(ctx, g, cfg, bp, src, mb=2, grad_sink=lambda s, e: dl_pad[s:e])
+    assert status == "ORL_OK"
+    # packed run through the same calls, micro-batches of 2 sequences
+    bk = Buffers(B, T, DEV)
+    tok = g["tokens"]
+    dl_pk = torch.zeros_like(packed["new"])
+    mbs = [(s, min(B, s + 2)) for s in range(0, B, 2)]
+    view = lambda r, s: packed[r][int(cu[s]):]  # noqa: E731
+    orl.orl_begin_iteration(ctx)
+    for s, e in mbs:
+        orl.orl_logprobs(ctx, tok, g["lengths"], view("old", s), bk.logp_old, seq_offset=s, cu_seqlens=cu, n_seq=e - s)
+    for s, e in mbs:
+        orl.orl_logprobs(ctx, tok, g["lengths"], view("ref", s), bk.logp_ref, seq_offset=s, cu_seqlens=cu,
+                         n_seq=e - s, partner_logp=bk.logp_old, kl_est=cfg.kl_est_reward, beta_reward=cfg.beta_reward,
+                         seq_reward=g["seq_reward"], kl=bk.kl, shaped_reward=bk.shaped)
+    orl.orl_advantages(ctx, g["lengths"], bk.adv, kind="gae", gamma=cfg.gamma, lam=cfg.lam, shaped_reward=bk.shaped,
+                       values=g["values_old"], seq_reward=g["seq_reward"], ret=bk.ret)
+    orl.orl_whiten_stats(ctx, True)
+    for s, e in mbs:
+        orl.orl_ppo_loss(ctx, tok, g["lengths"], view("new", s), cfg.ppo, bk.logp_old, bk.adv, bk.logp_new,
+                         seq_offset=s, cu_seqlens=cu, n_seq=e - s, logp_ref=bk.logp_ref, ret=bk.ret,
+                         v_new=g["values_new"], v_old=g["values_old"], entropy=bk.entropy, lse=bk.lse,
+                         dloss_dlogp=bk.dlogp, dloss_dv=bk.dv)
+    for s, e in mbs:
+        orl.orl_logits_grad(ctx, tok, g["lengths"], view("new", s), cfg.ppo, bk.lse, bk.entropy, bk.dlogp,
+                            dl_pk[int(cu[s]):], seq_offset=s, cu_seqlens=cu, n_seq=e - s)
+    status, st_pk = orl.orl_finalize(ctx, cfg.ppo)
+    assert status == "ORL_OK" and st_pk == st_pad
+    for k in ("logp_old", "logp_ref", "logp_new", "entropy", "adv", "ret", "dlogp", "dv", "lse"):
+        assert torch.equal(getattr(bk, k), getattr(bp, k)), k
+    for b in range(B):
+        assert torch.equal(dl_pk[int(cu[b]):int(cu[b + 1])], dl_pad[b, : int(L[b])])

@@ -73,14 +73,14 @@ def _load():
         lib.oracle_whiten_value.argtypes = [f64, f64, f64]
         lib.oracle_whiten_value.restype = f64
         lib.oracle_ppo_loss.argtypes = [i64, i64, P, P, P, P, P, P, P, P, P,
-                                        f64, f64, f64, f64, f64, i32, i32, f64, f64,
+                                        f64, f64, f64, f64, f64, i32, i32, f64, f64, i32, f64,
                                         P, P, P, P, P, P]
         lib.oracle_ppo_loss.restype = None
         lib.oracle_logits_grad_row.argtypes = [P, i64, i64, f64, f64, f64, P]
         lib.oracle_logits_grad_row.restype = None
         lib.oracle_kl_controller_step.argtypes = [P, f64, f64, f64, f64]
         lib.oracle_kl_controller_step.restype = i32
-        lib.oracle_stats.argtypes = [P, f64, f64, f64, i32, P]
+        lib.oracle_stats.argtypes = [P, f64, f64, f64, i32, i32, f64, P]
         lib.oracle_stats.restype = i32
         _lib = lib
         return lib
@@ -237,14 +237,17 @@ def whiten(adv, lengths, mean, std):
 # --------------------------------------------------------------------------- S7-S10
 def ppo_loss(lengths, logp_new, logp_old, adv_w, *, logp_ref=None, ret=None, v_new=None,
              v_old=None, entropy=None, eps_low=0.2, eps_high=0.2, eps_v=0.0, c1=0.0,
-             beta_loss=0.0, kl_est="k1", kl_in_loss=False, ratio_guard=30.0, n_global=None):
+             beta_loss=0.0, kl_est="k1", kl_in_loss=False, ratio_guard=30.0, n_global=None,
+             seq_mean=False, n_seq=None):
     lib = _load()
     logp_new, logp_old, adv_w = _f64(logp_new), _f64(logp_old), _f64(adv_w)
     B, T = logp_new.shape
     lengths = _i32(lengths)
     if n_global is None:
         n_global = float(np.minimum(lengths, T).clip(min=0).sum())
-    sums = np.zeros(11)
+    if n_seq is None:
+        n_seq = float(np.count_nonzero(lengths > 0))
+    sums = np.zeros(15)
     obj, vl, dlogp, dv = (np.zeros((B, T)) for _ in range(4))
     clipped = np.zeros((B, T), dtype=np.uint8)
     logp_ref, ret, v_new, v_old, entropy = map(_f64, (logp_ref, ret, v_new, v_old, entropy))
@@ -252,7 +255,8 @@ def ppo_loss(lengths, logp_new, logp_old, adv_w, *, logp_ref=None, ret=None, v_n
                         _p(ret), _p(v_new), _p(v_old), _p(entropy), float(eps_low),
                         float(eps_high), float(eps_v), float(c1), float(beta_loss),
                         KL.get(kl_est, kl_est), int(bool(kl_in_loss)), float(ratio_guard),
-                        float(n_global), _p(sums), _p(obj), _p(clipped), _p(vl), _p(dlogp), _p(dv))
+                        float(n_global), int(bool(seq_mean)), float(n_seq),
+                        _p(sums), _p(obj), _p(clipped), _p(vl), _p(dlogp), _p(dv))
     return dict(sums=sums, obj=obj, clipped=clipped, vl=vl, dlogp=dlogp, dv=dv)
 
 
@@ -260,12 +264,12 @@ STAT_NAMES = ("n_tokens", "policy_loss", "value_loss", "entropy", "kl", "approx_
               "clip_frac", "value_clip_frac", "ratio_mean", "total_loss")
 
 
-def stats(sums, c1=0.0, c2=0.0, beta_loss=0.0, kl_in_loss=False):
+def stats(sums, c1=0.0, c2=0.0, beta_loss=0.0, kl_in_loss=False, seq_mean=False, n_seq=0.0):
     lib = _load()
-    sums = _f64(sums)
+    sums = _f64(np.concatenate([np.ravel(sums), np.zeros(max(0, 15 - np.size(sums)))]))
     out = np.zeros(10)
     rc = lib.oracle_stats(_p(sums), float(c1), float(c2), float(beta_loss),
-                          int(bool(kl_in_loss)), _p(out))
+                          int(bool(kl_in_loss)), int(bool(seq_mean)), float(n_seq), _p(out))
     d = dict(zip(STAT_NAMES, map(float, out)))
     d["empty"] = bool(rc)
     d["n_guard"] = int(sums[9])
@@ -283,12 +287,13 @@ def logits_grad_row(x, y, inv_temp, w, a):
     return g
 
 
-def logits_grad(logits, tokens, lengths, dlogp, inv_temp, c2, n_global):
-    """[B,T,V] dL/dlogits (zeros on masked rows); `logits` as for logprobs()."""
+def logits_grad(logits, tokens, lengths, dlogp, inv_temp, c2, n_global, seq_mean=False, n_seq=0.0):
+    """[B,T,V] dL/dlogits (zeros on masked rows); `logits` as for logprobs().
+    The entropy weight per row is c2/N (token mean) or c2/(n_seq L_b) (NEXT-2 seq-mean)."""
     B, T, V = logits.shape
     out = np.zeros((B, T, V))
-    a = c2 / n_global
     for b in range(B):
+        a = c2 / (n_seq * float(lengths[b])) if seq_mean else c2 / n_global
         for t in range(int(lengths[b])):
             row = logits[b, t]
             x = (row.astype(np.uint32) << 16).view(np.float32).astype(np.float64) \

@@ -344,6 +344,10 @@ double oracle_whiten_value(double a, double mean, double std)
  *     N = n_global (all ranks' valid tokens, Z11).  A' = adv_w, already
  *     whitened by the caller when whitening is on.  Optional arrays may be
  *     NULL (no critic: v_new == NULL; no reference: logp_ref == NULL).
+ *     NEXT-2 sequence-mean aggregation (Z31): sums[11..14] hold the
+ *     per-sequence-mean sums  sum_t obj/L_b, vl/L_b, H/L_b, k(new,ref)/L_b
+ *     (always); with seq_mean = 1 the derivatives are divided by
+ *     n_seq * L_b instead of N (n_seq = all ranks' sequences with L_b > 0).
  * ---------------------------------------------------------------------- */
 void oracle_ppo_loss(int64_t B, int64_t T, const int32_t *lengths,
                      const double *logp_new, const double *logp_old,
@@ -352,10 +356,11 @@ void oracle_ppo_loss(int64_t B, int64_t T, const int32_t *lengths,
                      const double *entropy, double eps_low, double eps_high,
                      double eps_v, double c1, double beta_loss, int kl_est,
                      int kl_in_loss, double ratio_guard, double n_global,
+                     int seq_mean, double n_seq,
                      double *sums, double *obj_out, uint8_t *clipped_out,
                      double *vl_out, double *dlogp_out, double *dv_out)
 {
-    for (int k = 0; k < 11; ++k) sums[k] = 0.0;
+    for (int k = 0; k < 15; ++k) sums[k] = 0.0;
     for (int64_t b = 0; b < B; ++b)
         for (int64_t t = 0; t < T; ++t) {
             int64_t i = b * T + t;
@@ -415,14 +420,20 @@ void oracle_ppo_loss(int64_t B, int64_t T, const int32_t *lengths,
             if (fabs(dold) > ratio_guard) sums[9] += 1.0;
             if (!(isfinite(obj) && isfinite(vl) && isfinite(H) && isfinite(kref)))
                 sums[10] += 1.0;
+            double Lb = (double)lengths[b];
+            sums[11] += obj / Lb;
+            sums[12] += vl / Lb;
+            sums[13] += H / Lb;
+            sums[14] += kref / Lb;
 
+            double denom = seq_mean ? n_seq * Lb : n_global;
             if (obj_out) obj_out[i] = obj;
             if (clipped_out) clipped_out[i] = (uint8_t)clipped;
             if (vl_out) vl_out[i] = vl;
             if (dlogp_out)
                 dlogp_out[i] = ((clipped ? 0.0 : -rho * A) +
-                                (kl_in_loss ? beta_loss * dkref : 0.0)) / n_global;
-            if (dv_out) dv_out[i] = c1 * dvl / n_global;
+                                (kl_in_loss ? beta_loss * dkref : 0.0)) / denom;
+            if (dv_out) dv_out[i] = c1 * dvl / denom;
         }
 }
 
@@ -432,19 +443,23 @@ void oracle_ppo_loss(int64_t B, int64_t T, const int32_t *lengths,
  *        4 kl (loss estimator, new vs ref) 5 approx_kl_old (k3, old vs new)
  *        6 clip_frac 7 value_clip_frac 8 ratio_mean
  *        9 total = policy + c1 value - c2 entropy + [kl_in_loss] beta kl
+ *   seq_mean = 1 (NEXT-2, Z31): policy_loss, value_loss, entropy and kl are
+ *   means over the n_seq sequences of the per-sequence token means,
+ *   e.g. policy_loss = -(1/n_seq) sum_b (1/L_b) sum_t obj; the shares and
+ *   ratio_mean stay token means.
  *   N = 0 returns 1 (ORL_E_EMPTY_BATCH) and leaves out[] at 0.
  * ---------------------------------------------------------------------- */
 int oracle_stats(const double *sums, double c1, double c2, double beta_loss,
-                 int kl_in_loss, double *out)
+                 int kl_in_loss, int seq_mean, double n_seq, double *out)
 {
     for (int k = 0; k < 10; ++k) out[k] = 0.0;
     double N = sums[0];
     if (!(N > 0.0)) return 1;
     out[0] = N;
-    out[1] = -sums[1] / N;
-    out[2] = sums[2] / N;
-    out[3] = sums[3] / N;
-    out[4] = sums[4] / N;
+    out[1] = seq_mean ? -sums[11] / n_seq : -sums[1] / N;
+    out[2] = seq_mean ? sums[12] / n_seq : sums[2] / N;
+    out[3] = seq_mean ? sums[13] / n_seq : sums[3] / N;
+    out[4] = seq_mean ? sums[14] / n_seq : sums[4] / N;
     out[5] = sums[7] / N;
     out[6] = sums[5] / N;
     out[7] = sums[6] / N;

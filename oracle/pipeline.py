@@ -20,7 +20,7 @@ from . import (broadcast_seq, discounted_returns, gae, group_advantages, group_m
 DEFAULTS = dict(inv_temp=1.0, kl_mode="reward", kl_est_reward="k1", beta_reward=0.01,
                 adv_kind="gae", gamma=1.0, lam=0.95, group_size=1, whiten=True,
                 eps_low=0.2, eps_high=0.2, eps_v=0.2, c1=0.5, c2=0.0, beta_loss=0.0,
-                kl_est_loss="k2", ratio_guard=30.0)
+                kl_est_loss="k2", ratio_guard=30.0, loss_agg="token_mean")
 
 
 def _s1(shard, role, inv_temp):
@@ -68,9 +68,11 @@ def pipeline(shards, cfg=None):
     valid = np.concatenate([o["adv"][b, : int(L_b)] for o, sh in zip(out, shards)
                             for b, L_b in enumerate(sh["lengths"])] or [np.zeros(0)])
     n_global = float(valid.size)
+    n_seq = float(sum(int(np.count_nonzero(np.asarray(sh["lengths"]) > 0)) for sh in shards))
+    seq_mean = cfg["loss_agg"] == "seq_mean_token_mean"
     do_whiten = bool(cfg["whiten"]) and kind != "grpo"
     mean, std, warn = whiten_moments(valid)
-    glob = dict(n_global=n_global, adv_mean=mean, adv_std=std, whiten_warn=warn and do_whiten)
+    glob = dict(n_global=n_global, n_seq=n_seq, adv_mean=mean, adv_std=std, whiten_warn=warn and do_whiten)
     for o, sh in zip(out, shards):
         if do_whiten and not warn:
             o["adv_w"] = whiten(o["adv"], sh["lengths"], mean, std)
@@ -78,7 +80,7 @@ def pipeline(shards, cfg=None):
             o["adv_w"] = o["adv"]
 
     # ---- S7-S9 loss per shard, S10 sums in shard order ---------------------------
-    sums = np.zeros(11)
+    sums = np.zeros(15)
     for o, sh in zip(out, shards):
         s_new = _s1(sh, "new", cfg["inv_temp"])
         o["logp_new"], o["entropy"] = s_new["logp"], s_new["entropy"]
@@ -91,11 +93,12 @@ def pipeline(shards, cfg=None):
                        eps_v=cfg["eps_v"], c1=cfg["c1"] if critic else 0.0,
                        beta_loss=cfg["beta_loss"], kl_est=cfg["kl_est_loss"],
                        kl_in_loss=cfg["kl_mode"] == "loss" and o["logp_ref"] is not None,
-                       ratio_guard=cfg["ratio_guard"], n_global=n_global)
+                       ratio_guard=cfg["ratio_guard"], n_global=n_global, seq_mean=seq_mean, n_seq=n_seq)
         o.update(obj=res["obj"], clipped=res["clipped"], vl=res["vl"], dlogp=res["dlogp"],
                  dv=res["dv"], sums=res["sums"])
         sums = sums + res["sums"]
     kl_in_loss = cfg["kl_mode"] == "loss" and out and out[0]["logp_ref"] is not None
-    st = stats(sums, c1=cfg["c1"], c2=cfg["c2"], beta_loss=cfg["beta_loss"], kl_in_loss=kl_in_loss)
+    st = stats(sums, c1=cfg["c1"], c2=cfg["c2"], beta_loss=cfg["beta_loss"], kl_in_loss=kl_in_loss,
+               seq_mean=seq_mean, n_seq=n_seq)
     glob.update(sums=sums, stats=st)
     return out, glob

@@ -71,7 +71,7 @@ def _worker(rank, world, port, kind, q):
         # C2: gather the loss partials and sum them in rank order
         sums = [None] * world
         dist.all_gather_object(sums, res["sums"])
-        tot = np.zeros(11)
+        tot = np.zeros(15)
         for r in range(world):
             tot = tot + sums[r]
         st = oracle.stats(tot, c1=cfg["c1"], c2=cfg["c2"], beta_loss=cfg.get("beta_loss", 0.0),

@@ -521,3 +521,83 @@ def test_next3_kl_controller_spec_examples(golden):
     # the proportional error is clipped to +-0.5: far-off observations move beta by 1 +- 0.5/horizon
     assert oracle.kl_controller_step(1.0, 0.01, 2.0, 1e6, 1e9)[0] == 1.25
     assert oracle.kl_controller_step(1.0, 0.01, 2.0, 0.0, 1e9)[0] == 0.75
+
+
+# ----------------------------------------------------------------------------- NEXT-2 seq-mean
+def test_next2_seq_mean_aggregation_definition_and_gradients():
+    """Sequence-mean loss aggregation (Z31): against its numpy definition, equal to the
+    token mean when every response has the same length, and its per-token
+    derivatives by central differences."""
+    B, T = 4, 6
+    L = np.array([6, 2, 0, 3], np.int32)
+    lo = rng.normal(-1, 0.2, (B, T))
+    ln = lo + rng.normal(0, 0.3, (B, T))
+    A, R = rng.normal(0, 1, (B, T)), rng.normal(0, 1, (B, T))
+    vo = rng.normal(0, 1, (B, T))
+    vn = vo + rng.normal(0, 0.3, (B, T))
+    lr, H = lo + 0.05, np.abs(rng.normal(1, 0.5, (B, T)))
+    kw = dict(logp_ref=lr, ret=R, v_new=vn, v_old=vo, entropy=H, eps_v=0.2, c1=0.5, beta_loss=0.1,
+              kl_est="k2", kl_in_loss=True, eps_low=0.2, eps_high=0.28)
+    res = oracle.ppo_loss(L, ln, lo, A, seq_mean=True, **kw)
+    st = oracle.stats(res["sums"], c1=0.5, c2=0.01, beta_loss=0.1, kl_in_loss=True, seq_mean=True, n_seq=3.0)
+    seqs = [b for b in range(B) if L[b] > 0]
+    per = lambda a: np.mean([a[b, :L[b]].mean() for b in seqs])  # noqa: E731
+    assert abs(st["policy_loss"] + per(res["obj"])) < 1e-14
+    assert abs(st["value_loss"] - per(res["vl"])) < 1e-14
+    assert abs(st["entropy"] - per(H)) < 1e-14
+    d = ln - lr
+    assert abs(st["kl"] - per(0.5 * d * d)) < 1e-14
+    # token-mean shares are unchanged by the aggregation mode
+    st_tok = oracle.stats(res["sums"], c1=0.5, c2=0.01, beta_loss=0.1, kl_in_loss=True)
+    for k in ("clip_frac", "value_clip_frac", "ratio_mean", "approx_kl_old", "n_tokens"):
+        assert st[k] == st_tok[k]
+    # equal lengths: seq-mean == token-mean
+    Le = np.array([4, 4, 4, 4], np.int32)
+    r1 = oracle.ppo_loss(Le, ln, lo, A, seq_mean=True, **kw)
+    s1 = oracle.stats(r1["sums"], c1=0.5, c2=0.01, beta_loss=0.1, kl_in_loss=True, seq_mean=True, n_seq=4.0)
+    s0 = oracle.stats(r1["sums"], c1=0.5, c2=0.01, beta_loss=0.1, kl_in_loss=True)
+    for k in ("policy_loss", "value_loss", "entropy", "kl", "total_loss"):
+        assert abs(s1[k] - s0[k]) < 1e-14
+    r2 = oracle.ppo_loss(Le, ln, lo, A, **kw)
+    np.testing.assert_allclose(r1["dlogp"], r2["dlogp"], rtol=1e-14, atol=1e-17)
+    # derivatives of the seq-mean total by central differences
+    def tot(lpn, vnn):
+        r = oracle.ppo_loss(L, lpn, lo, A, seq_mean=True, **dict(kw, v_new=vnn))
+        return oracle.stats(r["sums"], c1=0.5, c2=0.01, beta_loss=0.1, kl_in_loss=True, seq_mean=True,
+                            n_seq=3.0)["total_loss"]
+    h = 1e-6
+    for b in seqs:
+        for t in range(L[b]):
+            p, m = ln.copy(), ln.copy()
+            p[b, t] += h
+            m[b, t] -= h
+            assert abs((tot(p, vn) - tot(m, vn)) / (2 * h) - res["dlogp"][b, t]) < 1e-7
+            p, m = vn.copy(), vn.copy()
+            p[b, t] += h
+            m[b, t] -= h
+            assert abs((tot(ln, p) - tot(ln, m)) / (2 * h) - res["dv"][b, t]) < 1e-7
+
+
+def test_next2_seq_mean_logits_grad_finite_differences():
+    B, T, V = 2, 3, 5
+    L = np.array([3, 1], np.int32)
+    x = rng.normal(0, 1.5, (B, T, V))
+    tok = rng.integers(0, V, (B, T)).astype(np.int32)
+    lo = rng.normal(-1.5, 0.3, (B, T))
+    A = rng.normal(0, 1, (B, T))
+
+    def total(xn):
+        o = oracle.logprobs(xn, tok, L)
+        r = oracle.ppo_loss(L, o["logp"], lo, A, entropy=o["entropy"], seq_mean=True)
+        return oracle.stats(r["sums"], c2=0.05, seq_mean=True, n_seq=2.0)["total_loss"], r
+
+    _, r = total(x)
+    g = oracle.logits_grad(x, tok, L, r["dlogp"], 1.0, 0.05, float(L.sum()), seq_mean=True, n_seq=2.0)
+    h = 1e-6
+    for b in range(B):
+        for t in range(L[b]):
+            for v in range(V):
+                xp, xm = x.copy(), x.copy()
+                xp[b, t, v] += h
+                xm[b, t, v] -= h
+                assert abs((total(xp)[0] - total(xm)[0]) / (2 * h) - g[b, t, v]) < 2e-8

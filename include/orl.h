@@ -53,6 +53,7 @@ extern "C" {
 #define ORL_VERSION 1
 #define ORL_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
 #define ORL_STATS_N 16          /* length of the device stats vector */
+#define ORL_PARTIALS_N 24       /* length of a rank's loss/stat partial (hooks) */
 #define ORL_MAX_SEQ_PER_CALL 8192
 
 typedef enum {
@@ -137,6 +138,10 @@ typedef struct {
     int32_t kl_loss_est;/* orl_kl used for the loss term and the kl stat    */
     int32_t kl_in_loss; /* 1: total += beta_loss * mean k(new, ref)  (Z5)   */
     double ratio_guard; /* |logp_new - logp_old| > guard counts (Z22); 30   */
+    int32_t loss_agg;   /* 0 = token mean over all ranks' tokens (Z11);     */
+                        /* 1 = mean over sequences of per-sequence token    */
+                        /*     means (NEXT-2, Z31; S:243 names the default) */
+    int32_t pad_;
 } orl_ppo_cfg;
 
 /* Host-side statistics.  Means are over the N valid tokens of
@@ -320,15 +325,15 @@ orl_status orl_kl_controller_step(double *beta, double target, double horizon, d
 
 /* ---- collective boundary hooks (testing / custom transports) ----------- */
 
-/* which = 0: this rank's whitening partial (double[4]: count, mean, M2, 0),
- *            valid after orl_advantages;
- * which = 1: this rank's loss/stat partial (double[ORL_STATS_N]), valid
+/* which = 0: this rank's whitening partial (double[4]: count, mean, M2,
+ *            sequences with L_b > 0), valid after orl_advantages;
+ * which = 1: this rank's loss/stat partial (double[ORL_PARTIALS_N]), valid
  *            after the last orl_ppo_loss.
  * Copies it to host memory `host_out` (synchronises `stream`). */
 orl_status orl_export_partials(orl_ctx *ctx, int which, double *host_out, void *stream);
 
 /* Supplies the gathered partials of `world` ranks (host, [world][4] or
- * [world][ORL_STATS_N], rank order) in place of the NCCL all-gather for the
+ * [world][ORL_PARTIALS_N], rank order) in place of the NCCL all-gather for the
  * next orl_whiten_stats (which = 0) or orl_finalize (which = 1) on this
  * context.  Lets one process emulate n ranks on one GPU with the exact
  * device merge the NCCL path runs. */

@@ -293,6 +293,8 @@ def logits_grad(logits, tokens, lengths, dlogp, inv_temp, c2, n_global, seq_mean
     B, T, V = logits.shape
     out = np.zeros((B, T, V))
     for b in range(B):
+        if int(lengths[b]) <= 0:
+            continue
         a = c2 / (n_seq * float(lengths[b])) if seq_mean else c2 / n_global
         for t in range(int(lengths[b])):
             row = logits[b, t]

@@ -255,8 +255,10 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         }
         return;
     } else {
-        // S7-S9 (Z11-Z17, Z22), all in fp64
-        const double N = wh[0];
+        // S7-S9 (Z11-Z17, Z22), all in fp64.  Derivatives are
+        // per token of the token mean (1/N) or, NEXT-2 sequence mean (Z31),
+        // of the mean of per-sequence means (1/(N_seq L_b)).
+        const double N = p.loss_agg == 1 ? wh[4] * (double)L : wh[0];
         double A = (double)side[2];
         if (wh[3] != 0.0) A = (A - wh[1]) / (wh[2] + 1e-8);
         const double lpn = (double)logp_f, lpo = (double)side[0];
@@ -302,6 +304,11 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         wacc[8] += rho;
         if (fabs(dold) > p.ratio_guard) wacc[9] += 1.0;
         if (!(isfinite(obj) && isfinite(vl) && isfinite(Hd) && isfinite(kref))) wacc[10] += 1.0;
+        const double invL = 1.0 / (double)L;
+        wacc[11] += obj * invL;
+        wacc[12] += vl * invL;
+        wacc[13] += Hd * invL;
+        wacc[14] += kref * invL;
         if (p.dlogp)
             p.dlogp[i] = (float)(((clipped ? 0.0 : -rho * A) +
                                   (p.kl_in_loss ? p.beta_loss * dkref : 0.0)) / N);
@@ -617,9 +624,10 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         const int ew = warp - kEpilogueWarp;  // rows rl with rl % kEpiWarps == ew
         asm volatile("griddepcontrol.wait;" ::: "memory");
         zero_masked(p, cum, lane + 32 * ew, 32 * kEpiWarps, MODE);
-        double wh[4] = {0.0, 0.0, 0.0, 0.0};
+        double wh[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         if (MODE == kModeLoss) {
             wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
+            wh[4] = p.whiten[4];
         }
         const int nside = MODE == kModeLoss ? 6 : 2;
         for (int64_t j = blockIdx.x + (int64_t)ew * gridDim.x, rl = ew; j < N;
@@ -751,9 +759,10 @@ __global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
     else build_prefix(p, cum_s, warp_tot);
     const int64_t N = cum[p.B - 1];
     zero_masked(p, cum, tid, 256, MODE);
-    double wh[4] = {0.0, 0.0, 0.0, 0.0};
+    double wh[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (MODE == kModeLoss) {
         wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
+        wh[4] = p.whiten[4];
     }
     for (int64_t j = blockIdx.x; j < N; j += gridDim.x) {
         int b, t;

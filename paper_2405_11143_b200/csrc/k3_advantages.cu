@@ -178,18 +178,24 @@ __device__ __forceinline__ void chan_merge(double &n, double &mean, double &M2, 
 }
 
 __global__ void whiten_local_kernel(const double *seq_part, int B, double *slot) {
-    __shared__ double sn[256], sm[256], s2[256];
+    __shared__ double sn[256], sm[256], s2[256], sc[256];
     const int tid = threadIdx.x;
     const int per = (B + 255) / 256;
     const int beg = min(B, tid * per), end = min(B, beg + per);
-    double n = 0.0, mean = 0.0, M2 = 0.0;
-    for (int q = beg; q < end; ++q) chan_merge(n, mean, M2, seq_part[3 * q], seq_part[3 * q + 1], seq_part[3 * q + 2]);
-    sn[tid] = n; sm[tid] = mean; s2[tid] = M2;
+    double n = 0.0, mean = 0.0, M2 = 0.0, nseq = 0.0;
+    for (int q = beg; q < end; ++q) {
+        chan_merge(n, mean, M2, seq_part[3 * q], seq_part[3 * q + 1], seq_part[3 * q + 2]);
+        nseq += seq_part[3 * q] > 0.0 ? 1.0 : 0.0;
+    }
+    sn[tid] = n; sm[tid] = mean; s2[tid] = M2; sc[tid] = nseq;
     __syncthreads();
     if (tid == 0) {
-        double N = 0.0, mu = 0.0, m2 = 0.0;
-        for (int q = 0; q < 256; ++q) chan_merge(N, mu, m2, sn[q], sm[q], s2[q]);
-        slot[0] = N; slot[1] = mu; slot[2] = m2; slot[3] = 0.0;
+        double N = 0.0, mu = 0.0, m2 = 0.0, S = 0.0;
+        for (int q = 0; q < 256; ++q) {
+            chan_merge(N, mu, m2, sn[q], sm[q], s2[q]);
+            S += sc[q];
+        }
+        slot[0] = N; slot[1] = mu; slot[2] = m2; slot[3] = S;   // slot 3: sequences with L_b > 0
     }
 }
 
@@ -200,13 +206,17 @@ cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_sl
 
 __global__ void whiten_merge_kernel(const double *gather, int world, int want, double *whiten,
                                     double *flags) {
-    double N = 0.0, mu = 0.0, M2 = 0.0;
-    for (int r = 0; r < world; ++r) chan_merge(N, mu, M2, gather[4 * r], gather[4 * r + 1], gather[4 * r + 2]);
+    double N = 0.0, mu = 0.0, M2 = 0.0, S = 0.0;
+    for (int r = 0; r < world; ++r) {
+        chan_merge(N, mu, M2, gather[4 * r], gather[4 * r + 1], gather[4 * r + 2]);
+        S += gather[4 * r + 3];
+    }
     const bool apply = want && N >= 2.0;
     whiten[0] = N;
     whiten[1] = apply ? mu : 0.0;
     whiten[2] = apply ? sqrt(M2 / N) : 0.0;
     whiten[3] = apply ? 1.0 : 0.0;
+    whiten[4] = S;
     flags[0] = (want && N < 2.0) ? 1.0 : 0.0;
 }
 
@@ -220,10 +230,10 @@ cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten
 __global__ void stats_pack_kernel(const double *acc, const unsigned long long *err, double *out) {
     const int k = threadIdx.x;
     if (k < kNumPartials) out[k] = acc[k];
-    if (k == 12) out[12] = (double)err[0];
-    if (k == 13) out[13] = (double)err[1];
-    if (k == 14) out[14] = (double)err[2];
-    if (k == 15) out[15] = 0.0;
+    else if (k == 16) out[16] = (double)err[0];
+    else if (k == 17) out[17] = (double)err[1];
+    else if (k == 18) out[18] = (double)err[2];
+    else if (k < kStatsSlots) out[k] = 0.0;
 }
 
 cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, double *out,
@@ -233,40 +243,42 @@ cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, 
 }
 
 // S10: rank-ordered sum of the gathered partials, then the means.
+// loss_agg = 1 (NEXT-2, Z31): policy/value/entropy/kl are means over the N_seq
+// sequences of per-sequence token means; shares and ratio stay token means.
 __global__ void stats_final_kernel(const double *gather, int world, const double *whiten,
                                    double *flags, double c1, double c2, double beta_loss,
-                                   int kl_in_loss, double *st) {
+                                   int kl_in_loss, int loss_agg, double *st) {
     double t[kStatsSlots];
     for (int k = 0; k < kStatsSlots; ++k) t[k] = 0.0;
     for (int r = 0; r < world; ++r)
         for (int k = 0; k < kStatsSlots; ++k) t[k] += gather[kStatsSlots * r + k];
-    const double N = t[0];
-    const double inv = N > 0.0 ? 1.0 / N : 0.0;
+    const double N = t[0], S = whiten[4];
+    const bool ok = N > 0.0;
+    const bool sm = loss_agg == 1 && S > 0.0;
     st[0] = N;
-    st[1] = N > 0.0 ? -t[1] / N : 0.0;
-    st[2] = N > 0.0 ? t[2] / N : 0.0;
-    st[3] = N > 0.0 ? t[3] / N : 0.0;
-    st[4] = N > 0.0 ? t[4] / N : 0.0;
-    st[5] = N > 0.0 ? t[7] / N : 0.0;
-    st[6] = N > 0.0 ? t[5] / N : 0.0;
-    st[7] = N > 0.0 ? t[6] / N : 0.0;
-    st[8] = N > 0.0 ? t[8] / N : 0.0;
-    (void)inv;
+    st[1] = !ok ? 0.0 : sm ? -t[11] / S : -t[1] / N;
+    st[2] = !ok ? 0.0 : sm ? t[12] / S : t[2] / N;
+    st[3] = !ok ? 0.0 : sm ? t[13] / S : t[3] / N;
+    st[4] = !ok ? 0.0 : sm ? t[14] / S : t[4] / N;
+    st[5] = ok ? t[7] / N : 0.0;
+    st[6] = ok ? t[5] / N : 0.0;
+    st[7] = ok ? t[6] / N : 0.0;
+    st[8] = ok ? t[8] / N : 0.0;
     st[9] = st[1] + c1 * st[2] - c2 * st[3] + (kl_in_loss ? beta_loss * st[4] : 0.0);
     st[10] = whiten[1];
     st[11] = whiten[2];
     st[12] = t[9];
-    st[13] = t[10] + t[13];
-    st[14] = t[12];
+    st[13] = t[10] + t[17];
+    st[14] = t[16];
     st[15] = flags[0];
-    flags[1] = t[14];  // invalid lengths (ORL_E_MASK)
+    flags[1] = t[18];  // invalid lengths (ORL_E_MASK)
 }
 
 cudaError_t launch_stats_final(const double *gather, int world, const double *whiten,
                                const double *flags, double c1, double c2, double beta_loss,
-                               int kl_in_loss, double *stats_out, cudaStream_t s) {
+                               int kl_in_loss, int loss_agg, double *stats_out, cudaStream_t s) {
     stats_final_kernel<<<1, 1, 0, s>>>(gather, world, whiten, const_cast<double *>(flags), c1, c2,
-                                       beta_loss, kl_in_loss, stats_out);
+                                       beta_loss, kl_in_loss, loss_agg, stats_out);
     return cudaGetLastError();
 }
 

@@ -99,8 +99,10 @@ __device__ __forceinline__ uint32_t f32x2_to_bf16x2(float lo, float hi) {
     return r;
 }
 
-// Row constants from the saved forward quantities.
-__device__ __forceinline__ k5::RowInfo row_info(const K5Params &p, int64_t gi, int y, float a) {
+// Row constants from the saved forward quantities.  a = c2/N (token mean) or
+// c2/(N_seq L_b) (NEXT-2 sequence mean).
+__device__ __forceinline__ k5::RowInfo row_info(const K5Params &p, int64_t gi, int y, int L) {
+    const float a = (float)(p.loss_agg == 1 ? p.c2 / (p.whiten[4] * (double)L) : p.c2 / p.whiten[0]);
     k5::RowInfo r;
     const float lse = __ldg(p.lse + gi), H = __ldg(p.entropy + gi), w = __ldg(p.dlogp + gi);
     r.y = y;
@@ -136,7 +138,6 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
     const int64_t row_bytes = p.V * (int64_t)sizeof(Tin);
     // The saved per-token inputs come from the actor pass (a previous kernel).
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const float a = (float)(p.c2 / p.whiten[0]);   // c2 / N_global
 
     if (warp == kConsumerWarps) {
         if (lane == 0) {
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                 int b, t;
                 locate_row(cum, p.B, j, b, t);
                 const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
-                const RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), a);
+                const RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), cum[b] - (b > 0 ? cum[b - 1] : 0));
                 const char *src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b,
                                                              p.stride_t) * (int64_t)sizeof(Tin);
                 for (int64_t off = 0; off < row_bytes; off += kChunk) {
@@ -283,7 +284,6 @@ __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
     }
     else k5_build_prefix(p, cum_s, warp_tot);
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const float a = (float)(p.c2 / p.whiten[0]);
     const int64_t total = (int64_t)p.B * p.T;
     for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
         const int b = (int)(q / p.T), t = (int)(q % p.T);
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
         const Tin *row = reinterpret_cast<const Tin *>(p.base) +
                          logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t);
         const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
-        const k5::RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), a);
+        const k5::RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), L);
         for (int64_t v = threadIdx.x; v < p.V; v += blockDim.x) {
             float x;
             if (sizeof(Tin) == 2) x = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(row)[v]) << 16);

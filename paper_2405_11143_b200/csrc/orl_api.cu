@@ -24,6 +24,7 @@
 using namespace orl;
 
 static_assert(sizeof(ncclUniqueId) == ORL_UNIQUE_ID_BYTES, "unique id size");
+static_assert(kStatsSlots == ORL_PARTIALS_N && kStatsOut == ORL_STATS_N, "stats vector sizes");
 
 namespace {
 constexpr int kMaxWorld = 256;
@@ -214,16 +215,16 @@ extern "C" orl_status orl_create(int device, int world, int rank, const unsigned
               cudaMalloc(&ctx->d_ws, (size_t)kNumPartials * ctx->ws_stride * sizeof(double)) == cudaSuccess &&
               cudaMalloc(&ctx->d_ticket, sizeof(unsigned int)) == cudaSuccess &&
               cudaMalloc(&ctx->d_gather_w, (size_t)kMaxWorld * 4 * sizeof(double)) == cudaSuccess &&
-              cudaMalloc(&ctx->d_whiten, 4 * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ctx->d_whiten, kWhitenSlots * sizeof(double)) == cudaSuccess &&
               cudaMalloc(&ctx->d_flags, 4 * sizeof(double)) == cudaSuccess &&
               cudaMalloc(&ctx->d_gather_s, (size_t)kMaxWorld * kStatsSlots * sizeof(double)) == cudaSuccess &&
-              cudaMalloc(&ctx->d_stats, kStatsSlots * sizeof(double)) == cudaSuccess &&
-              cudaMallocHost(&ctx->h_stats, (kStatsSlots + 4) * sizeof(double)) == cudaSuccess;
+              cudaMalloc(&ctx->d_stats, kStatsOut * sizeof(double)) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_stats, (kStatsOut + 4) * sizeof(double)) == cudaSuccess;
     if (!ok) return cleanup_fail(fail(nullptr, ORL_E_CUDA, "device allocation failed"));
     ok = cudaMemset(ctx->d_acc, 0, 16 * sizeof(double)) == cudaSuccess &&
          cudaMemset(ctx->d_err, 0, kNumErr * sizeof(unsigned long long)) == cudaSuccess &&
          cudaMemset(ctx->d_ticket, 0, sizeof(unsigned int)) == cudaSuccess &&
-         cudaMemset(ctx->d_whiten, 0, 4 * sizeof(double)) == cudaSuccess &&
+         cudaMemset(ctx->d_whiten, 0, kWhitenSlots * sizeof(double)) == cudaSuccess &&
          cudaMemset(ctx->d_flags, 0, 4 * sizeof(double)) == cudaSuccess &&
          cudaDeviceSynchronize() == cudaSuccess;
     if (!ok) return cleanup_fail(fail(nullptr, ORL_E_CUDA, "device init failed"));
@@ -272,7 +273,7 @@ extern "C" orl_status orl_begin_iteration(orl_ctx *ctx, void *stream) {
     cudaStream_t s = as_stream(stream);
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_acc, 0, 16 * sizeof(double), s));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_err, 0, kNumErr * sizeof(unsigned long long), s));
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_whiten, 0, 4 * sizeof(double), s));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_whiten, 0, kWhitenSlots * sizeof(double), s));
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(double), s));
     ctx->have_adv = ctx->have_whiten = false;
     ctx->imported_w = ctx->imported_s = 0;
@@ -426,6 +427,8 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
         return fail(ctx, ORL_E_INVALID_ARG, "invalid orl_ppo_cfg values");
     if (cfg->kl_loss_est < 1 || cfg->kl_loss_est > 3)
         return fail(ctx, ORL_E_INVALID_ARG, "kl_loss_est=%d not in {1,2,3}", cfg->kl_loss_est);
+    if (cfg->loss_agg != 0 && cfg->loss_agg != 1)
+        return fail(ctx, ORL_E_INVALID_ARG, "loss_agg=%d not in {0,1}", cfg->loss_agg);
     if (cfg->kl_in_loss && !logp_ref) return fail(ctx, ORL_E_INVALID_ARG, "kl_in_loss needs logp_ref");
     if (!ctx->have_whiten) return fail(ctx, ORL_E_STATE, "orl_ppo_loss before orl_whiten_stats");
     if ((st = set_device(ctx))) return st;
@@ -450,6 +453,7 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
     p.ratio_guard = cfg->ratio_guard;
     p.kl_loss_est = cfg->kl_loss_est;
     p.kl_in_loss = cfg->kl_in_loss;
+    p.loss_agg = cfg->loss_agg;
     if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
     CUDA_TRY(ctx, launch_k1(p, tma_eligible(actor), kModeLoss, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
@@ -499,6 +503,7 @@ extern "C" orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const 
     p.dlogp = dloss_dlogp;
     p.whiten = ctx->d_whiten;
     p.zero_masked = zero_masked ? 1 : 0;
+    p.loss_agg = cfg->loss_agg;
     const int64_t elt = p.elt;
     const bool tma = tma_eligible(actor) && (reinterpret_cast<uintptr_t>(dlogits) % 16 == 0) &&
                      ((out_stride_t * elt) % 16 == 0) && ((out_stride_b * elt) % 16 == 0);
@@ -527,15 +532,15 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
                                         kStatsSlots, ncclDouble, ctx->comm, s));
     }
     CUDA_TRY(ctx, launch_stats_final(ctx->d_gather_s, world, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
-                                     cfg->beta_loss, cfg->kl_in_loss, ctx->d_stats, s));
+                                     cfg->beta_loss, cfg->kl_in_loss, cfg->loss_agg, ctx->d_stats, s));
     ctx->launches += 1;
     ctx->imported_s = 0;
     if (dev_out)
-        CUDA_TRY(ctx, cudaMemcpyAsync(dev_out, ctx->d_stats, kStatsSlots * sizeof(double),
+        CUDA_TRY(ctx, cudaMemcpyAsync(dev_out, ctx->d_stats, kStatsOut * sizeof(double),
                                       cudaMemcpyDeviceToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, kStatsSlots * sizeof(double),
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, kStatsOut * sizeof(double),
                                   cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats + kStatsSlots, ctx->d_flags, 4 * sizeof(double),
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats + kStatsOut, ctx->d_flags, 4 * sizeof(double),
                                   cudaMemcpyDeviceToHost, s));
     CUDA_TRY(ctx, cudaStreamSynchronize(s));
     const double *h = ctx->h_stats;
@@ -558,7 +563,7 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
         host_out->whiten_warn = h[15] != 0.0;
         host_out->pad_ = 0;
     }
-    const double mask_err = h[kStatsSlots + 1];
+    const double mask_err = h[kStatsOut + 1];
     if (h[14] > 0) return fail(ctx, ORL_E_TOKEN_RANGE, "%lld token(s) outside [0, V)", (long long)h[14]);
     if (mask_err > 0) return fail(ctx, ORL_E_MASK, "%lld invalid length(s)", (long long)mask_err);
     if (h[13] > 0) return fail(ctx, ORL_E_NONFINITE, "%lld non-finite value(s)", (long long)h[13]);

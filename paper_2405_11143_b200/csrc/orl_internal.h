@@ -13,8 +13,11 @@ enum K1Mode { kModeLogprob = 0, kModeLoss = 1 };
 // Loss-partial vector (fp64), one per CTA and per context accumulator:
 //  0 n  1 sum obj  2 sum vl  3 sum H  4 sum k(new,ref)  5 n clipped
 //  6 n value-clipped  7 sum k3(old-new)  8 sum rho  9 n guard
-//  10 n non-finite loss terms  11 unused
-constexpr int kNumPartials = 12;
+//  10 n non-finite loss terms
+//  11..14 per-sequence-mean sums (NEXT-2): sum obj/L_b, vl/L_b, H/L_b, k/L_b
+constexpr int kNumPartials = 15;
+// Whitening/count vector on the device: N_global, mu, sigma, apply, N_seq, 0, 0, 0
+constexpr int kWhitenSlots = 8;
 // Device error counters (uint64): 0 token out of range, 1 non-finite S1 rows,
 // 2 invalid lengths (L_b < 0 or > T).
 constexpr int kNumErr = 4;
@@ -42,8 +45,8 @@ struct K1Params {
     const float *logp_old, *logp_ref, *adv, *ret, *v_new, *v_old;
     float *dlogp, *dv;
     double eps_low, eps_high, eps_v, c1, beta_loss, ratio_guard;
-    int kl_loss_est, kl_in_loss;
-    const double *whiten;  // device [4]: N_global, mu, sigma, apply
+    int kl_loss_est, kl_in_loss, loss_agg;
+    const double *whiten;  // device [kWhitenSlots]: N_global, mu, sigma, apply, N_seq
     const int32_t *cum_global;  // prefix of the micro-batch lengths (large B), else NULL
     // accounting
     double *ws;            // [kNumPartials][ws_stride] per-CTA partials
@@ -78,9 +81,10 @@ struct K5Params {
     const int32_t *tokens, *lengths;
     const int32_t *cu_seqlens;           // packed varlen logits / dlogits, else NULL
     const float *lse, *entropy, *dlogp;  // saved by the actor pass
-    const double *whiten;                // device [4]: N_global first
+    const double *whiten;                // device [kWhitenSlots]: N_global first, N_seq at 4
     const int32_t *cum_global;           // prefix of the micro-batch lengths (large B), else NULL
     int zero_masked;
+    int loss_agg;                        // 0 token mean, 1 sequence mean (NEXT-2)
 };
 cudaError_t launch_k5(const K5Params &p, bool tma, int num_sms, cudaStream_t s);
 size_t k5_smem_bytes(int B);
@@ -106,13 +110,14 @@ cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten
                                 double *flags, cudaStream_t s);
 
 // Fold the error counters into the loss accumulator copy for the collective:
-// out[kStatsSlots] = acc[0..11], err -> slots 12..14.
-constexpr int kStatsSlots = 16;
+// out[kStatsSlots] = acc[0..14], err -> slots 16..18 (ORL_PARTIALS_N in orl.h).
+constexpr int kStatsSlots = 24;
+constexpr int kStatsOut = 16;  // final stats vector (ORL_STATS_N)
 cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, double *out,
                               cudaStream_t s);
 // Sum gathered [world][16] in rank order and form the stats vector.
 cudaError_t launch_stats_final(const double *gather, int world, const double *whiten,
                                const double *flags, double c1, double c2, double beta_loss,
-                               int kl_in_loss, double *stats_out, cudaStream_t s);
+                               int kl_in_loss, int loss_agg, double *stats_out, cudaStream_t s);
 
 }  // namespace orl

@@ -23,6 +23,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 UNIQUE_ID_BYTES = 128
 STATS_N = 16
+PARTIALS_N = 24
+LOSS_AGG = {"token_mean": 0, "seq_mean_token_mean": 1}
 MAX_SEQ_PER_CALL = 8192
 
 STATUS = {0: "ORL_OK", 1: "ORL_E_INVALID_ARG", 2: "ORL_E_SHAPE", 3: "ORL_E_ALIGN", 4: "ORL_E_DTYPE",
@@ -49,7 +51,8 @@ class PpoCfg(ctypes.Structure):
     _fields_ = [("eps_low", ctypes.c_double), ("eps_high", ctypes.c_double),
                 ("eps_value", ctypes.c_double), ("c1", ctypes.c_double), ("c2", ctypes.c_double),
                 ("beta_loss", ctypes.c_double), ("kl_loss_est", ctypes.c_int32),
-                ("kl_in_loss", ctypes.c_int32), ("ratio_guard", ctypes.c_double)]
+                ("kl_in_loss", ctypes.c_int32), ("ratio_guard", ctypes.c_double),
+                ("loss_agg", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -118,10 +121,12 @@ class PPOConfig:
     kl_loss_est: str = "k2"
     kl_in_loss: bool = False
     ratio_guard: float = 30.0
+    loss_agg: str = "token_mean"
 
     def c(self) -> PpoCfg:
         return PpoCfg(self.eps_low, self.eps_high, self.eps_value, self.c1, self.c2, self.beta_loss,
-                      KL[self.kl_loss_est], int(bool(self.kl_in_loss)), self.ratio_guard)
+                      KL[self.kl_loss_est], int(bool(self.kl_in_loss)), self.ratio_guard,
+                      LOSS_AGG[self.loss_agg], 0)
 
 
 def version() -> int:
@@ -271,7 +276,7 @@ def orl_finalize(ctx: Context, cfg: PPOConfig, dev_out=None, stream=None, raise_
 
 def orl_export_partials(ctx: Context, which: int, stream=None):
     import numpy as np
-    n = 4 if which == 0 else STATS_N
+    n = 4 if which == 0 else PARTIALS_N
     buf = np.zeros(n, dtype=np.float64)
     ctx.check(_lib.orl_export_partials(ctx.h, int(which), buf.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
     return buf

@@ -38,7 +38,8 @@ class PathConfig:
                    beta_reward=c.get("beta_reward", 0.0) if kl_mode == "reward" else 0.0,
                    ppo=_orl.PPOConfig(eps_low=c["eps_low"], eps_high=c["eps_high"], eps_value=c["eps_v"],
                                       c1=c["c1"], c2=c["c2"], beta_loss=c.get("beta_loss", 0.0),
-                                      kl_loss_est=c.get("kl_est_loss", "k2"), kl_in_loss=kl_mode == "loss"))
+                                      kl_loss_est=c.get("kl_est_loss", "k2"), kl_in_loss=kl_mode == "loss",
+                                      loss_agg=c.get("loss_agg", "token_mean")))
 
     @property
     def critic(self) -> bool:

@@ -563,3 +563,38 @@ def test_next2_packed_varlen_matches_padded(ctx):
         assert torch.equal(getattr(bk, k), getattr(bp, k)), k
     for b in range(B):
         assert torch.equal(dl_pk[int(cu[b]):int(cu[b + 1])], dl_pad[b, : int(L[b])])
+
+
+@pytest.mark.parametrize("kind", ["gae", "grpo"])
+def test_next2_seq_mean_aggregation(ctx, kind):
+    """Sequence-mean loss aggregation (NEXT-2, Z31): stats, per-token gradients and
+    dL/dlogits against the oracle (stage isolation), tiny fp32 and mid bf16."""
+    for dtype, V, B, T in (("f32", 32, 8, 16), ("bf16", 4096, 6, 48)):
+        c = dict(synth.CONFIGS["tiny"], V=V, adv_kind=kind, loss_agg="seq_mean_token_mean", c2=0.02,
+                 group_size=2 if kind == "grpo" else 1)
+        if kind == "grpo":
+            c.update(kl_mode="loss", kl_est_loss="k3", beta_loss=0.05, whiten=False, eps_v=0.0, c1=0.0)
+        if dtype == "f32":
+            g = _to_dev(synth.make_batch(3, B, T, V, "f32", "stress", "tiny", c["rewards"], c["group_size"]))
+        else:
+            g = _gpu_batch(3, B, T, V, "mixed", "group_bernoulli" if kind == "grpo" else "normal", 2, "stress")
+        cfg = PathConfig.from_synth(c)
+        tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+        dl = torch.zeros(B, T, V, dtype=tdt, device=DEV)
+        bufs = Buffers(B, T, DEV, c["group_size"])
+        src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+        status, st = run_iteration(ctx, g, cfg, bufs, src, mb=3, grad_sink=lambda s, e: dl[s:e])
+        torch.cuda.synchronize()
+        assert status == "ORL_OK"
+        npb = synth.batch_to_numpy(g)
+        m = parity.valid_mask(npb["lengths"], T)
+        out_i, glob_i = _isolated_oracle(npb, bufs, c)
+        _check_downstream(bufs, out_i[0], glob_i, st, m, f"seqmean-{kind}-{dtype}")
+        n_seq = float(np.count_nonzero(npb["lengths"] > 0))
+        o = oracle.logits_grad(npb["logits_new"], npb["tokens"], npb["lengths"], _np(bufs.dlogp).astype(np.float64),
+                               1.0, 0.02, float(m.sum()), seq_mean=True, n_seq=n_seq)
+        H = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"])["entropy"]
+        # per-row entropy weight a = c2 / (n_seq L_b): bound it by the largest (shortest row)
+        a_max = 0.02 / (n_seq * max(1, int(npb["lengths"][npb["lengths"] > 0].min())))
+        _check_grad(dl.float().cpu().numpy(), o, m, 2e-5 if dtype == "f32" else 8e-3, f"seqmean-{dtype}",
+                    _np(bufs.dlogp), H, a_max, 1.0)

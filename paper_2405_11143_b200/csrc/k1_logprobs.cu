@@ -369,8 +369,14 @@ struct ThreadAcc {
 
 __device__ __forceinline__ uint64_t bf16x2_to_f32x2(uint32_t w) {
     uint64_t r;
+#ifdef ORL_K1_PRMT_UNPACK
+    // byte permutes on the ALU pipe (no IMAD on the FMA pipe for the shift)
+    asm("{\n\t.reg .b32 lo, hi;\n\tprmt.b32 lo, %1, 0, 0x1044;\n\tprmt.b32 hi, %1, 0, 0x3244;\n\t"
+        "mov.b64 %0, {lo, hi};\n\t}" : "=l"(r) : "r"(w));
+#else
     asm("{\n\t.reg .b32 lo, hi;\n\tshl.b32 lo, %1, 16;\n\tand.b32 hi, %1, 0xffff0000;\n\t"
         "mov.b64 %0, {lo, hi};\n\t}" : "=l"(r) : "r"(w));
+#endif
     return r;
 }
 

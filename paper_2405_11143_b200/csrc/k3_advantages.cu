@@ -189,13 +189,19 @@ __global__ void whiten_local_kernel(const double *seq_part, int B, double *slot)
     }
     sn[tid] = n; sm[tid] = mean; s2[tid] = M2; sc[tid] = nseq;
     __syncthreads();
-    if (tid == 0) {
-        double N = 0.0, mu = 0.0, m2 = 0.0, S = 0.0;
-        for (int q = 0; q < 256; ++q) {
-            chan_merge(N, mu, m2, sn[q], sm[q], s2[q]);
-            S += sc[q];
+    // fixed-shape pairwise tree (deterministic, log depth): slot i absorbs i + h
+    for (int h = 128; h >= 1; h >>= 1) {
+        if (tid < h) {
+            double a = sn[tid], am = sm[tid], a2 = s2[tid];
+            chan_merge(a, am, a2, sn[tid + h], sm[tid + h], s2[tid + h]);
+            sn[tid] = a; sm[tid] = am; s2[tid] = a2;
+            sc[tid] += sc[tid + h];
         }
-        slot[0] = N; slot[1] = mu; slot[2] = m2; slot[3] = S;   // slot 3: sequences with L_b > 0
+        __syncthreads();
+    }
+    if (tid == 0) {
+        slot[0] = sn[0]; slot[1] = sm[0]; slot[2] = s2[0];
+        slot[3] = sc[0];   // sequences with L_b > 0
     }
 }
 

@@ -190,6 +190,7 @@ def run_ours(args):
     B, T, V, mb = c["B"], c["T"], c["V"], c["mb"]
     if args.batch:
         B = args.batch
+    pool_mb = 0
     cfg = PathConfig.from_synth(c)
     seed = 1234 + rank
     tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
@@ -200,14 +201,32 @@ def run_ours(args):
     tok = synth.tokens_for(B, T, V, seed).to(dev)
     R = synth.rewards_for(B, seed, c["rewards"], c["group_size"]).to(dev)
     v_old, v_new = (v.to(dev) for v in synth.values_for(B, T, seed))
-    logits = {r: torch.empty(B, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
-    for s in range(0, B, mb):
-        e = min(B, s + mb)
-        synth.fill_logits_(tuple(logits[r][s:e] for r in synth.ROLES), tok[s:e], seed, s // mb, "realistic")
+    full_bytes = 3 * B * T * V * elt
+    pooled = full_bytes > 0.80 * torch.cuda.mem_get_info()[0]
+    if pooled:
+        # The three models' logits of this config do not fit in HBM (e.g. longcot
+        # 3 x 79.7 GB, grpo 3 x 2.15 TB): every micro-batch streams from a pool of
+        # `pool_mb` micro-batch buffers per model (>= 8 GB each, >> L2), filled once.
+        per_mb = mb * T * V * elt
+        pool_mb = max(1, min(len(range(0, B, mb)), int(0.70 * torch.cuda.mem_get_info()[0] // (3 * per_mb))))
+        pool = {r: torch.empty(pool_mb * mb, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
+        for k in range(pool_mb):
+            sl = slice(k * mb, (k + 1) * mb)
+            synth.fill_logits_(tuple(pool[r][sl] for r in synth.ROLES), tok[sl], seed, k, "realistic")
+        logits = None
+
+        def src(role, s, e):
+            k = (s // mb) % pool_mb
+            return pool[role][k * mb:k * mb + (e - s)]
+    else:
+        logits = {r: torch.empty(B, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
+        for s in range(0, B, mb):
+            e = min(B, s + mb)
+            synth.fill_logits_(tuple(logits[r][s:e] for r in synth.ROLES), tok[s:e], seed, s // mb, "realistic")
+        src = lambda role, s, e: logits[role][s:e]  # noqa: E731
     batch = dict(tokens=tok, lengths=L, seq_reward=R, values_old=v_old, values_new=v_new)
     bufs = Buffers(B, T, dev, c["group_size"])
     stream = torch.cuda.current_stream()
-    src = lambda role, s, e: logits[role][s:e]  # noqa: E731
     n_tok_rank = int(L.clamp(max=T).sum().item())
     n_mb = len(range(0, B, mb))
 
@@ -292,12 +311,12 @@ def run_ours(args):
 
     # ---- NEXT-1: the backward pass dL/dlogits (separate leg, not in `value`) ----
     next1 = None
-    if not args.no_next1 and world == 1:
+    if not args.no_next1 and world == 1 and not pooled:
         next1 = run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok_rank)
 
     # ---- e2e: host buffers, H2D/D2H inside the timed region --------------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not pooled:
         e2e = run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank)
 
     # ---- oracle on the host cores (rank 0, N = 1 only) ------------------------
@@ -305,8 +324,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         n_seq = args.ref_seqs
         cores = len(os.sched_getaffinity(0))
+        n_seq = min(n_seq, mb) if pooled else n_seq
         bnp = {k: v[:n_seq].detach().cpu().numpy() for k, v in batch.items()}
-        host_logits = {r: synth.to_numpy_logits(logits[r][:n_seq]) for r in synth.ROLES}
+        host_logits = {r: synth.to_numpy_logits(src(r, 0, n_seq)) for r in synth.ROLES}
         toks, dt = _oracle_sample(lambda role, n: host_logits[role][:n], bnp, c, n_seq, cores)
         cpu = {"value": toks / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {n_seq} sequences x {T} tokens of the same rollout (3 x {n_seq * T} vocab rows), "
@@ -318,7 +338,9 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
                 "config": {"workload": _workload_desc(args.config, c, B, world), "global_batch": B * world,
                            "seq_len": T, "vocab": V, "parallelism": f"dp{world}",
-                           "l2": "inputs larger than L2 (3 x %.1f GB logits per rank vs 126 MB L2)" % (B * T * V * elt / 1e9)},
+                           "l2": "inputs larger than L2 (3 x %.1f GB logits per rank vs 126 MB L2)" % (B * T * V * elt / 1e9),
+                           "logits": ("pool of %d micro-batch buffers per model reused across the %d micro-batches "
+                                      "(full batch does not fit)" % (pool_mb, n_mb)) if pooled else "resident"},
                 "status": status, "stats": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in st.items()},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
                 "next1_logits_grad": next1,

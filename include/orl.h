@@ -310,6 +310,21 @@ orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits 
 orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
                         double *dev_out, void *stream);
 
+/* orl_ppo_loss and orl_logits_grad in one pass over the actor logits (NEXT-1,
+ * fused): every row is streamed from HBM once for the loss epilogue (kept in L2
+ * with an evict_last hint) and re-read from L2 one row later for the gradient,
+ * so the HBM traffic is V*elt read + V*elt written per token instead of
+ * 2 V*elt read + V*elt written.  Same arguments and outputs as the two calls;
+ * entropy, lse and dloss_dlogp are required here.  Falls back to the two
+ * passes when the logits or dlogits layout is not 16-byte aligned. */
+orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
+                                 float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
+                                 const float *logp_ref, const float *adv, const float *ret,
+                                 const float *v_new, const float *v_old, float *logp_new,
+                                 float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
+                                 void *dlogits, int64_t out_stride_b, int64_t out_stride_t,
+                                 int zero_masked, void *stream);
+
 /* ---- NEXT-3: adaptive KL coefficient and early stop (host only) -------- */
 
 /* Host scalar update, no device work ("adaptive KL penalty

@@ -78,6 +78,19 @@ struct RowSlot {
     float pad[31];
 };
 
+// Backward row constants (kModeLossGrad): published by the epilogue warp of the
+// row, read by the consumers when they stream the row a second time (from L2).
+struct GradRow {
+    int64_t out_off;  // element offset of the dlogits row
+    int32_t y;
+    float l2;         // lse * log2(e)
+    float A1;         // inv_temp * a * ln2,   a = c2/N or c2/(N_seq L_b)
+    float A0;         // inv_temp * (a H - w)
+    float wt;         // inv_temp * w   (delta term at v = y)
+    int32_t pad;
+};
+constexpr int kGradRows = 4;  // ring; each slot always written by the same epilogue warp
+
 struct __align__(128) K1Smem {
     uint8_t stage[kStages][kChunk];
     uint64_t full[kStages];
@@ -85,6 +98,8 @@ struct __align__(128) K1Smem {
     uint64_t row_full[kSlots];
     uint64_t row_empty[kSlots];
     int32_t row_y[kRowInfo];
+    uint64_t grad_full[kGradRows];
+    GradRow grad[kGradRows];
     RowSlot slot[kSlots];
     double wacc[kEpiWarps][kNumPartials];
 };
@@ -206,7 +221,7 @@ __device__ void zero_masked(const K1Params &p, const int32_t *cum, int lt, int n
 __device__ __forceinline__ float load_side(const K1Params &p, int mode, int k, int64_t i, int b) {
     const float *ptr = nullptr;
     int64_t idx = i;
-    if (mode == kModeLoss) {
+    if (mode != kModeLogprob) {
         ptr = k == 0 ? p.logp_old : k == 1 ? p.logp_ref : k == 2 ? p.adv : k == 3 ? p.ret
             : k == 4 ? p.v_new : k == 5 ? p.v_old : nullptr;
     } else {
@@ -218,9 +233,15 @@ __device__ __forceinline__ float load_side(const K1Params &p, int mode, int k, i
 
 // fp64 per-row epilogue (runs on one thread).  `tot` is the merged online
 // state of the row, `target` the raw logit x[b,t,y] (as float, exact).
+// Quantities the fused backward needs from the forward epilogue of a row.
+struct EpiOut {
+    float lse, H, w;
+};
+
 template <int MODE>
 __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Online tot,
-                             float target, const float *side, const double *wh, double *wacc) {
+                             float target, const float *side, const double *wh, double *wacc,
+                             EpiOut *eo = nullptr) {
     const int64_t i = (p.seq_offset + b) * (int64_t)p.T + t;
     const bool oob = (y < 0) || (y >= p.V);
     const double log2s = log2((double)tot.s);
@@ -309,10 +330,14 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         wacc[12] += vl * invL;
         wacc[13] += Hd * invL;
         wacc[14] += kref * invL;
-        if (p.dlogp)
-            p.dlogp[i] = (float)(((clipped ? 0.0 : -rho * A) +
-                                  (p.kl_in_loss ? p.beta_loss * dkref : 0.0)) / N);
+        const float wf = (float)(((clipped ? 0.0 : -rho * A) + (p.kl_in_loss ? p.beta_loss * dkref : 0.0)) / N);
+        if (p.dlogp) p.dlogp[i] = wf;
         if (p.dv) p.dv[i] = (float)(p.c1 * dvl / N);
+        if (eo) {
+            eo->lse = (float)lse;
+            eo->H = H_f;
+            eo->w = wf;
+        }
     }
 }
 
@@ -573,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             mbar_init(&S.row_full[s], kConsumerWarps);
             mbar_init(&S.row_empty[s], 1);
         }
+        for (int s = 0; s < kGradRows; ++s) mbar_init(&S.grad_full[s], 1);
         fence_mbar_init();
     }
     if (tid < kEpiWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
@@ -592,34 +618,51 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 
     if (warp == kProducerWarp) {
         // ===================== producer: one lane issues the TMA bulk copies ======
+        // kModeLossGrad streams every row twice: forward chunks F(i) (kept in L2
+        // with evict_last) and, one row later, the same row again for the backward
+        // B(i) (an L2 hit, evict_first): F0, F1, B0, F2, B1, ..., B(n-1).
         if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
+            const uint64_t pol_first = l2_evict_first_policy();
+            const uint64_t pol_fwd = MODE == kModeLossGrad ? l2_evict_last_policy() : pol_first;
             int stage = 0;
             uint32_t phase = 0;
-            int64_t j = blockIdx.x;
+            const int64_t n_rows = N > (int64_t)blockIdx.x ? (N - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
             int b = 0, t = 0, y = 0;
-            if (j < N) {
-                locate_row(cum, p.B, j, b, t);
+            if (n_rows > 0) {
+                locate_row(cum, p.B, blockIdx.x, b, t);
                 y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
             }
-            for (int rl = 0; j < N; j += gridDim.x, ++rl) {
-                const int64_t jn = j + gridDim.x;  // prefetch the next row's token id
-                int bn = 0, tn = 0, yn = 0;
-                if (jn < N) {
-                    locate_row(cum, p.B, jn, bn, tn);
-                    yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
+            const char *prev_src = nullptr;
+            for (int64_t rl = 0; rl <= n_rows; ++rl) {
+                const char *src = nullptr;
+                if (rl < n_rows) {
+                    const int64_t jn = blockIdx.x + (rl + 1) * (int64_t)gridDim.x;  // prefetch next row's token
+                    int bn = 0, tn = 0, yn = 0;
+                    if (jn < N) {
+                        locate_row(cum, p.B, jn, bn, tn);
+                        yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
+                    }
+                    src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
+                    for (int64_t off = 0; off < row_bytes; off += kChunk) {
+                        const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
+                        mbar_wait(&S.empty[stage], phase ^ 1u);
+                        if (off == 0) S.row_y[rl % kRowInfo] = y;  // published by the arrive below
+                        mbar_arrive_expect_tx(&S.full[stage], bytes);
+                        tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol_fwd);
+                        if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                    }
+                    b = bn; t = tn; y = yn;
                 }
-                const char *src =
-                    p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
-                for (int64_t off = 0; off < row_bytes; off += kChunk) {
-                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
-                    mbar_wait(&S.empty[stage], phase ^ 1u);
-                    if (off == 0) S.row_y[rl % kRowInfo] = y;  // published by the arrive below
-                    mbar_arrive_expect_tx(&S.full[stage], bytes);
-                    tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
-                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                if (MODE == kModeLossGrad && rl > 0) {
+                    for (int64_t off = 0; off < row_bytes; off += kChunk) {
+                        const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
+                        mbar_wait(&S.empty[stage], phase ^ 1u);
+                        mbar_arrive_expect_tx(&S.full[stage], bytes);
+                        tma_load_1d(S.stage[stage], prev_src + off, bytes, &S.full[stage], pol_first);
+                        if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                    }
                 }
-                b = bn; t = tn; y = yn;
+                prev_src = src;
             }
         }
         return;
@@ -631,11 +674,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         asm volatile("griddepcontrol.wait;" ::: "memory");
         zero_masked(p, cum, lane + 32 * ew, 32 * kEpiWarps, MODE);
         double wh[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        if (MODE == kModeLoss) {
+        if (MODE != kModeLogprob) {
             wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
             wh[4] = p.whiten[4];
         }
-        const int nside = MODE == kModeLoss ? 6 : 2;
+        const int nside = MODE != kModeLogprob ? 6 : 2;
         for (int64_t j = blockIdx.x + (int64_t)ew * gridDim.x, rl = ew; j < N;
              j += (int64_t)kEpiWarps * gridDim.x, rl += kEpiWarps) {
             int b, t;
@@ -660,11 +703,24 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             if (lane == 0) {
                 mbar_arrive(&S.row_empty[slot]);
                 const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew]);
+                EpiOut eo{0.f, 0.f, 0.f};
+                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew], &eo);
+                if (MODE == kModeLossGrad) {
+                    // same fp32 constants as K5 (orl_logits_grad) computes from the saved arrays
+                    const float a = (float)(p.loss_agg == 1 ? p.c2_ent / (wh[4] * (double)L) : p.c2_ent / wh[0]);
+                    GradRow &g = S.grad[rl % kGradRows];
+                    g.out_off = logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.out_stride_b, p.out_stride_t);
+                    g.y = y;
+                    g.l2 = eo.lse * kLog2e;
+                    g.A1 = p.inv_temp * a * (float)kLn2;
+                    g.A0 = p.inv_temp * (a * eo.H - eo.w);
+                    g.wt = p.inv_temp * eo.w;
+                    mbar_arrive(&S.grad_full[rl % kGradRows]);
+                }
             }
             __syncwarp();
         }
-        if (MODE == kModeLoss) {
+        if (MODE != kModeLogprob) {
             if (kEpiWarps > 1) named_bar_sync(1, 32 * kEpiWarps);
             if (ew == 0) {
                 double tot[kNumPartials];
@@ -685,12 +741,15 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 #ifdef ORL_K1_ALWAYS_ENT
     const bool ent = true;
 #else
-    const bool ent = MODE == kModeLoss || p.entropy != nullptr;
+    const bool ent = MODE != kModeLogprob || p.entropy != nullptr;
 #endif
     const uint64_t c2p = pack2(p.c2, p.c2);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t j = blockIdx.x, rl = 0; j < N; j += gridDim.x, ++rl) {
+    const int64_t n_rows = N > (int64_t)blockIdx.x ? (N - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    for (int64_t rl = 0; rl <= n_rows; ++rl) {
+        if (rl < n_rows) {
+        // ---------------- forward pass over row rl ----------------
         ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
         float tgt = 0.f;
         bool have_tgt = false;
@@ -741,6 +800,98 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         if (have_tgt) R.target = tgt;
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.row_full[slot]);
+        }
+        if (MODE == kModeLossGrad && rl > 0) {
+            // ---------------- backward pass over row rl-1 (NEXT-1, from L2) ----------------
+            // dL/dx_v = p_v (A1 t_v + A0) + [v = y] wt,  t_v = (x_v c - lse log2e)
+            const int64_t rb = rl - 1;
+            mbar_wait(&S.grad_full[rb % kGradRows], (uint32_t)(rb / kGradRows) & 1u);
+            const GradRow g = S.grad[rb % kGradRows];
+            Tin *orow = reinterpret_cast<Tin *>(p.dlogits) + g.out_off;
+            const uint64_t nl2 = pack2(-g.l2, -g.l2), A1p = pack2(g.A1, g.A1), A0p = pack2(g.A0, g.A0);
+            const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin);
+            for (int64_t off = 0; off < row_bytes; off += kChunk) {
+                const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
+                const int nvec = bytes >> 4;
+                mbar_wait(&S.full[stage], phase);
+                const uint8_t *sb = S.stage[stage];
+                const bool own_y = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= off && ybyte < off + bytes &&
+                                   (((int)(ybyte - off) >> 4) % kConsumers) == ct;
+                float xy = 0.f;
+                if (own_y) {
+                    const uint8_t *q = sb + (ybyte - off);
+                    xy = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(q)) << 16)
+                                          : *reinterpret_cast<const float *>(q);
+                }
+                uint4 v[kVecPerThread];
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    const int vi = ct + k * kConsumers;
+                    if (vi < nvec) v[k] = lds128(sb + vi * 16);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.empty[stage]);
+                if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                char *obase = reinterpret_cast<char *>(orow) + off;
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    const int vi = ct + k * kConsumers;
+                    if (vi >= nvec) continue;
+                    const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                    uint32_t o[4];
+                    if (sizeof(Tin) == 2) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[q]), c2p, nl2);
+                            float t0, t1;
+                            unpack2(t2, t0, t1);
+                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
+                            float g0, g1;
+                            unpack2(gr, g0, g1);
+                            o[q] = f32x2_to_bf16x2_rn(g0, g1);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            uint64_t x;
+                            asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(w4[2 * q]), "r"(w4[2 * q + 1]));
+                            const uint64_t t2 = ffma2(x, c2p, nl2);
+                            float t0, t1;
+                            unpack2(t2, t0, t1);
+                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
+                            float g0, g1;
+                            unpack2(gr, g0, g1);
+                            o[2 * q] = __float_as_uint(g0);
+                            o[2 * q + 1] = __float_as_uint(g1);
+                        }
+                    }
+                    stg128_cs(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+                }
+                if (own_y) {  // program-ordered rewrite of the target element with the delta term
+                    const float t2 = fmaf(xy, p.c2, -g.l2);
+                    const float gy = ex2(t2) * fmaf(g.A1, t2, g.A0) + g.wt;
+                    if (sizeof(Tin) == 2) {
+                        const uint32_t hb = f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu;
+                        asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + g.y), "h"((unsigned short)hb) : "memory");
+                    } else {
+                        reinterpret_cast<float *>(orow)[g.y] = gy;
+                    }
+                }
+            }
+        }
+    }
+    if (MODE == kModeLossGrad && p.zero_masked_grad && !p.cu_seqlens) {
+        // zero the dlogits rows of the masked positions (padded layout)
+        const int64_t total = (int64_t)p.B * p.T;
+        for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
+            const int b = (int)(q / p.T), t = (int)(q % p.T);
+            const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+            if (t < L) continue;
+            char *orow = reinterpret_cast<char *>(p.dlogits) +
+                         ((int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t) * (int64_t)sizeof(Tin);
+            for (int64_t o = (int64_t)ct * 16; o < row_bytes; o += (int64_t)kConsumers * 16)
+                stg128_cs(orow + o, make_uint4(0u, 0u, 0u, 0u));
+        }
     }
 }
 
@@ -766,7 +917,7 @@ __global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
     const int64_t N = cum[p.B - 1];
     zero_masked(p, cum, tid, 256, MODE);
     double wh[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (MODE == kModeLoss) {
+    if (MODE != kModeLogprob) {
         wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
         wh[4] = p.whiten[4];
     }
@@ -815,14 +966,14 @@ __global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
         if (tid == 0) {
             Online tot{sm_m[0], sm_s[0], sm_u[0]};
             for (int w = 1; w < 8; ++w) tot = online_merge(tot, Online{sm_m[w], sm_s[w], sm_u[w]});
-            const int nside = MODE == kModeLoss ? 6 : 2;
+            const int nside = MODE != kModeLogprob ? 6 : 2;
             for (int k = 0; k < nside; ++k) side[k] = load_side(p, MODE, k, gi, b);
             const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
             row_epilogue<MODE>(p, b, t, L, y, tot, sm_tgt, side, wh, wacc[0]);
         }
         __syncthreads();
     }
-    if (MODE == kModeLoss) finish_partials(p, wacc, 1, tid, 256, -1);
+    if (MODE != kModeLogprob) finish_partials(p, wacc, 1, tid, 256, -1);
 }
 
 // ---------------------------------------------------------------- launcher
@@ -875,6 +1026,11 @@ static cudaError_t launch_typed(const K1Params &p, bool tma, int num_sms, cudaSt
 }
 
 cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaStream_t s) {
+    if (mode == kModeLossGrad) {  // fused actor forward + backward: TMA kernel only
+        if (!tma) return cudaErrorInvalidValue;
+        return p.elt == 2 ? launch_tma<uint16_t, kModeLossGrad, 0>(p, num_sms, s)
+                          : launch_tma<float, kModeLossGrad, 0>(p, num_sms, s);
+    }
     if (p.elt == 2)
         return mode == kModeLoss ? launch_typed<uint16_t, kModeLoss>(p, tma, num_sms, s)
                                  : launch_typed<uint16_t, kModeLogprob>(p, tma, num_sms, s);

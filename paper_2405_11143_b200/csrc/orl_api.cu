@@ -403,12 +403,17 @@ extern "C" orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream) {
 }
 
 // ------------------------------------------------------------------ S1 + S7..S9
-extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
-                                   float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
-                                   const float *logp_ref, const float *adv, const float *ret,
-                                   const float *v_new, const float *v_old, float *logp_new,
-                                   float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                                   void *stream) {
+struct GradOut {  // optional fused backward (orl_ppo_loss_and_grad)
+    void *dlogits;
+    int64_t stride_b, stride_t;
+    int zero_masked;
+};
+
+static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor, float inv_temp,
+                                const orl_ppo_cfg *cfg, const float *logp_old, const float *logp_ref,
+                                const float *adv, const float *ret, const float *v_new, const float *v_old,
+                                float *logp_new, float *entropy, float *lse, float *dloss_dlogp,
+                                float *dloss_dv, const GradOut *grad, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
     orl_status st = validate_rows_logits(ctx, rows, actor, inv_temp);
     if (st) return st;
@@ -455,9 +460,59 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
     p.kl_in_loss = cfg->kl_in_loss;
     p.loss_agg = cfg->loss_agg;
     if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
-    CUDA_TRY(ctx, launch_k1(p, tma_eligible(actor), kModeLoss, ctx->num_sms, as_stream(stream)));
+    const bool tma = tma_eligible(actor);
+    if (!grad) {
+        CUDA_TRY(ctx, launch_k1(p, tma, kModeLoss, ctx->num_sms, as_stream(stream)));
+        ctx->launches += 1;
+        return ORL_OK;
+    }
+    // fused actor forward + backward (NEXT-1): one TMA launch when both the logits
+    // and dlogits layouts allow it, else the loss pass followed by the K5 pass.
+    const int64_t elt = p.elt;
+    const bool out_ok = (reinterpret_cast<uintptr_t>(grad->dlogits) % 16 == 0) &&
+                        ((grad->stride_t * elt) % 16 == 0) && ((grad->stride_b * elt) % 16 == 0);
+    if (tma && out_ok) {
+        p.dlogits = grad->dlogits;
+        p.out_stride_b = grad->stride_b;
+        p.out_stride_t = grad->stride_t;
+        p.c2_ent = cfg->c2;
+        p.zero_masked_grad = grad->zero_masked;
+        CUDA_TRY(ctx, launch_k1(p, true, kModeLossGrad, ctx->num_sms, as_stream(stream)));
+        ctx->launches += 1;
+        return ORL_OK;
+    }
+    CUDA_TRY(ctx, launch_k1(p, tma, kModeLoss, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
-    return ORL_OK;
+    return orl_logits_grad(ctx, rows, actor, inv_temp, cfg, lse, entropy, dloss_dlogp, grad->dlogits,
+                           grad->stride_b, grad->stride_t, grad->zero_masked, stream);
+}
+
+extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
+                                   float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
+                                   const float *logp_ref, const float *adv, const float *ret,
+                                   const float *v_new, const float *v_old, float *logp_new,
+                                   float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
+                                   void *stream) {
+    return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
+                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, nullptr, stream);
+}
+
+extern "C" orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
+                                            float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
+                                            const float *logp_ref, const float *adv, const float *ret,
+                                            const float *v_new, const float *v_old, float *logp_new,
+                                            float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
+                                            void *dlogits, int64_t out_stride_b, int64_t out_stride_t,
+                                            int zero_masked, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (!actor || !dlogits || !entropy || !lse || !dloss_dlogp)
+        return fail(ctx, ORL_E_INVALID_ARG, "dlogits, entropy, lse and dloss_dlogp are required");
+    if (out_stride_t < actor->V || out_stride_b < 0)
+        return fail(ctx, ORL_E_SHAPE, "dlogits strides (%lld, %lld) invalid", (long long)out_stride_b,
+                    (long long)out_stride_t);
+    const GradOut g{dlogits, out_stride_b, out_stride_t, zero_masked ? 1 : 0};
+    return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
+                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, &g, stream);
 }
 
 // ------------------------------------------------------------------ NEXT-1

@@ -8,7 +8,7 @@ namespace orl {
 
 // K1 modes: S1 (+ the S2/S3 reward epilogue when `partner` is set) or the
 // actor pass with the S7-S9 loss epilogue.
-enum K1Mode { kModeLogprob = 0, kModeLoss = 1 };
+enum K1Mode { kModeLogprob = 0, kModeLoss = 1, kModeLossGrad = 2 };
 
 // Loss-partial vector (fp64), one per CTA and per context accumulator:
 //  0 n  1 sum obj  2 sum vl  3 sum H  4 sum k(new,ref)  5 n clipped
@@ -47,6 +47,11 @@ struct K1Params {
     double eps_low, eps_high, eps_v, c1, beta_loss, ratio_guard;
     int kl_loss_est, kl_in_loss, loss_agg;
     const double *whiten;  // device [kWhitenSlots]: N_global, mu, sigma, apply, N_seq
+    // kModeLossGrad (NEXT-1 fused): dL/dlogits written in the same launch
+    void *dlogits;
+    int64_t out_stride_b, out_stride_t;
+    double c2_ent;         // entropy coefficient of the total loss
+    int zero_masked_grad;
     const int32_t *cum_global;  // prefix of the micro-batch lengths (large B), else NULL
     // accounting
     double *ws;            // [kNumPartials][ws_stride] per-CTA partials

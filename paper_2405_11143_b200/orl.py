@@ -82,6 +82,9 @@ _lib.orl_advantages.argtypes = [_P, _I64, _I64, _P, _I32, _F64, _F64, _I32, _P, 
 _lib.orl_whiten_stats.argtypes = [_P, _I32, _P]
 _lib.orl_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
                               ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+_lib.orl_ppo_loss_and_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
+                                       ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                       _I64, _I64, _I32, _P]
 _lib.orl_logits_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32, ctypes.POINTER(PpoCfg),
                                  _P, _P, _P, _P, _I64, _I64, _I32, _P]
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
@@ -90,7 +93,7 @@ _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
 _lib.orl_kl_controller_step.argtypes = [ctypes.POINTER(_F64), _F64, _F64, _F64, _F64, ctypes.POINTER(ctypes.c_int)]
 for _f in ("orl_kl_controller_step", "orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
            "orl_advantages", "orl_whiten_stats", "orl_ppo_loss", "orl_finalize",
-           "orl_export_partials", "orl_import_partials", "orl_logits_grad"):
+           "orl_export_partials", "orl_import_partials", "orl_logits_grad", "orl_ppo_loss_and_grad"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 
@@ -241,6 +244,26 @@ def orl_ppo_loss(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old
                            _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
                            _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
                            _ptr(dloss_dv), _stream(stream))
+    return ctx.check(st)
+
+
+def orl_ppo_loss_and_grad(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
+                          entropy, lse, dloss_dlogp, dlogits, seq_offset=0, inv_temp=1.0, logp_ref=None,
+                          ret=None, v_new=None, v_old=None, dloss_dv=None, zero_masked=True, stream=None,
+                          cu_seqlens=None, n_seq=None):
+    """S1 + S7..S9 + NEXT-1 in one pass over the actor logits (the row is re-read from L2)."""
+    T = tokens.shape[1]
+    B = n_seq if cu_seqlens is not None else logits.shape[0]
+    if dlogits.dtype != logits.dtype or dlogits.shape[-1] != logits.shape[-1] or dlogits.stride(-1) != 1:
+        raise ValueError("dlogits must be a view with the logits dtype, V and unit V stride")
+    rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
+    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
+    sb = 0 if cu_seqlens is not None else dlogits.stride(0)
+    st = _lib.orl_ppo_loss_and_grad(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
+                                    _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
+                                    _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
+                                    _ptr(dloss_dv), _ptr(dlogits), sb, dlogits.stride(-2), int(bool(zero_masked)),
+                                    _stream(stream))
     return ctx.check(st)
 
 

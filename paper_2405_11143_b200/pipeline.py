@@ -70,7 +70,7 @@ def microbatches(B: int, mb: int):
 def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers, logits: LogitsSource,
                   mb: int, stream: Optional[torch.cuda.Stream] = None, finalize: bool = True,
                   on_k1: Optional[Callable[[str], object]] = None,
-                  grad_sink: Optional[Callable[[int, int], torch.Tensor]] = None):
+                  grad_sink: Optional[Callable[[int, int], torch.Tensor]] = None, fused_grad: bool = True):
     """One iteration on this rank.  `batch` holds device tensors tokens [B,T] int32,
     lengths [B] int32, seq_reward [B] f32 and (critic) values_old / values_new [B,T].
     `on_k1(tag)` (optional) is called around every K1 launch for timing hooks.
@@ -105,6 +105,20 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
                         stream=stream)
     _orl.orl_whiten_stats(ctx, cfg.whiten and cfg.adv_kind != "grpo", stream)         # S6 + C1
     critic = cfg.critic and batch.get("values_new") is not None
+    if grad_sink is not None and fused_grad:           # S1 + S7..S9 + NEXT-1 in one pass
+        for s, e in mbs:
+            h = hook("new+grad")
+            _orl.orl_ppo_loss_and_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.logp_old, bufs.adv,
+                                       bufs.logp_new, seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
+                                       ret=bufs.ret if critic else None,
+                                       v_new=batch["values_new"] if critic else None,
+                                       v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
+                                       lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
+                                       dlogits=grad_sink(s, e), stream=stream)
+            if h: h()
+        if not finalize:
+            return None
+        return _orl.orl_finalize(ctx, cfg.ppo, dev_out=bufs.stats_dev, stream=stream)
     for s, e in mbs:                                   # S1 + S7..S9, actor
         h = hook("new")
         _orl.orl_ppo_loss(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.logp_old, bufs.adv, bufs.logp_new,

@@ -598,3 +598,25 @@ def test_next2_seq_mean_aggregation(ctx, kind):
         a_max = 0.02 / (n_seq * max(1, int(npb["lengths"][npb["lengths"] > 0].min())))
         _check_grad(dl.float().cpu().numpy(), o, m, 2e-5 if dtype == "f32" else 8e-3, f"seqmean-{dtype}",
                     _np(bufs.dlogp), H, a_max, 1.0)
+
+
+@pytest.mark.parametrize("agg", ["token_mean", "seq_mean_token_mean"])
+def test_next1_fused_forward_backward_matches_two_passes(ctx, agg):
+    """orl_ppo_loss_and_grad (one pass, the row re-read from L2) gives the same bits as
+    orl_ppo_loss followed by orl_logits_grad (K5)."""
+    B, T, V = 6, 96, 8192
+    g = _gpu_batch(29, B, T, V, "mixed", mode="stress")
+    cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V, c2=0.01, loss_agg=agg))
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    out = {}
+    for fused in (True, False):
+        dl = torch.full((B, T, V), 7.0, dtype=torch.bfloat16, device=DEV)
+        bufs = Buffers(B, T, DEV)
+        status, st = run_iteration(ctx, g, cfg, bufs, src, mb=4, grad_sink=lambda s, e: dl[s:e], fused_grad=fused)
+        torch.cuda.synchronize()
+        assert status == "ORL_OK"
+        out[fused] = (st, dl, bufs)
+    assert out[True][0] == out[False][0]
+    assert torch.equal(out[True][1], out[False][1])
+    for k in ("logp_new", "entropy", "lse", "dlogp", "dv"):
+        assert torch.equal(getattr(out[True][2], k), getattr(out[False][2], k)), k

@@ -74,6 +74,9 @@ def run(name, kind, i):
         return y.copy_(xv)
     if kind == "grad":           # NEXT-1 backward: read logits + write dlogits
         return orl.orl_logits_grad(ctx, tok, L, xv, cfg, lse, ent, dl, dlog, seq_offset=s)
+    if kind == "lossgrad":       # fused actor forward + backward: read once (+ L2 re-read), write dlogits
+        return orl.orl_ppo_loss_and_grad(ctx, tok, L, xv, cfg, lo, adv, lpn, seq_offset=s, entropy=ent, lse=lse,
+                                         dloss_dlogp=dl, dlogits=dlog)
     if kind == "logp":
         orl.orl_logprobs(ctx, tok, L, xv, lp, seq_offset=s)
     elif kind == "logp+H":
@@ -112,7 +115,7 @@ clk = [float(l.split(",")[0]) for l in out.strip().splitlines() if l.strip()]
 pw = [float(l.split(",")[1]) for l in out.strip().splitlines() if l.strip()]
 for (name, kind), v in res.items():
     ms = statistics.median(v)
-    gb = a.mb * T * V * 2 / 1e9 * (2 if kind in ("copy", "grad") else 1)
+    gb = a.mb * T * V * 2 / 1e9 * (2 if kind in ("copy", "grad", "lossgrad") else 1)
     print(f"{name:28s} {kind:7s} V={V}: {ms * 1e3:8.1f} us/launch  {gb / ms * 1e3:8.1f} GB/s  "
           f"(min {min(v) * 1e3:.1f} max {max(v) * 1e3:.1f})")
 if clk:

@@ -371,26 +371,47 @@ def run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok):
             orl.orl_logits_grad(ctx, tok, L, logits["new"][s:e], cfg.ppo, bufs.lse, bufs.entropy, bufs.dlogp,
                                 dl[s:e], seq_offset=s, inv_temp=cfg.inv_temp, stream=stream)
 
-    for _ in range(2):
-        once()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def fused():
+        critic = cfg.critic
+        for s in range(0, B, mb):
+            e = min(B, s + mb)
+            orl.orl_ppo_loss_and_grad(ctx, tok, L, logits["new"][s:e], cfg.ppo, bufs.logp_old, bufs.adv,
+                                      bufs.logp_new, seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
+                                      ret=bufs.ret if critic else None,
+                                      v_new=batch["values_new"] if critic else None,
+                                      v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
+                                      lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
+                                      dlogits=dl[s:e], stream=stream)
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
     reps = max(3, args.steps // 4)
-    a.record(stream)
-    for _ in range(reps):
-        once()
-    b.record(stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
+    ms = timed(once)
     byts = n_tok * V * 2 * 2
     peak, _ = _peaks()
+    # fused actor pass (loss epilogue + backward, the row re-read from L2); its
+    # bytes are those of the two-pass path minus the HBM re-read it avoids
+    ms_f = timed(fused)
     del dl
     torch.cuda.empty_cache()
     return {"tokens_per_s": round(n_tok / (ms / 1e3), 1), "ms_per_pass": round(ms, 4),
             "roofline": {"bound": "hbm", "achieved": round(byts / (ms / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(byts / (ms / 1e3) / 1e9 / peak, 4),
                          "bytes": "V*2 read + V*2 written per valid token"},
-            "kernel": "k5_tma_kernel", "launches": len(range(0, B, mb)), "reps": reps}
+            "kernel": "k5_tma_kernel", "launches": len(range(0, B, mb)), "reps": reps,
+            "fused_actor_pass": {"api": "orl_ppo_loss_and_grad", "tokens_per_s": round(n_tok / (ms_f / 1e3), 1),
+                                 "ms": round(ms_f, 4),
+                                 "algorithmic_GBps": round(byts / (ms_f / 1e3) / 1e9, 1)}}
 
 
 def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank):

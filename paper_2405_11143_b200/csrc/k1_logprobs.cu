@@ -623,7 +623,18 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         // B(i) (an L2 hit, evict_first): F0, F1, B0, F2, B1, ..., B(n-1).
         if (lane == 0) {
             const uint64_t pol_first = l2_evict_first_policy();
-            const uint64_t pol_fwd = MODE == kModeLossGrad ? l2_evict_last_policy() : pol_first;
+#ifndef ORL_K1_FUSED_FWD_POL
+#define ORL_K1_FUSED_FWD_POL 1
+#endif
+#ifndef ORL_K1_FUSED_BWD_POL
+#define ORL_K1_FUSED_BWD_POL 0
+#endif
+            const uint64_t pol_fwd = MODE != kModeLossGrad ? pol_first
+                                     : ORL_K1_FUSED_FWD_POL == 1 ? l2_evict_last_policy()
+                                     : ORL_K1_FUSED_FWD_POL == 2 ? l2_evict_normal_policy() : pol_first;
+            const uint64_t pol_bwd = ORL_K1_FUSED_BWD_POL == 0 ? pol_first
+                                     : ORL_K1_FUSED_BWD_POL == 2 ? l2_evict_normal_policy()
+                                     : l2_evict_unchanged_policy();
             int stage = 0;
             uint32_t phase = 0;
             const int64_t n_rows = N > (int64_t)blockIdx.x ? (N - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -658,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
                         mbar_wait(&S.empty[stage], phase ^ 1u);
                         mbar_arrive_expect_tx(&S.full[stage], bytes);
-                        tma_load_1d(S.stage[stage], prev_src + off, bytes, &S.full[stage], pol_first);
+                        tma_load_1d(S.stage[stage], prev_src + off, bytes, &S.full[stage], pol_bwd);
                         if (++stage == kStages) { stage = 0; phase ^= 1u; }
                     }
                 }

@@ -90,6 +90,14 @@ struct GradRow {
     int32_t pad;
 };
 constexpr int kGradRows = 4;  // ring; each slot always written by the same epilogue warp
+// Fused actor pass: the backward of row i starts after the first kFusedSplit
+// chunks of row i+1's forward (0 = right after row i: the re-read is an L2 hit
+// but the consumers wait for row i's epilogue; the full row = a one-row lag,
+// which re-reads from HBM because ~76 MB of traffic separates the two touches).
+#ifndef ORL_K1_FUSED_SPLIT
+#define ORL_K1_FUSED_SPLIT 3
+#endif
+constexpr int kFusedSplit = ORL_K1_FUSED_SPLIT;
 
 struct __align__(128) K1Smem {
     uint8_t stage[kStages][kChunk];
@@ -626,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 #ifndef ORL_K1_FUSED_FWD_POL
 #define ORL_K1_FUSED_FWD_POL 1
 #endif
+
 #ifndef ORL_K1_FUSED_BWD_POL
 #define ORL_K1_FUSED_BWD_POL 0
 #endif
@@ -638,40 +647,42 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             int stage = 0;
             uint32_t phase = 0;
             const int64_t n_rows = N > (int64_t)blockIdx.x ? (N - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+            const int64_t nch = (row_bytes + kChunk - 1) / kChunk;
+            const int64_t ksplit = MODE == kModeLossGrad ? min((int64_t)kFusedSplit, nch) : nch;
             int b = 0, t = 0, y = 0;
             if (n_rows > 0) {
                 locate_row(cum, p.B, blockIdx.x, b, t);
                 y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
             }
+            auto issue = [&](const char *src, int64_t c0, int64_t c1, uint64_t pol, int64_t publish_rl) {
+                for (int64_t c = c0; c < c1; ++c) {
+                    const int64_t off = c * kChunk;
+                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
+                    mbar_wait(&S.empty[stage], phase ^ 1u);
+                    if (c == 0 && publish_rl >= 0) S.row_y[publish_rl % kRowInfo] = y;  // released by the arrive
+                    mbar_arrive_expect_tx(&S.full[stage], bytes);
+                    tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+            };
             const char *prev_src = nullptr;
+            // kModeLossGrad schedule per CTA: F(i)[0, k), B(i-1), F(i)[k, nch), ... , B(n-1)
             for (int64_t rl = 0; rl <= n_rows; ++rl) {
                 const char *src = nullptr;
+                int bn = 0, tn = 0, yn = 0;
                 if (rl < n_rows) {
                     const int64_t jn = blockIdx.x + (rl + 1) * (int64_t)gridDim.x;  // prefetch next row's token
-                    int bn = 0, tn = 0, yn = 0;
                     if (jn < N) {
                         locate_row(cum, p.B, jn, bn, tn);
                         yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
                     }
                     src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
-                    for (int64_t off = 0; off < row_bytes; off += kChunk) {
-                        const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
-                        mbar_wait(&S.empty[stage], phase ^ 1u);
-                        if (off == 0) S.row_y[rl % kRowInfo] = y;  // published by the arrive below
-                        mbar_arrive_expect_tx(&S.full[stage], bytes);
-                        tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol_fwd);
-                        if (++stage == kStages) { stage = 0; phase ^= 1u; }
-                    }
-                    b = bn; t = tn; y = yn;
+                    issue(src, 0, ksplit, pol_fwd, rl);
                 }
-                if (MODE == kModeLossGrad && rl > 0) {
-                    for (int64_t off = 0; off < row_bytes; off += kChunk) {
-                        const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
-                        mbar_wait(&S.empty[stage], phase ^ 1u);
-                        mbar_arrive_expect_tx(&S.full[stage], bytes);
-                        tma_load_1d(S.stage[stage], prev_src + off, bytes, &S.full[stage], pol_bwd);
-                        if (++stage == kStages) { stage = 0; phase ^= 1u; }
-                    }
+                if (MODE == kModeLossGrad && rl > 0) issue(prev_src, 0, nch, pol_bwd, -1);
+                if (rl < n_rows) {
+                    issue(src, ksplit, nch, pol_fwd, -1);
+                    b = bn; t = tn; y = yn;
                 }
                 prev_src = src;
             }
@@ -758,20 +769,23 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     int stage = 0;
     uint32_t phase = 0;
     const int64_t n_rows = N > (int64_t)blockIdx.x ? (N - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    for (int64_t rl = 0; rl <= n_rows; ++rl) {
-        if (rl < n_rows) {
-        // ---------------- forward pass over row rl ----------------
-        ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
-        float tgt = 0.f;
-        bool have_tgt = false;
-        int64_t tchunk = -1;
-        int tin = 0;
-        bool towner = false;
-        int64_t ci = 0;
-        for (int64_t off = 0; off < row_bytes; off += kChunk, ++ci) {
+    const int64_t nch = (row_bytes + kChunk - 1) / kChunk;
+    const int64_t ksplit = MODE == kModeLossGrad ? min((int64_t)kFusedSplit, nch) : nch;
+    // forward state of the row in progress (survives an interleaved backward row)
+    ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
+    float tgt = 0.f;
+    bool have_tgt = false;
+    int64_t tchunk = -1;
+    int tin = 0;
+    bool towner = false;
+    auto fwd_chunks = [&](int64_t rl, int64_t c0, int64_t c1) {
+        for (int64_t ci = c0; ci < c1; ++ci) {
+            const int64_t off = ci * kChunk;
             const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
             mbar_wait(&S.full[stage], phase);
-            if (off == 0) {  // which chunk / thread holds the target logit
+            if (ci == 0) {  // row start: which chunk / thread holds the target logit
+                acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
+                have_tgt = false;
                 const int y = S.row_y[rl % kRowInfo];
                 const bool y_ok = (y >= 0) && ((int64_t)y < p.V);
                 const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin);
@@ -786,7 +800,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                           : *reinterpret_cast<const float *>(sb + tin);
                 have_tgt = true;
             }
-            // copy this thread's 64 B to registers and hand the stage back to the
+            // copy this thread's bytes to registers and hand the stage back to the
             // producer before computing, so the ring keeps ~all stages in flight
             uint32_t w[kW];
             if (bytes == kChunk) load_words<Tin, true>(w, sb, ct, kChunk >> 4);
@@ -794,11 +808,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
-            const bool first = off == 0;
-            if (ent) process_words<Tin, true, POLY>(acc, w, first, p.c2, c2p);
-            else process_words<Tin, false, POLY>(acc, w, first, p.c2, c2p);
+            if (ent) process_words<Tin, true, POLY>(acc, w, ci == 0, p.c2, c2p);
+            else process_words<Tin, false, POLY>(acc, w, ci == 0, p.c2, c2p);
         }
-        // ---- row end: publish this thread's state to the row slot ----
+    };
+    auto fwd_publish = [&](int64_t rl) {  // row end: this thread's state into the row slot
         float s0, s1, s2, s3;
         unpack2(fadd2(acc.sA, acc.sB), s0, s1);
         unpack2(fadd2(acc.uA, acc.uB), s2, s3);
@@ -811,84 +825,96 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         if (have_tgt) R.target = tgt;
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.row_full[slot]);
-        }
-        if (MODE == kModeLossGrad && rl > 0) {
-            // ---------------- backward pass over row rl-1 (NEXT-1, from L2) ----------------
-            // dL/dx_v = p_v (A1 t_v + A0) + [v = y] wt,  t_v = (x_v c - lse log2e)
-            const int64_t rb = rl - 1;
-            mbar_wait(&S.grad_full[rb % kGradRows], (uint32_t)(rb / kGradRows) & 1u);
-            const GradRow g = S.grad[rb % kGradRows];
-            Tin *orow = reinterpret_cast<Tin *>(p.dlogits) + g.out_off;
-            const uint64_t nl2 = pack2(-g.l2, -g.l2), A1p = pack2(g.A1, g.A1), A0p = pack2(g.A0, g.A0);
-            const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin);
-            for (int64_t off = 0; off < row_bytes; off += kChunk) {
-                const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
-                const int nvec = bytes >> 4;
-                mbar_wait(&S.full[stage], phase);
-                const uint8_t *sb = S.stage[stage];
-                const bool own_y = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= off && ybyte < off + bytes &&
-                                   (((int)(ybyte - off) >> 4) % kConsumers) == ct;
-                float xy = 0.f;
-                if (own_y) {
-                    const uint8_t *q = sb + (ybyte - off);
-                    xy = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(q)) << 16)
-                                          : *reinterpret_cast<const float *>(q);
-                }
-                uint4 v[kVecPerThread];
+    };
+    auto bwd_row = [&](int64_t rb) {
+        // backward pass over row rb (NEXT-1, re-read from L2):
+        // dL/dx_v = p_v (A1 t_v + A0) + [v = y] wt,  t_v = x_v c - lse log2 e
+        mbar_wait(&S.grad_full[rb % kGradRows], (uint32_t)(rb / kGradRows) & 1u);
+        const GradRow g = S.grad[rb % kGradRows];
+        Tin *orow = reinterpret_cast<Tin *>(p.dlogits) + g.out_off;
+        const uint64_t nl2 = pack2(-g.l2, -g.l2), A1p = pack2(g.A1, g.A1), A0p = pack2(g.A0, g.A0);
+        const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin);
+        const uint64_t st_pol = l2_evict_first_policy();
+        for (int64_t off = 0; off < row_bytes; off += kChunk) {
+            const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
+            const int nvec = bytes >> 4;
+            mbar_wait(&S.full[stage], phase);
+            const uint8_t *sb = S.stage[stage];
+            const bool own_y = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= off && ybyte < off + bytes &&
+                               (((int)(ybyte - off) >> 4) % kConsumers) == ct;
+            float xy = 0.f;
+            if (own_y) {
+                const uint8_t *q = sb + (ybyte - off);
+                xy = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(q)) << 16)
+                                      : *reinterpret_cast<const float *>(q);
+            }
+            uint4 v[kVecPerThread];
 #pragma unroll
-                for (int k = 0; k < kVecPerThread; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    if (vi < nvec) v[k] = lds128(sb + vi * 16);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.empty[stage]);
-                if (++stage == kStages) { stage = 0; phase ^= 1u; }
-                char *obase = reinterpret_cast<char *>(orow) + off;
+            for (int k = 0; k < kVecPerThread; ++k) {
+                const int vi = ct + k * kConsumers;
+                if (vi < nvec) v[k] = lds128(sb + vi * 16);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1u; }
+            char *obase = reinterpret_cast<char *>(orow) + off;
 #pragma unroll
-                for (int k = 0; k < kVecPerThread; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    if (vi >= nvec) continue;
-                    const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                    uint32_t o[4];
-                    if (sizeof(Tin) == 2) {
+            for (int k = 0; k < kVecPerThread; ++k) {
+                const int vi = ct + k * kConsumers;
+                if (vi >= nvec) continue;
+                const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                uint32_t o[4];
+                if (sizeof(Tin) == 2) {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[q]), c2p, nl2);
-                            float t0, t1;
-                            unpack2(t2, t0, t1);
-                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
-                            float g0, g1;
-                            unpack2(gr, g0, g1);
-                            o[q] = f32x2_to_bf16x2_rn(g0, g1);
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 2; ++q) {
-                            uint64_t x;
-                            asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(w4[2 * q]), "r"(w4[2 * q + 1]));
-                            const uint64_t t2 = ffma2(x, c2p, nl2);
-                            float t0, t1;
-                            unpack2(t2, t0, t1);
-                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
-                            float g0, g1;
-                            unpack2(gr, g0, g1);
-                            o[2 * q] = __float_as_uint(g0);
-                            o[2 * q + 1] = __float_as_uint(g1);
-                        }
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[q]), c2p, nl2);
+                        float t0, t1;
+                        unpack2(t2, t0, t1);
+                        const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
+                        float g0, g1;
+                        unpack2(gr, g0, g1);
+                        o[q] = f32x2_to_bf16x2_rn(g0, g1);
                     }
-                    stg128_cs(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
-                }
-                if (own_y) {  // program-ordered rewrite of the target element with the delta term
-                    const float t2 = fmaf(xy, p.c2, -g.l2);
-                    const float gy = ex2(t2) * fmaf(g.A1, t2, g.A0) + g.wt;
-                    if (sizeof(Tin) == 2) {
-                        const uint32_t hb = f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu;
-                        asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + g.y), "h"((unsigned short)hb) : "memory");
-                    } else {
-                        reinterpret_cast<float *>(orow)[g.y] = gy;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        uint64_t x;
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(w4[2 * q]), "r"(w4[2 * q + 1]));
+                        const uint64_t t2 = ffma2(x, c2p, nl2);
+                        float t0, t1;
+                        unpack2(t2, t0, t1);
+                        const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
+                        float g0, g1;
+                        unpack2(gr, g0, g1);
+                        o[2 * q] = __float_as_uint(g0);
+                        o[2 * q + 1] = __float_as_uint(g1);
                     }
+                }
+#ifdef ORL_K1_FUSED_STORE_CS
+                stg128_cs(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+#else
+                stg128_hint(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]), st_pol);
+#endif
+            }
+            if (own_y) {  // program-ordered rewrite of the target element with the delta term
+                const float t2 = fmaf(xy, p.c2, -g.l2);
+                const float gy = ex2(t2) * fmaf(g.A1, t2, g.A0) + g.wt;
+                if (sizeof(Tin) == 2) {
+                    const uint32_t hb = f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu;
+                    asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + g.y), "h"((unsigned short)hb) : "memory");
+                } else {
+                    reinterpret_cast<float *>(orow)[g.y] = gy;
                 }
             }
+        }
+    };
+    // schedule (mirrors the producer): F(i)[0, k), B(i-1), F(i)[k, nch), publish F(i)
+    for (int64_t rl = 0; rl <= n_rows; ++rl) {
+        if (rl < n_rows) fwd_chunks(rl, 0, ksplit);
+        if (MODE == kModeLossGrad && rl > 0) bwd_row(rl - 1);
+        if (rl < n_rows) {
+            fwd_chunks(rl, ksplit, nch);
+            fwd_publish(rl);
         }
     }
     if (MODE == kModeLossGrad && p.zero_masked_grad && !p.cu_seqlens) {

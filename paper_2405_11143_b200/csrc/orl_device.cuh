@@ -187,6 +187,13 @@ __device__ __forceinline__ void stg128_cs(void *p, uint4 v) {
                  "r"(v.w)
                  : "memory");
 }
+// Streaming store with an explicit L2 eviction policy (e.g. evict_first, so the
+// dlogits of the fused actor pass do not push the rows it re-reads out of L2).
+__device__ __forceinline__ void stg128_hint(void *p, uint4 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ uint32_t f32x2_to_bf16x2_rn(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

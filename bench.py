@@ -178,7 +178,10 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun (even with one rank) use the distributed plumbing: NCCL process
+    # group, unique-id broadcast, liborl NCCL communicator, barriers, max over ranks
+    dist_mode = "WORLD_SIZE" in os.environ
+    if dist_mode:
         dist.init_process_group("nccl", device_id=dev)
         uid = [orl.orl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -258,7 +261,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         status, st = step(False)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_mode:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -271,13 +274,13 @@ def run_ours(args):
         status, st = step(True)
     t1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_mode:
         dist.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
     launches = (ctx.launch_count - l0) // args.steps
     ms = t0.elapsed_time(t1) / args.steps
-    if world > 1:
+    if dist_mode:
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
@@ -347,7 +350,7 @@ def run_ours(args):
                 "per_gpu_tokens_per_s": round(value / world, 1)}
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if dist_mode:
         dist.destroy_process_group()
 
 
@@ -476,7 +479,7 @@ def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens
     steps = max(2, args.steps // 5)
     one_step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -484,7 +487,7 @@ def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens
         one_step()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    if world > 1:
+    if dist.is_initialized():
         tt = torch.tensor([dt], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())

@@ -81,6 +81,8 @@ def _load():
         lib.oracle_kl_controller_step.argtypes = [P, f64, f64, f64, f64]
         lib.oracle_kl_controller_step.restype = i32
         lib.oracle_stats.argtypes = [P, f64, f64, f64, i32, i32, f64, P]
+        lib.oracle_lmhead_rows.argtypes = [P, i64, P, i64, i64, i64, i64, P, f64, P, P, P, P]
+        lib.oracle_lmhead_rows.restype = i64
         lib.oracle_stats.restype = i32
         _lib = lib
         return lib
@@ -285,6 +287,57 @@ def logits_grad_row(x, y, inv_temp, w, a):
     g = np.zeros(x.size)
     lib.oracle_logits_grad_row(_p(x), x.size, int(y), float(inv_temp), float(w), float(a), _p(g))
     return g
+
+
+def lmhead_rows(h_bits, W_bits, y, inv_temp=1.0):
+    """NEXT-4: S1 of the LM-head logits z = h W^T (fp64) per row.
+
+    h_bits [R, d] and W_bits [V, d] are bf16 bit patterns (uint16); y [R]
+    (int32; y < 0 = row not computed).  Returns dict logp, entropy, lse, z_y
+    ([R] fp64) and n_nonfinite."""
+    lib = _load()
+    h = np.ascontiguousarray(h_bits, dtype=np.uint16)
+    W = np.ascontiguousarray(W_bits, dtype=np.uint16)
+    y = _i32(y)
+    R, d = h.shape
+    V = W.shape[0]
+    assert W.shape[1] == d and y.shape == (R,)
+    out = {k: np.zeros(R) for k in ("logp", "entropy", "lse", "z_y")}
+    bad = lib.oracle_lmhead_rows(_p(h), d, _p(W), d, R, d, V, _p(y), float(inv_temp), _p(out["logp"]),
+                                 _p(out["entropy"]), _p(out["lse"]), _p(out["z_y"]))
+    out["n_nonfinite"] = int(bad)
+    return out
+
+
+def lmhead_row_index(B, T, lengths, cu_seqlens=None, seq_offset=0):
+    """Hidden-row index of every valid (b,t) of a call (orl.h orl_lmhead):
+    packed cu_seqlens[so+b] - cu_seqlens[so] + t, else b*T + t.  Returns
+    (b, t, r) arrays in (b,t) order."""
+    bs, ts, rs = [], [], []
+    for b in range(B):
+        for t in range(int(lengths[seq_offset + b])):
+            r = (int(cu_seqlens[seq_offset + b]) - int(cu_seqlens[seq_offset]) + t) if cu_seqlens is not None \
+                else b * T + t
+            bs.append(b), ts.append(t), rs.append(r)
+    return np.array(bs, dtype=np.int64), np.array(ts, dtype=np.int64), np.array(rs, dtype=np.int64)
+
+
+def lmhead_logprobs(h_bits, W_bits, tokens, lengths, inv_temp=1.0, cu_seqlens=None):
+    """NEXT-4 over a batch: [B,T] logp, entropy, lse (zeros at masked positions)
+    from the hidden rows h_bits [R, d] (row index as in lmhead_row_index)."""
+    B, T = tokens.shape
+    bs, ts, rs = lmhead_row_index(B, T, lengths, cu_seqlens)
+    R = h_bits.shape[0]
+    y = np.full(R, -1, dtype=np.int32)
+    y[rs] = tokens[bs, ts]
+    o = lmhead_rows(h_bits, W_bits, y, inv_temp)
+    res = {}
+    for k in ("logp", "entropy", "lse", "z_y"):
+        a = np.zeros((B, T))
+        a[bs, ts] = o[k][rs]
+        res[k] = a
+    res["n_nonfinite"] = o["n_nonfinite"]
+    return res
 
 
 def logits_grad(logits, tokens, lengths, dlogp, inv_temp, c2, n_global, seq_mean=False, n_seq=0.0):

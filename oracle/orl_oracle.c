@@ -509,3 +509,43 @@ int oracle_kl_controller_step(double *beta, double target, double horizon, doubl
     *beta = *beta * (1.0 + e / horizon);
     return observed > max_kl;
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT-4  LM head + S1 ("the actor model ...
+ * forward", P:191/P:193 log-probabilities):
+ *     z_{r,v} = sum_k h_{r,k} W_{v,k}          (the LM-head logits, fp64)
+ *     then S1 of row r on x = inv_temp * z_r, target y_r (oracle_row_logsoftmax).
+ * h is [R, d] with row pitch ld_h, W is [V, d] with row pitch ld_w, both bf16
+ * bit patterns (exact in fp64).  y_r < 0 marks a row that is not computed
+ * (outputs 0); y_r >= V gives NaN outputs (token range).  gathered_z = z_{r,y}.
+ * Returns the number of non-finite rows.
+ * ---------------------------------------------------------------------- */
+int64_t oracle_lmhead_rows(const uint16_t *h, int64_t ld_h, const uint16_t *W, int64_t ld_w,
+                           int64_t R, int64_t d, int64_t V, const int32_t *y, double inv_temp,
+                           double *logp, double *entropy, double *lse, double *gathered_z)
+{
+    int64_t bad = 0;
+    double *z = (double *)malloc((size_t)(V > 0 ? V : 1) * sizeof(double));
+    double *x = (double *)malloc((size_t)(V > 0 ? V : 1) * sizeof(double));
+    for (int64_t r = 0; r < R; ++r) {
+        logp[r] = entropy[r] = lse[r] = gathered_z[r] = 0.0;
+        if (y[r] < 0)
+            continue;
+        if (y[r] >= V) {
+            logp[r] = entropy[r] = lse[r] = gathered_z[r] = NAN;
+            continue;
+        }
+        for (int64_t v = 0; v < V; ++v) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < d; ++k)
+                acc += bf16_bits_to_double(h[r * ld_h + k]) * bf16_bits_to_double(W[v * ld_w + k]);
+            z[v] = acc;
+            x[v] = inv_temp * acc;
+        }
+        bad += oracle_row_logsoftmax(x, V, y[r], &lse[r], &logp[r], &entropy[r]);
+        gathered_z[r] = z[y[r]];
+    }
+    free(z);
+    free(x);
+    return bad;
+}

@@ -601,3 +601,85 @@ def test_next2_seq_mean_logits_grad_finite_differences():
                 xp[b, t, v] += h
                 xm[b, t, v] -= h
                 assert abs((total(xp)[0] - total(xm)[0]) / (2 * h) - g[b, t, v]) < 2e-8
+
+
+# ----------------------------------------------------------------------------- NEXT-4
+def _bf16_bits(a):
+    """Round fp32 values to bf16 bit patterns (RNE) with torch (a library routine)."""
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16)
+    return t.view(torch.int16).numpy().view(np.uint16)
+
+
+def _bf16_val(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def test_next4_lmhead_vs_library_bruteforce():
+    """z = h W^T then log-softmax / logsumexp / entropy, all via numpy + scipy."""
+    from scipy.special import log_softmax, logsumexp
+    R, d, V = 9, 48, 37
+    h = _bf16_bits(rng.normal(0, 1, (R, d)))
+    W = _bf16_bits(rng.normal(0, 0.3, (V, d)))
+    y = rng.integers(0, V, R).astype(np.int32)
+    for inv_temp in (1.0, 1.0 / 0.7):
+        o = oracle.lmhead_rows(h, W, y, inv_temp)
+        z = _bf16_val(h) @ _bf16_val(W).T
+        ls = log_softmax(inv_temp * z, axis=1)
+        np.testing.assert_allclose(o["lse"], logsumexp(inv_temp * z, axis=1), rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(o["logp"], ls[np.arange(R), y], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(o["entropy"], -(np.exp(ls) * ls).sum(1), rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(o["z_y"], z[np.arange(R), y], rtol=1e-14, atol=1e-14)
+
+
+def test_next4_zero_head_is_uniform():
+    """W = 0: every logit is 0 -> lse = ln V, H = ln V, logp = -ln V (closed form)."""
+    R, d, V = 5, 16, 50
+    h = _bf16_bits(rng.normal(0, 1, (R, d)))
+    W = np.zeros((V, d), np.uint16)
+    o = oracle.lmhead_rows(h, W, np.arange(R, dtype=np.int32), 1.3)
+    np.testing.assert_allclose(o["lse"], math.log(V), rtol=1e-15)
+    np.testing.assert_allclose(o["entropy"], math.log(V), rtol=1e-14)
+    np.testing.assert_allclose(o["logp"], -math.log(V), rtol=1e-15)
+
+
+def test_next4_common_row_shift_invariance():
+    """W_v -> W_v + w0 for every v adds h.w0 to every logit of the row: logp and
+    H are unchanged, lse moves by inv_temp h.w0.  Small-integer bf16 values keep
+    every sum exact."""
+    R, d, V = 6, 12, 21
+    h = _bf16_bits(rng.integers(-3, 4, (R, d)).astype(np.float32))
+    W0 = rng.integers(-2, 3, (V, d)).astype(np.float32)
+    w0 = rng.integers(-2, 3, d).astype(np.float32)
+    y = rng.integers(0, V, R).astype(np.int32)
+    a = oracle.lmhead_rows(h, _bf16_bits(W0), y, 0.5)
+    b = oracle.lmhead_rows(h, _bf16_bits(W0 + w0), y, 0.5)
+    shift = 0.5 * (_bf16_val(h) @ w0.astype(np.float64))
+    np.testing.assert_allclose(b["logp"], a["logp"], atol=1e-12)
+    np.testing.assert_allclose(b["entropy"], a["entropy"], atol=1e-12)
+    np.testing.assert_allclose(b["lse"] - a["lse"], shift, atol=1e-12)
+
+
+def test_next4_identity_head_reduces_to_s1():
+    """W = c I (V = d): z_{r,v} = c h_{r,v}, so NEXT-4 equals S1 on those logits
+    and gathered z_y = c h_{r,y}; masked rows (y < 0) are zeros, y >= V is NaN."""
+    R, d = 7, 32
+    c = 2.0
+    hv = rng.normal(0, 2, (R, d)).astype(np.float32)
+    h = _bf16_bits(hv)
+    W = _bf16_bits(c * np.eye(d, dtype=np.float32))
+    y = rng.integers(0, d, R).astype(np.int32)
+    y[2] = -1
+    y[5] = d
+    o = oracle.lmhead_rows(h, W, y, 1.0)
+    logits = (c * _bf16_val(h)).astype(np.float32).reshape(1, R, d)
+    toks = np.where(y < 0, 0, np.minimum(y, d - 1)).reshape(1, R)
+    s1 = oracle.logprobs(logits, toks, np.array([R], np.int32), 1.0)
+    for r in range(R):
+        if r == 2:
+            assert o["logp"][r] == 0.0 and o["entropy"][r] == 0.0 and o["lse"][r] == 0.0
+        elif r == 5:
+            assert np.isnan(o["logp"][r]) and np.isnan(o["lse"][r])
+        else:
+            assert abs(o["logp"][r] - s1["logp"][0, r]) < 1e-12
+            assert abs(o["entropy"][r] - s1["entropy"][0, r]) < 1e-12
+            assert abs(o["z_y"][r] - c * _bf16_val(h)[r, y[r]]) == 0.0

@@ -43,8 +43,9 @@ def main():
              "(tools/k1_bench.py: 8 sequences x 1024 tokens x V=128256 bf16 = 2.10 GB of logits per launch,",
              "the bench's launch shape; profiles/run_ncu_k1.sh).", ""]
     traffic = {}
-    for kind in ("logp", "logp+H", "loss"):
-        rep = os.path.join(d, f"k1_{kind}.ncu-rep")
+    fwd = ("logp", "logp+H", "loss")
+    for kind in fwd + ("lossgrad", "grad"):
+        rep = os.path.join(d, f"k5_{kind}.ncu-rep" if kind == "grad" else f"k1_{kind}.ncu-rep")
         if not os.path.exists(rep):
             continue
         r = raw(rep)[0]
@@ -57,7 +58,7 @@ def main():
         rd = float(r["dram__bytes_read.sum"][0]) * (1e9 if r["dram__bytes_read.sum"][1] == "Gbyte" else 1e6 if r["dram__bytes_read.sum"][1] == "Mbyte" else 1)
         wr = float(r["dram__bytes_write.sum"][0]) * (1e9 if r["dram__bytes_write.sum"][1] == "Gbyte" else 1e6 if r["dram__bytes_write.sum"][1] == "Mbyte" else 1e3 if r["dram__bytes_write.sum"][1] == "Kbyte" else 1)
         t = float(r["gpu__time_duration.sum"][0]) * (1e-6 if r["gpu__time_duration.sum"][1] == "us" else 1e-9 if r["gpu__time_duration.sum"][1] == "ns" else 1e-3)
-        alg = 8 * 1024 * 128256 * 2
+        alg = 8 * 1024 * 128256 * 2 * (1 if kind in fwd else 2)  # backward: + bf16 dlogits written
         lines += [f"| algorithmic logits bytes | {alg} |", f"| traffic / algorithmic | {(rd + wr) / alg:.4f} |",
                   f"| achieved (traffic / duration, under ncu) | {(rd + wr) / t / 1e9:.1f} GB/s |", ""]
         stalls = sorted(((float(v[0] or 0), k) for k, v in r.items() if k.startswith("smsp__pcsamp_warps_issue_stalled_")
@@ -66,7 +67,8 @@ def main():
         traffic[kind] = rd + wr
     if traffic:
         json.dump({"V": 128256, "T": 1024, "mb": 8, "tag": tag,
-                   "dram_bytes_per_launch": round(sum(traffic.values()) / len(traffic)),
+                   "dram_bytes_per_launch": round(sum(traffic[k] for k in fwd if k in traffic) /
+                                                  max(1, sum(k in traffic for k in fwd))),
                    "per_variant": {k: round(v) for k, v in traffic.items()}},
                   open(os.path.join(os.path.dirname(__file__), "k1_traffic.json"), "w"), indent=1)
     if len(sys.argv) > 3:

@@ -325,6 +325,48 @@ orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_l
                                  void *dlogits, int64_t out_stride_b, int64_t out_stride_t,
                                  int zero_masked, void *stream);
 
+/* ---- NEXT-4: LM head fused with S1 (tensor cores) ---------------------- */
+
+/* The policy's LM head applied to its final hidden states (the actor
+ * forward that produces the logits).  Logits row (b,t) is
+ *     z[b,t,v] = sum_k hidden[r,k] weight[v,k],   k < d,  v < V,
+ * with r = cu_seqlens[seq_offset+b] - cu_seqlens[seq_offset] + t when
+ * rows->cu_seqlens is set (packed) and r = b*T + t otherwise, relative to
+ * `hidden` (the micro-batch's first row).  The product runs on the tcgen05
+ * tensor cores (bf16 inputs, fp32 accumulation) and is reduced on chip to the
+ * S1 online state, so the [rows, V] logits are never written to memory.
+ * hidden and weight are bf16, 16-byte aligned, with 16-byte aligned row
+ * pitches ld_hidden, ld_weight (elements, >= d); ORL_E_ALIGN otherwise.
+ * Every r a valid (b,t) maps to must be < R; a row that does not is counted
+ * as a mask error (ORL_E_MASK) with NaN outputs.  Rows of `hidden` that no
+ * valid (b,t) maps to are multiplied but do not affect any output. */
+typedef struct {
+    const void *hidden; /* [R, d] bf16 final hidden states of the micro-batch */
+    const void *weight; /* [V, d] bf16 unembedding matrix                     */
+    int64_t R;          /* rows of hidden                                     */
+    int64_t d;          /* hidden size                                        */
+    int64_t V;          /* vocabulary size (= rows of weight)                 */
+    int64_t ld_hidden;  /* row pitch of hidden, elements                      */
+    int64_t ld_weight;  /* row pitch of weight, elements                      */
+} orl_lmhead;
+
+/* orl_logprobs with the logits computed from an LM head: same outputs and
+ * options (S1, and S2+S3 when partner_logp is set), x = inv_temp * z.
+ * `gathered` receives z[b,t,y] as the fp32 accumulator value. */
+orl_status orl_lmhead_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *head,
+                               float inv_temp, float *logp, float *entropy, float *lse,
+                               float *gathered, const float *partner_logp, int kl_est,
+                               double beta_reward, const float *seq_reward, float *kl,
+                               float *shaped_reward, void *stream);
+
+/* orl_ppo_loss with the actor logits computed from its LM head (as above). */
+orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *head,
+                               float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
+                               const float *logp_ref, const float *adv, const float *ret,
+                               const float *v_new, const float *v_old, float *logp_new,
+                               float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
+                               void *stream);
+
 /* ---- NEXT-3: adaptive KL coefficient and early stop (host only) -------- */
 
 /* Host scalar update, no device work ("adaptive KL penalty

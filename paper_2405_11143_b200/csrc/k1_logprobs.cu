@@ -1013,6 +1013,96 @@ __global__ void __launch_bounds__(256) k1_generic_kernel(const K1Params p) {
     if (MODE != kModeLogprob) finish_partials(p, wacc, 1, tid, 256, -1);
 }
 
+// ---------------------------------------------------------------- NEXT-4 merge
+// One thread per valid row: merge the row's K6 split partials (m, s, u) in
+// split order (online_merge), take z_y from the split holding column y, and
+// run the same row epilogue as the streaming kernels.  Loss partials: per
+// thread, xor-tree per warp, warp order per CTA, CTA order by the last CTA.
+template <int MODE>
+__global__ void __launch_bounds__(256) k6_merge_kernel(const K1Params p) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ double wacc[8][kNumPartials];
+    int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw);
+    int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
+    // launched programmatically after K6: its partials are visible after this wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.cum_global) __syncthreads();
+    else build_prefix(p, cum_s, warp_tot);
+    const int64_t N = cum[p.B - 1];
+    zero_masked(p, cum, tid, 256, MODE);
+    double wh[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (MODE != kModeLogprob) {
+        wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3];
+        wh[4] = p.whiten[4];
+    }
+    double acc[kNumPartials];
+#pragma unroll
+    for (int c = 0; c < kNumPartials; ++c) acc[c] = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * 256 + tid; j < N; j += (int64_t)gridDim.x * 256) {
+        int b, t;
+        locate_row(cum, p.B, j, b, t);
+        const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
+        const int y = __ldg(p.tokens + gi);
+        const int64_t r = p.cu_seqlens
+                              ? (int64_t)(__ldg(p.cu_seqlens + p.seq_offset + b) - __ldg(p.cu_seqlens + p.seq_offset)) + t
+                              : (int64_t)b * p.T + t;
+        if (r >= p.lm_R) {  // the hidden matrix does not hold this row: layout/lengths mismatch
+            atomicAdd(&p.err[2], 1ull);
+            const float nan = __int_as_float(0x7fc00000);
+            p.logp[gi] = nan;
+            if (p.entropy) p.entropy[gi] = nan;
+            if (p.lse) p.lse[gi] = nan;
+            continue;
+        }
+        Online tot{kMInit, 0.f, 0.f};
+        for (int sp = 0; sp < p.lm_nsplit; ++sp) {
+            const float4 q = p.lm_parts[(int64_t)sp * p.lm_stride + r];
+            tot = online_merge(tot, Online{q.x, q.y, q.z});
+        }
+        float target = 0.f;
+        if (y >= 0 && y < p.V) target = p.lm_parts[(int64_t)(y / p.lm_split_cols) * p.lm_stride + r].w;
+        float side[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int nside = MODE != kModeLogprob ? 6 : 2;
+        for (int k = 0; k < nside; ++k) side[k] = load_side(p, MODE, k, gi, b);
+        const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+        row_epilogue<MODE>(p, b, t, L, y, tot, target, side, wh, acc);
+    }
+    if (MODE != kModeLogprob) {
+#pragma unroll
+        for (int c = 0; c < kNumPartials; ++c) {
+            double v = acc[c];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) wacc[warp][c] = v;
+        }
+        finish_partials(p, wacc, 8, tid, 256, -1);
+    }
+}
+
+cudaError_t launch_k6_merge(const K1Params &p, int mode, int num_sms, cudaStream_t s) {
+    const size_t smem = sizeof(int32_t) * (size_t)((p.cum_global ? 0 : p.B) + 32);
+    auto kern = mode == kModeLoss ? k6_merge_kernel<kModeLoss> : k6_merge_kernel<kModeLogprob>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = ((int64_t)p.B * p.T + 255) / 256;
+    if (grid > (int64_t)num_sms * 4) grid = (int64_t)num_sms * 4;
+    if (grid > p.ws_stride) grid = p.ws_stride;
+    if (grid < 1) grid = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 // ---------------------------------------------------------------- launcher
 template <typename Tin, int MODE, int POLY>
 static cudaError_t launch_tma(const K1Params &p, int num_sms, cudaStream_t s) {

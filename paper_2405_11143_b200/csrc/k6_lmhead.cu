@@ -1,0 +1,327 @@
+// k6_lmhead.cu -- NEXT-4: the LM-head GEMM fused with the online log-sum-exp.
+//
+// z[r, v] = sum_k h[r, k] W[v, k] (the actor's LM head) is computed on
+// the 5th-generation tensor cores (tcgen05.mma, bf16 x bf16 -> fp32 in TMEM)
+// and reduced on the fly to the S1 online state (m, s, u) of each row
+// (orl_device.cuh) -- the [R, V] logits never exist in HBM.  One CTA owns a
+// 128-row M-tile of h and a contiguous range ("split") of 256-column vocab
+// tiles; it writes one partial (m, s, u, z_y) per row per split, and
+// K1's merge kernel (k1_logprobs.cu, k6_merge_kernel) combines the splits in a
+// fixed order and runs the S1/S2/S3 or S7-S9 row epilogue.
+//
+// Warp roles (192 threads, one CTA per SM):
+//   warp 0      TMA producer: 2-D tensor-map loads of the A (h, 128 x 64) and
+//               B (W, 256 x 64) k-blocks into a 4-stage SWIZZLE_128B ring;
+//   warp 1      TMEM allocator (512 columns = two 128 x 256 fp32 accumulators)
+//               and MMA issuer (one thread: 4 x UMMA 128x256x16 per k-block,
+//               tcgen05.commit -> smem-slot release / accumulator ready);
+//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time from the lane
+//               quarter the warp may access, online max/sum/moment in log2
+//               units, target gather; releases the accumulator to the MMA warp
+//               so tile i+1's MMAs overlap tile i's epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "orl_device.cuh"
+#include "orl_internal.h"
+
+namespace orl {
+namespace {
+
+constexpr int kBM = 128, kBN = kLmTileN, kBK = 64, kStages = 4, kUmmaK = 16;
+constexpr uint32_t kBytesA = kBM * kBK * 2, kBytesB = kBN * kBK * 2, kStageBytes = kBytesA + kBytesB;
+constexpr int kThreads6 = 192;
+constexpr uint32_t kTmemCols = 2 * kBN;
+static_assert(kTmemCols == 512, "two 256-column fp32 accumulators fill TMEM");
+static_assert(kStageBytes % 1024 == 0, "SWIZZLE_128B tiles need 1024-byte alignment");
+
+struct K6Bars {
+    uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+    uint32_t tmem_base;
+};
+constexpr size_t kSmem6 = (size_t)kStages * kStageBytes + 1024 + sizeof(K6Bars);
+
+// ----------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y,
+                                            uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor of a K-major SWIZZLE_128B tile (rows of 64
+// bf16 = 128 B, 8-row swizzle atoms 1024 B apart): start >> 4, LBO = 1
+// (unused for swizzled K-major), SBO = 1024 B >> 4, version 1 (sm_100),
+// layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Instruction descriptor, kind::f16: D fp32 (bit 4), A and B bf16 (bits 7, 10),
+// both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kBM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+        "[%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Target token of hidden row r (or -1 when r is not a valid (b,t) of the call).
+__device__ int row_target(const K6Params &p, int64_t r) {
+    int b, t;
+    if (p.cu_seqlens) {
+        const int32_t *cu = p.cu_seqlens + p.seq_offset;
+        const int32_t c0 = __ldg(cu);
+        int lo = 0, hi = p.B - 1;  // last b with cu[b] - c0 <= r
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int64_t)(__ldg(cu + mid) - c0) <= r) lo = mid;
+            else hi = mid - 1;
+        }
+        b = lo;
+        const int64_t tt = r - (int64_t)(__ldg(cu + b) - c0);
+        if (tt < 0 || tt >= p.T) return -1;
+        t = (int)tt;
+    } else {
+        b = (int)(r / p.T);
+        t = (int)(r % p.T);
+        if (b >= p.B) return -1;
+    }
+    int L = __ldg(p.lengths + p.seq_offset + b);
+    L = L < 0 ? 0 : (L > p.T ? p.T : L);
+    if (t >= L) return -1;
+    return __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
+}
+
+__global__ void __launch_bounds__(kThreads6, 1)
+    k6_lmhead_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const K6Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    K6Bars *bars = reinterpret_cast<K6Bars *>(sm + kStages * kStageBytes);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_tile = blockIdx.x % p.m_tiles, split = blockIdx.x / p.m_tiles;
+    const int t_beg = split * p.tiles_per_split;
+    const int t_end = min(p.n_tiles, t_beg + p.tiles_per_split);
+    const int ntiles = t_end - t_beg;
+    const int kblocks = (p.d + kBK - 1) / kBK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bars->full[s], 1);
+            mbar_init(&bars->empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bars->tfull[a], 1);
+            mbar_init(&bars->tempty[a], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&bars->tmem_base)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = bars->tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            prefetch_tmap(&tmA);
+            prefetch_tmap(&tmB);
+            const uint64_t pol_a = l2_evict_last_policy();    // h: re-read for every vocab tile
+            const uint64_t pol_b = l2_evict_normal_policy();  // W: shared by the concurrent M-tiles
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < ntiles; ++i) {
+                const int n0 = (t_beg + i) * kBN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&bars->empty[stage], phase ^ 1u);
+                    uint8_t *sa = sm + stage * kStageBytes;
+                    mbar_arrive_expect_tx(&bars->full[stage], kStageBytes);
+                    tma_load_2d(sa, &tmA, &bars->full[stage], kb * kBK, m_tile * kBM, pol_a);
+                    tma_load_2d(sa + kBytesA, &tmB, &bars->full[stage], kb * kBK, n0, pol_b);
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < ntiles; ++i) {
+                const int a = i & 1;
+                const uint32_t aphase = (uint32_t)(i >> 1) & 1u;
+                mbar_wait(&bars->tempty[a], aphase ^ 1u);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(a * kBN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&bars->full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(sm + stage * kStageBytes);
+                    const uint64_t da = sw128_kmajor_desc(sa), db = sw128_kmajor_desc(sa + kBytesA);
+#pragma unroll
+                    for (int k = 0; k < kBK / kUmmaK; ++k)  // +32 B along K inside the 128-B swizzle row
+                        umma_bf16(d_tmem, da + 2 * k, db + 2 * k, (kb | k) != 0 ? 1u : 0u);
+                    umma_commit(&bars->empty[stage]);
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+                umma_commit(&bars->tfull[a]);
+            }
+        }
+    } else {
+        // epilogue: warp w may read TMEM lanes 32 (w % 4) .. +31
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int64_t r = (int64_t)m_tile * kBM + row;
+        const int y = r < p.R ? row_target(p, r) : -1;
+        const float c2 = p.c2;
+        float m = kMInit, s = 0.f, u = 0.f, tgt = __int_as_float(0x7fc00000);
+        for (int i = 0; i < ntiles; ++i) {
+            const int a = i & 1;
+            const uint32_t aphase = (uint32_t)(i >> 1) & 1u;
+            mbar_wait(&bars->tfull[a], aphase);
+            tc_fence_after();
+            const int n0 = (t_beg + i) * kBN;
+#pragma unroll 1
+            for (int c = 0; c < kBN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * kBN + c * 32), v);
+                const int col0 = n0 + c * 32;
+                const int nvalid = p.V - col0;  // columns >= V are TMA zero-fill: excluded
+                if ((unsigned)(y - col0) < 32u) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j == y - col0) tgt = __uint_as_float(v[j]);
+                }
+                if (nvalid <= 0) continue;
+                float x[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    x[j] = j < nvalid ? __uint_as_float(v[j]) : kNegClampF32;
+                float cm0 = x[0], cm1 = x[1];
+#pragma unroll
+                for (int j = 2; j < 32; j += 2) {
+                    cm0 = fmax_nan(cm0, x[j]);
+                    cm1 = fmax_nan(cm1, x[j + 1]);
+                }
+                const float mn = fmax_nan(m, fmax_nan(cm0, cm1) * c2);
+                const float dm = m - mn, rs = ex2(dm);
+                u = rs * fmaf(dm, s, u);
+                s = rs * s;
+                m = mn;
+                float s0 = 0.f, s1 = 0.f, u0 = 0.f, u1 = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                    const float t0 = fmaf(x[j], c2, -m), t1 = fmaf(x[j + 1], c2, -m);
+                    const float e0 = ex2(t0), e1 = ex2(t1);
+                    s0 += e0;
+                    s1 += e1;
+                    u0 = fmaf(e0, t0, u0);
+                    u1 = fmaf(e1, t1, u1);
+                }
+                s += s0 + s1;
+                u += u0 + u1;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->tempty[a]);
+        }
+        if (r < p.R) p.parts[(int64_t)split * p.part_stride + r] = make_float4(m, s, u, tgt);
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+void k6_plan(K6Params &p, int num_sms) {
+    p.m_tiles = (int)((p.R + kBM - 1) / kBM);
+    p.n_tiles = (int)((p.V + kBN - 1) / kBN);
+    int tps = 8;
+    if (const char *e = getenv("ORL_K6_TPS")) tps = atoi(e);
+    const int64_t total = (int64_t)p.m_tiles * p.n_tiles;
+    if (total < (int64_t)num_sms * tps) tps = (int)(total / num_sms);  // keep every SM busy on small problems
+    if (tps < 1) tps = 1;
+    if (tps > p.n_tiles) tps = p.n_tiles;
+    p.tiles_per_split = tps;
+    p.n_split = (p.n_tiles + tps - 1) / tps;
+}
+
+cudaError_t launch_k6(const K6Params &p, const void *hidden, int64_t ld_hidden, const void *weight,
+                      int64_t ld_weight, cudaStream_t s) {
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, hidden, p.R, p.d, ld_hidden, kBM) || !make_map(&mb, weight, p.V, p.d, ld_weight, kBN))
+        return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(k6_lmhead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem6);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = (int64_t)p.m_tiles * p.n_split;
+    if (grid < 1 || grid > 0x7fffffff) return cudaErrorInvalidConfiguration;
+    k6_lmhead_kernel<<<(unsigned)grid, kThreads6, kSmem6, s>>>(ma, mb, p);
+    return cudaGetLastError();
+}
+
+}  // namespace orl

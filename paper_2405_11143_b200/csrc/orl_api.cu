@@ -51,6 +51,8 @@ struct orl_ctx {
     double *h_stats = nullptr;         // pinned [16 + 4]
     int32_t *d_cum = nullptr;          // length prefix of large micro-batches
     int64_t cum_cap = 0;
+    float4 *d_lm_parts = nullptr;      // NEXT-4 split partials
+    int64_t lm_cap = 0;
     bool have_adv = false, have_whiten = false;
     int imported_w = 0, imported_s = 0;
     uint64_t launches = 0;
@@ -92,13 +94,10 @@ static orl_status set_device(orl_ctx *ctx) {
     return ORL_OK;
 }
 
-static orl_status validate_rows_logits(orl_ctx *ctx, const orl_rows *rows, const orl_logits *lg,
-                                       float inv_temp) {
-    if (!rows || !lg) return fail(ctx, ORL_E_INVALID_ARG, "rows/logits is NULL");
-    if (!rows->tokens || !rows->lengths || !lg->ptr)
-        return fail(ctx, ORL_E_INVALID_ARG, "tokens, lengths and logits.ptr are required");
-    if (lg->dtype != ORL_BF16 && lg->dtype != ORL_F32)
-        return fail(ctx, ORL_E_DTYPE, "unknown logits dtype %d", lg->dtype);
+static orl_status validate_rows(orl_ctx *ctx, const orl_rows *rows, float inv_temp) {
+    if (!rows) return fail(ctx, ORL_E_INVALID_ARG, "rows is NULL");
+    if (!rows->tokens || !rows->lengths)
+        return fail(ctx, ORL_E_INVALID_ARG, "tokens and lengths are required");
     if (rows->B < 1 || rows->B > ORL_MAX_SEQ_PER_CALL)
         return fail(ctx, ORL_E_SHAPE, "B=%lld outside [1, %d]", (long long)rows->B, ORL_MAX_SEQ_PER_CALL);
     if (rows->T < 1 || rows->seq_offset < 0)
@@ -106,15 +105,45 @@ static orl_status validate_rows_logits(orl_ctx *ctx, const orl_rows *rows, const
                     (long long)rows->seq_offset);
     if (rows->B * rows->T >= (int64_t)1 << 31 || (rows->seq_offset + rows->B) * rows->T >= (int64_t)1 << 40)
         return fail(ctx, ORL_E_SHAPE, "B*T too large");
+    if (!(inv_temp > 0.f) || !(inv_temp <= 1.0e4f))
+        return fail(ctx, ORL_E_INVALID_ARG, "inv_temp=%g must be in (0, 1e4]", (double)inv_temp);
+    if (!aligned4(rows->tokens) || !aligned4(rows->lengths) || !aligned4(rows->cu_seqlens))
+        return fail(ctx, ORL_E_ALIGN, "tokens/lengths/cu_seqlens must be 4-byte aligned");
+    return ORL_OK;
+}
+
+static orl_status validate_rows_logits(orl_ctx *ctx, const orl_rows *rows, const orl_logits *lg,
+                                       float inv_temp) {
+    if (!lg) return fail(ctx, ORL_E_INVALID_ARG, "logits is NULL");
+    if (!lg->ptr) return fail(ctx, ORL_E_INVALID_ARG, "logits.ptr is required");
+    if (lg->dtype != ORL_BF16 && lg->dtype != ORL_F32)
+        return fail(ctx, ORL_E_DTYPE, "unknown logits dtype %d", lg->dtype);
+    orl_status st = validate_rows(ctx, rows, inv_temp);
+    if (st) return st;
     if (lg->V < 1 || lg->V >= ((int64_t)1 << 31))
         return fail(ctx, ORL_E_SHAPE, "V=%lld invalid", (long long)lg->V);
     if (lg->stride_t < lg->V || lg->stride_b < 0)
         return fail(ctx, ORL_E_SHAPE, "strides (%lld, %lld) invalid for V=%lld", (long long)lg->stride_b,
                     (long long)lg->stride_t, (long long)lg->V);
-    if (!(inv_temp > 0.f) || !(inv_temp <= 1.0e4f))
-        return fail(ctx, ORL_E_INVALID_ARG, "inv_temp=%g must be in (0, 1e4]", (double)inv_temp);
-    if (!aligned4(rows->tokens) || !aligned4(rows->lengths) || !aligned4(rows->cu_seqlens))
-        return fail(ctx, ORL_E_ALIGN, "tokens/lengths/cu_seqlens must be 4-byte aligned");
+    return ORL_OK;
+}
+
+// NEXT-4: the LM-head source (hidden states + unembedding matrix, bf16).
+static orl_status validate_rows_lmhead(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *h,
+                                       float inv_temp) {
+    if (!h) return fail(ctx, ORL_E_INVALID_ARG, "lmhead is NULL");
+    if (!h->hidden || !h->weight) return fail(ctx, ORL_E_INVALID_ARG, "lmhead.hidden and lmhead.weight are required");
+    orl_status st = validate_rows(ctx, rows, inv_temp);
+    if (st) return st;
+    if (h->V < 1 || h->V >= ((int64_t)1 << 31)) return fail(ctx, ORL_E_SHAPE, "V=%lld invalid", (long long)h->V);
+    if (h->d < 1 || h->d >= ((int64_t)1 << 31)) return fail(ctx, ORL_E_SHAPE, "d=%lld invalid", (long long)h->d);
+    if (h->R < 1 || h->R >= ((int64_t)1 << 31)) return fail(ctx, ORL_E_SHAPE, "R=%lld invalid", (long long)h->R);
+    if (h->ld_hidden < h->d || h->ld_weight < h->d)
+        return fail(ctx, ORL_E_SHAPE, "row pitches (%lld, %lld) < d=%lld", (long long)h->ld_hidden,
+                    (long long)h->ld_weight, (long long)h->d);
+    if ((reinterpret_cast<uintptr_t>(h->hidden) | reinterpret_cast<uintptr_t>(h->weight)) % 16 != 0 ||
+        (h->ld_hidden * 2) % 16 != 0 || (h->ld_weight * 2) % 16 != 0)
+        return fail(ctx, ORL_E_ALIGN, "lmhead rows must be 16-byte aligned (base and pitch)");
     return ORL_OK;
 }
 
@@ -129,12 +158,14 @@ static bool tma_eligible(const orl_logits *lg) {
 static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const orl_logits *lg,
                         float inv_temp) {
     std::memset(&p, 0, sizeof p);
-    p.base = static_cast<const char *>(lg->ptr);
-    p.V = lg->V;
-    p.stride_b = lg->stride_b;
-    p.stride_t = lg->stride_t;
-    p.elt = lg->dtype == ORL_BF16 ? 2 : 4;
-    p.row_bytes = lg->V * p.elt;
+    if (lg) {
+        p.base = static_cast<const char *>(lg->ptr);
+        p.V = lg->V;
+        p.stride_b = lg->stride_b;
+        p.stride_t = lg->stride_t;
+        p.elt = lg->dtype == ORL_BF16 ? 2 : 4;
+        p.row_bytes = lg->V * p.elt;
+    }
     p.inv_temp = inv_temp;
     p.c2 = inv_temp * 1.4426950408889634f;
     {
@@ -255,6 +286,7 @@ extern "C" orl_status orl_destroy(orl_ctx *ctx) {
     cudaFree(ctx->d_gather_s);
     cudaFree(ctx->d_stats);
     cudaFree(ctx->d_cum);
+    cudaFree(ctx->d_lm_parts);
     if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
     delete ctx;
     return ORL_OK;
@@ -281,13 +313,53 @@ extern "C" orl_status orl_begin_iteration(orl_ctx *ctx, void *stream) {
 }
 
 // ------------------------------------------------------------------ S1 (+S2/S3)
-extern "C" orl_status orl_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_logits *logits,
-                                   float inv_temp, float *logp, float *entropy, float *lse,
-                                   float *gathered, const float *partner_logp, int kl_est,
-                                   double beta_reward, const float *seq_reward, float *kl,
-                                   float *shaped_reward, void *stream) {
+// NEXT-4: K6 (tcgen05 LM-head GEMM -> per-split online partials) then the
+// merge kernel with K1's row epilogue in `mode`.
+static orl_status run_lmhead(orl_ctx *ctx, K1Params &p, const orl_lmhead *h, int mode, cudaStream_t s) {
+    K6Params q;
+    std::memset(&q, 0, sizeof q);
+    q.R = h->R;
+    q.d = (int)h->d;
+    q.V = (int)h->V;
+    q.c2 = p.c2;
+    q.B = p.B;
+    q.T = p.T;
+    q.seq_offset = p.seq_offset;
+    q.tokens = p.tokens;
+    q.lengths = p.lengths;
+    q.cu_seqlens = p.cu_seqlens;
+    k6_plan(q, ctx->num_sms);
+    const int64_t need = (int64_t)q.n_split * q.R;
+    if (need > ctx->lm_cap) {
+        CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        cudaFree(ctx->d_lm_parts);
+        ctx->d_lm_parts = nullptr;
+        ctx->lm_cap = 0;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->d_lm_parts, (size_t)need * sizeof(float4)));
+        ctx->lm_cap = need;
+    }
+    q.parts = ctx->d_lm_parts;
+    q.part_stride = q.R;
+    CUDA_TRY(ctx, launch_k6(q, h->hidden, h->ld_hidden, h->weight, h->ld_weight, s));
+    p.V = h->V;
+    p.lm_parts = ctx->d_lm_parts;
+    p.lm_stride = q.R;
+    p.lm_R = q.R;
+    p.lm_nsplit = q.n_split;
+    p.lm_split_cols = q.tiles_per_split * kLmTileN;
+    CUDA_TRY(ctx, launch_k6_merge(p, mode, ctx->num_sms, s));
+    ctx->launches += 2;
+    return ORL_OK;
+}
+
+static orl_status logprobs_impl(orl_ctx *ctx, const orl_rows *rows, const orl_logits *logits,
+                                const orl_lmhead *head, float inv_temp, float *logp, float *entropy,
+                                float *lse, float *gathered, const float *partner_logp, int kl_est,
+                                double beta_reward, const float *seq_reward, float *kl,
+                                float *shaped_reward, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
-    orl_status st = validate_rows_logits(ctx, rows, logits, inv_temp);
+    orl_status st = head ? validate_rows_lmhead(ctx, rows, head, inv_temp)
+                         : validate_rows_logits(ctx, rows, logits, inv_temp);
     if (st) return st;
     if (!logp) return fail(ctx, ORL_E_INVALID_ARG, "logp is required");
     if (!aligned4(logp) || !aligned4(entropy) || !aligned4(lse) || !aligned4(gathered) ||
@@ -313,9 +385,30 @@ extern "C" orl_status orl_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl
     p.kl_out = kl;
     p.shaped = shaped_reward;
     if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
+    if (head) return run_lmhead(ctx, p, head, kModeLogprob, as_stream(stream));
     CUDA_TRY(ctx, launch_k1(p, tma_eligible(logits), kModeLogprob, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
     return ORL_OK;
+}
+
+extern "C" orl_status orl_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_logits *logits,
+                                   float inv_temp, float *logp, float *entropy, float *lse,
+                                   float *gathered, const float *partner_logp, int kl_est,
+                                   double beta_reward, const float *seq_reward, float *kl,
+                                   float *shaped_reward, void *stream) {
+    return logprobs_impl(ctx, rows, logits, nullptr, inv_temp, logp, entropy, lse, gathered, partner_logp,
+                         kl_est, beta_reward, seq_reward, kl, shaped_reward, stream);
+}
+
+extern "C" orl_status orl_lmhead_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *head,
+                                          float inv_temp, float *logp, float *entropy, float *lse,
+                                          float *gathered, const float *partner_logp, int kl_est,
+                                          double beta_reward, const float *seq_reward, float *kl,
+                                          float *shaped_reward, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (!head) return fail(ctx, ORL_E_INVALID_ARG, "lmhead is NULL");
+    return logprobs_impl(ctx, rows, nullptr, head, inv_temp, logp, entropy, lse, gathered, partner_logp,
+                         kl_est, beta_reward, seq_reward, kl, shaped_reward, stream);
 }
 
 // ------------------------------------------------------------------ S4/S4'/S5
@@ -413,9 +506,11 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
                                 const orl_ppo_cfg *cfg, const float *logp_old, const float *logp_ref,
                                 const float *adv, const float *ret, const float *v_new, const float *v_old,
                                 float *logp_new, float *entropy, float *lse, float *dloss_dlogp,
-                                float *dloss_dv, const GradOut *grad, void *stream) {
+                                float *dloss_dv, const GradOut *grad, void *stream,
+                                const orl_lmhead *head = nullptr) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
-    orl_status st = validate_rows_logits(ctx, rows, actor, inv_temp);
+    orl_status st = head ? validate_rows_lmhead(ctx, rows, head, inv_temp)
+                         : validate_rows_logits(ctx, rows, actor, inv_temp);
     if (st) return st;
     if (!cfg || !logp_old || !adv || !logp_new)
         return fail(ctx, ORL_E_INVALID_ARG, "cfg, logp_old, adv and logp_new are required");
@@ -460,6 +555,7 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     p.kl_in_loss = cfg->kl_in_loss;
     p.loss_agg = cfg->loss_agg;
     if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
+    if (head) return run_lmhead(ctx, p, head, kModeLoss, as_stream(stream));
     const bool tma = tma_eligible(actor);
     if (!grad) {
         CUDA_TRY(ctx, launch_k1(p, tma, kModeLoss, ctx->num_sms, as_stream(stream)));
@@ -495,6 +591,18 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
                                    void *stream) {
     return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
                          logp_new, entropy, lse, dloss_dlogp, dloss_dv, nullptr, stream);
+}
+
+extern "C" orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *head,
+                                          float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
+                                          const float *logp_ref, const float *adv, const float *ret,
+                                          const float *v_new, const float *v_old, float *logp_new,
+                                          float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
+                                          void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (!head) return fail(ctx, ORL_E_INVALID_ARG, "lmhead is NULL");
+    return ppo_loss_impl(ctx, rows, nullptr, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
+                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, nullptr, stream, head);
 }
 
 extern "C" orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,

@@ -53,6 +53,11 @@ struct K1Params {
     double c2_ent;         // entropy coefficient of the total loss
     int zero_masked_grad;
     const int32_t *cum_global;  // prefix of the micro-batch lengths (large B), else NULL
+    // NEXT-4 merge (k6_merge_kernel): per-split partials of the LM-head GEMM
+    const float4 *lm_parts;     // [lm_nsplit][lm_stride] (m, s, u, z_y) per hidden row
+    int64_t lm_stride;          // rows per split slab (>= lm_R)
+    int64_t lm_R;               // hidden rows
+    int lm_nsplit, lm_split_cols;  // splits, vocab columns per split
     // accounting
     double *ws;            // [kNumPartials][ws_stride] per-CTA partials
     int ws_stride;
@@ -93,6 +98,26 @@ struct K5Params {
 };
 cudaError_t launch_k5(const K5Params &p, bool tma, int num_sms, cudaStream_t s);
 size_t k5_smem_bytes(int B);
+
+// K6 (NEXT-4): LM-head GEMM (tcgen05) + online LSE partials.
+constexpr int kLmTileN = 256;  // vocab columns per UMMA tile
+struct K6Params {
+    int64_t R;          // hidden rows (TMA map height)
+    int d, V;           // hidden size, vocabulary
+    int m_tiles, n_tiles, tiles_per_split, n_split;  // filled by k6_plan
+    float c2;           // inv_temp * log2(e)
+    int B, T;
+    int64_t seq_offset;
+    const int32_t *tokens, *lengths, *cu_seqlens;
+    float4 *parts;      // [n_split][part_stride]
+    int64_t part_stride;
+};
+void k6_plan(K6Params &p, int num_sms);
+// hidden [R, d] and weight [V, d] bf16 with row pitches in elements (16-byte aligned rows).
+cudaError_t launch_k6(const K6Params &p, const void *hidden, int64_t ld_hidden, const void *weight,
+                      int64_t ld_weight, cudaStream_t s);
+// Merge the K6 partials of every valid row and run K1's row epilogue (mode 0 or 1).
+cudaError_t launch_k6_merge(const K1Params &p, int mode, int num_sms, cudaStream_t s);
 
 struct K3Params {
     int B, T, kind, G;

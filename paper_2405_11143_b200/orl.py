@@ -47,6 +47,12 @@ class Rows(ctypes.Structure):
                 ("tokens", ctypes.c_void_p), ("lengths", ctypes.c_void_p), ("cu_seqlens", ctypes.c_void_p)]
 
 
+class LmHead(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_void_p), ("weight", ctypes.c_void_p), ("R", ctypes.c_int64),
+                ("d", ctypes.c_int64), ("V", ctypes.c_int64), ("ld_hidden", ctypes.c_int64),
+                ("ld_weight", ctypes.c_int64)]
+
+
 class PpoCfg(ctypes.Structure):
     _fields_ = [("eps_low", ctypes.c_double), ("eps_high", ctypes.c_double),
                 ("eps_value", ctypes.c_double), ("c1", ctypes.c_double), ("c2", ctypes.c_double),
@@ -87,6 +93,10 @@ _lib.orl_ppo_loss_and_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(
                                        _I64, _I64, _I32, _P]
 _lib.orl_logits_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32, ctypes.POINTER(PpoCfg),
                                  _P, _P, _P, _P, _I64, _I64, _I32, _P]
+_lib.orl_lmhead_logprobs.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(LmHead), _F32, _P, _P, _P, _P,
+                                     _P, _I32, _F64, _P, _P, _P, _P]
+_lib.orl_lmhead_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(LmHead), _F32,
+                                     ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
@@ -215,6 +225,50 @@ def orl_logprobs(ctx: Context, tokens, lengths, logits, logp, *, seq_offset=0, i
                            _ptr(entropy), _ptr(lse), _ptr(gathered), _ptr(partner_logp),
                            KL.get(kl_est, kl_est), float(beta_reward), _ptr(seq_reward), _ptr(kl),
                            _ptr(shaped_reward), _stream(stream))
+    return ctx.check(st)
+
+
+def _lmhead(hidden, weight):
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("LM head hidden states and weight must be bf16")
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.stride(1) != 1 or weight.stride(1) != 1:
+        raise ValueError("hidden [R, d] and weight [V, d] must be 2-D with unit stride along d")
+    if hidden.shape[1] != weight.shape[1]:
+        raise ValueError(f"hidden size mismatch: {hidden.shape[1]} vs {weight.shape[1]}")
+    return LmHead(hidden.data_ptr(), weight.data_ptr(), hidden.shape[0], hidden.shape[1], weight.shape[0],
+                  hidden.stride(0), weight.stride(0))
+
+
+def orl_lmhead_logprobs(ctx: Context, tokens, lengths, hidden, weight, logp, *, B=None, seq_offset=0,
+                        inv_temp=1.0, entropy=None, lse=None, gathered=None, partner_logp=None, kl_est="k1",
+                        beta_reward=0.0, seq_reward=None, kl=None, shaped_reward=None, stream=None,
+                        cu_seqlens=None):
+    """NEXT-4: orl_logprobs with logits = hidden @ weight.T computed on the tensor cores
+    (never materialised).  hidden [R, d] holds the call's rows: packed by `cu_seqlens`
+    or b*T + t; `B` = sequences in the call (default: all from seq_offset)."""
+    T = tokens.shape[1]
+    if B is None:
+        B = tokens.shape[0] - seq_offset
+    rows, hd = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), _lmhead(hidden, weight)
+    st = _lib.orl_lmhead_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(hd), float(inv_temp), _ptr(logp),
+                                  _ptr(entropy), _ptr(lse), _ptr(gathered), _ptr(partner_logp),
+                                  KL.get(kl_est, kl_est), float(beta_reward), _ptr(seq_reward), _ptr(kl),
+                                  _ptr(shaped_reward), _stream(stream))
+    return ctx.check(st)
+
+
+def orl_lmhead_ppo_loss(ctx: Context, tokens, lengths, hidden, weight, cfg, logp_old, adv, logp_new, *,
+                        B=None, seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
+                        entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, stream=None, cu_seqlens=None):
+    """NEXT-4: orl_ppo_loss with the actor logits computed from its LM head."""
+    T = tokens.shape[1]
+    if B is None:
+        B = tokens.shape[0] - seq_offset
+    rows, hd, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), _lmhead(hidden, weight), cfg.c()
+    st = _lib.orl_lmhead_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(hd), float(inv_temp), ctypes.byref(c),
+                                  _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
+                                  _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
+                                  _ptr(dloss_dv), _stream(stream))
     return ctx.check(st)
 
 

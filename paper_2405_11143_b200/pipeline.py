@@ -9,7 +9,7 @@ bookkeeping live here; the arithmetic is in liborl.so.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Callable, Optional
+from typing import Callable, NamedTuple, Optional, Union
 
 import torch
 
@@ -60,7 +60,16 @@ class Buffers:
         self.stats_dev = torch.zeros(_orl.STATS_N, dtype=torch.float64, device=device)
 
 
-LogitsSource = Callable[[str, int, int], torch.Tensor]   # (role, seq_start, seq_end) -> [e-s, T, V]
+class LmHeadRows(NamedTuple):
+    """NEXT-4 source: a micro-batch's final hidden states [R, d] (row b*T + t, or packed
+    by `cu_seqlens`) and the policy's LM-head weight [V, d], both bf16."""
+    hidden: torch.Tensor
+    weight: torch.Tensor
+    cu_seqlens: Optional[torch.Tensor] = None
+
+
+# (role, seq_start, seq_end) -> [e-s, T, V] logits, or LmHeadRows (NEXT-4)
+LogitsSource = Callable[[str, int, int], Union[torch.Tensor, LmHeadRows]]
 
 
 def microbatches(B: int, mb: int):
@@ -81,19 +90,25 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
     mbs = microbatches(B, mb)
     hook = on_k1 or (lambda tag: None)
     _orl.orl_begin_iteration(ctx, stream)
+
+    def s1(src, s, e, out, **kw):
+        if isinstance(src, LmHeadRows):               # NEXT-4: logits never materialised
+            return _orl.orl_lmhead_logprobs(ctx, tok, L, src.hidden, src.weight, out, B=e - s, seq_offset=s,
+                                            inv_temp=cfg.inv_temp, cu_seqlens=src.cu_seqlens, stream=stream,
+                                            **kw)
+        return _orl.orl_logprobs(ctx, tok, L, src, out, seq_offset=s, inv_temp=cfg.inv_temp, stream=stream,
+                                 **kw)
+
     for s, e in mbs:                                   # S1, old policy
         h = hook("old")
-        _orl.orl_logprobs(ctx, tok, L, logits("old", s, e), bufs.logp_old, seq_offset=s,
-                          inv_temp=cfg.inv_temp, stream=stream)
+        s1(logits("old", s, e), s, e, bufs.logp_old)
         if h: h()
     if cfg.use_ref:
         for s, e in mbs:                               # S1+S2+S3, reference
             h = hook("ref")
-            _orl.orl_logprobs(ctx, tok, L, logits("ref", s, e), bufs.logp_ref, seq_offset=s,
-                              inv_temp=cfg.inv_temp, partner_logp=bufs.logp_old, kl_est=cfg.kl_est_reward,
-                              beta_reward=cfg.beta_reward if cfg.kl_mode == "reward" else 0.0,
-                              seq_reward=batch["seq_reward"], kl=bufs.kl, shaped_reward=bufs.shaped,
-                              stream=stream)
+            s1(logits("ref", s, e), s, e, bufs.logp_ref, partner_logp=bufs.logp_old, kl_est=cfg.kl_est_reward,
+               beta_reward=cfg.beta_reward if cfg.kl_mode == "reward" else 0.0,
+               seq_reward=batch["seq_reward"], kl=bufs.kl, shaped_reward=bufs.shaped)
             if h: h()
     else:
         raise NotImplementedError("the paper's PPO loop always has a reference model (P:193)")
@@ -105,6 +120,8 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
                         stream=stream)
     _orl.orl_whiten_stats(ctx, cfg.whiten and cfg.adv_kind != "grpo", stream)         # S6 + C1
     critic = cfg.critic and batch.get("values_new") is not None
+    if grad_sink is not None and isinstance(logits("new", 0, min(B, mb)), LmHeadRows):
+        raise NotImplementedError("dL/dlogits needs materialised logits; the LM-head path (NEXT-4) is forward-only")
     if grad_sink is not None and fused_grad:           # S1 + S7..S9 + NEXT-1 in one pass
         for s, e in mbs:
             h = hook("new+grad")
@@ -121,12 +138,16 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
         return _orl.orl_finalize(ctx, cfg.ppo, dev_out=bufs.stats_dev, stream=stream)
     for s, e in mbs:                                   # S1 + S7..S9, actor
         h = hook("new")
-        _orl.orl_ppo_loss(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.logp_old, bufs.adv, bufs.logp_new,
-                          seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
-                          ret=bufs.ret if critic else None, v_new=batch["values_new"] if critic else None,
-                          v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
-                          lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
-                          stream=stream)
+        src = logits("new", s, e)
+        kw = dict(seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
+                  ret=bufs.ret if critic else None, v_new=batch["values_new"] if critic else None,
+                  v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
+                  lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None, stream=stream)
+        if isinstance(src, LmHeadRows):
+            _orl.orl_lmhead_ppo_loss(ctx, tok, L, src.hidden, src.weight, cfg.ppo, bufs.logp_old, bufs.adv,
+                                     bufs.logp_new, B=e - s, cu_seqlens=src.cu_seqlens, **kw)
+        else:
+            _orl.orl_ppo_loss(ctx, tok, L, src, cfg.ppo, bufs.logp_old, bufs.adv, bufs.logp_new, **kw)
         if h: h()
     if grad_sink is not None:                          # NEXT-1: dL/dlogits
         for s, e in mbs:

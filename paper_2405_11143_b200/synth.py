@@ -175,3 +175,38 @@ def split_numpy(batch: dict, n: int, group_size: int = 1):
     for s, e in split_bounds(B, n, group_size):
         out.append({k: v[s:e] for k, v in batch.items()})
     return out
+
+
+@torch.no_grad()
+def make_lmhead_batch(seed: int, B: int, T: int, d: int, V: int, lengths="mixed", rewards="normal",
+                      group_size: int = 1, packed: bool = False, device="cpu", logit_std: float = 3.0):
+    """NEXT-4 inputs: final hidden states of the three roles and
+    one bf16 LM-head weight.  Rows: b*T + t (padded) or packed by cu_seqlens (valid
+    tokens only).  hidden_old = s_r N(0, I) with a per-row scale s_r ~ U(0.5, 1.5)
+    (entropy varies by row), hidden_ref = hidden_old + 0.05 N, hidden_new =
+    hidden_old + 0.03 N; W ~ N(0, logit_std^2 / d) so logits have std ~ logit_std s_r."""
+    L = lengths_for(B, T, seed, lengths) if isinstance(lengths, str) else torch.as_tensor(lengths, dtype=torch.int32)
+    tok = tokens_for(B, T, V, seed)
+    if packed:
+        cu = torch.zeros(B + 1, dtype=torch.int32)
+        cu[1:] = torch.cumsum(L.clamp(0, T), 0)
+        R = int(cu[-1])
+    else:
+        cu = None
+        R = B * T
+    R = max(R, 1)
+    g = torch.Generator(device=device).manual_seed(role_seed(seed, 20_000, 0))
+    base = torch.randn(R, d, generator=g, device=device)
+    base *= torch.rand(R, 1, generator=g, device=device) + 0.5
+    hid = {"old": base.to(torch.bfloat16),
+           "ref": (base + 0.05 * torch.randn(R, d, generator=g, device=device)).to(torch.bfloat16),
+           "new": (base + 0.03 * torch.randn(R, d, generator=g, device=device)).to(torch.bfloat16)}
+    del base
+    W = torch.empty(V, d, dtype=torch.bfloat16, device=device)
+    for s in range(0, V, 8192):  # chunked: no fp32 copy of the whole matrix
+        e = min(V, s + 8192)
+        W[s:e] = (torch.randn(e - s, d, generator=g, device=device) * (logit_std / d ** 0.5)).to(torch.bfloat16)
+    R_ = rewards_for(B, seed, rewards, group_size)
+    v_old, v_new = values_for(B, T, seed)
+    return dict(hidden_old=hid["old"], hidden_ref=hid["ref"], hidden_new=hid["new"], weight=W, tokens=tok,
+                lengths=L, cu_seqlens=cu, seq_reward=R_, values_old=v_old, values_new=v_new)

@@ -54,21 +54,25 @@ def test_library_is_sm100a(lib):
     sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
     assert "UBLKCP" in sass or "UTMALDG" in sass, "TMA bulk copies missing from SASS"
     assert "FFMA2" in sass and "MUFU.EX2" in sass
+    # NEXT-4: tcgen05 MMA (UTCHMMA), TMEM loads (LDTM) and 2-D tensor TMA in the LM-head kernel
+    assert "UTCHMMA" in sass and "LDTM" in sass and "UTMALDG.2D" in sass
 
 
 def test_struct_layouts_match_c(lib, tmp_path):
     from paper_2405_11143_b200 import orl
     src = tmp_path / "sz.c"
     src.write_text('#include "orl.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(void){'
-                   'printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(orl_logits), sizeof(orl_rows), sizeof(orl_ppo_cfg),'
+                   'printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(orl_logits), sizeof(orl_rows), sizeof(orl_ppo_cfg),'
                    ' sizeof(orl_stats), offsetof(orl_ppo_cfg, kl_loss_est), offsetof(orl_stats, n_guard),'
-                   ' offsetof(orl_ppo_cfg, ratio_guard), offsetof(orl_ppo_cfg, loss_agg));return 0;}\n')
+                   ' offsetof(orl_ppo_cfg, ratio_guard), offsetof(orl_ppo_cfg, loss_agg), sizeof(orl_lmhead),'
+                   ' offsetof(orl_lmhead, ld_weight));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     want = [ctypes.sizeof(orl.Logits), ctypes.sizeof(orl.Rows), ctypes.sizeof(orl.PpoCfg),
             ctypes.sizeof(orl.Stats), orl.PpoCfg.kl_loss_est.offset, orl.Stats.n_guard.offset,
-            orl.PpoCfg.ratio_guard.offset, orl.PpoCfg.loss_agg.offset]
+            orl.PpoCfg.ratio_guard.offset, orl.PpoCfg.loss_agg.offset, ctypes.sizeof(orl.LmHead),
+            orl.LmHead.ld_weight.offset]
     assert got == want
 
 

@@ -104,7 +104,7 @@ constexpr int kLmTileN = 256;  // vocab columns per UMMA tile
 struct K6Params {
     int64_t R;          // hidden rows (TMA map height)
     int d, V;           // hidden size, vocabulary
-    int m_tiles, n_tiles, tiles_per_split, n_split;  // filled by k6_plan
+    int m_tiles, n_tiles, tiles_per_split, n_split, grid, two_sm;  // filled by k6_plan
     float c2;           // inv_temp * log2(e)
     int B, T;
     int64_t seq_offset;

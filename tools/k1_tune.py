@@ -13,6 +13,12 @@ sys.path.insert(0, ROOT)
 VARIANTS = {
     "default": [],
     "always_ent": ["ORL_K1_ALWAYS_ENT=1"],
+    # K6 (NEXT-4) wait policies: epilogue / producer mbarrier suspend hints (ns)
+    "k6_spin": ["ORL_K6_EPI_SLEEP_NS=0", "ORL_K6_PROD_SLEEP_NS=0"],
+    "k6_epi2k": ["ORL_K6_EPI_SLEEP_NS=2000"],
+    "k6_epi20k": ["ORL_K6_EPI_SLEEP_NS=20000"],
+    "k6_epi20k_prod1k": ["ORL_K6_EPI_SLEEP_NS=20000", "ORL_K6_PROD_SLEEP_NS=1000"],
+    "k6_nomath": ["ORL_K6_EPI_NOMATH=1"],
 }
 OUT = os.path.join(ROOT, "build", "tune")
 
@@ -24,11 +30,13 @@ if sys.argv[1] == "build":
         list(ex.map(lambda n: build.build(force=True, defines=VARIANTS[n], out=os.path.join(OUT, f"liborl_{n}.so")), names))
     print("built", names)
 else:
-    for n in VARIANTS:
+    for n in (sys.argv[2:] or VARIANTS):
         so = os.path.join(OUT, f"liborl_{n}.so")
         if not os.path.exists(so):
             continue
         env = dict(os.environ, ORL_LIB_PATH=so)
-        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "k1_bench.py"), "--kinds", "logp,logp+H,loss"],
-                             env=env, capture_output=True, text=True)
+        cmd = [sys.executable, os.path.join(ROOT, "tools", "k1_bench.py"), "--kinds", "logp,logp+H,loss"]
+        if n.startswith("k6"):
+            cmd = [sys.executable, os.path.join(ROOT, "tools", "k6_bench.py"), "--reps", "300", "--no-baseline"]
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True)
         print(f"== {n}\n{out.stdout}{out.stderr[-500:] if out.returncode else ''}", flush=True)

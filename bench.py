@@ -40,6 +40,19 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def _bf16_peak(sustained: bool):
+    """Dense bf16 tensor peak in TFLOP/s: MEASURED_PEAKS.json (cuBLAS, burst or the
+    seconds-long power-capped loop), else the profiling guide's fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    key = "bf16_tflops_sustained" if sustained else "bf16_tflops"
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if key in d:
+            return float(d[key]), f"measured (MEASURED_PEAKS.json {key}, cuBLAS)"
+    return (1400.0, "fallback sustained (B200_PROFILING.md ~1.4 PFLOP/s under the power cap)") if sustained else \
+        (1590.0, "fallback burst (B200_PROFILING.md 1.59 PFLOP/s)")
+
+
 def _workload_desc(name, c, B, world):
     return (f"{name}: B={B}/rank T={c['T']} V={c['V']} {c['dtype']} logits x3 models resident in HBM, "
             f"adv={c['adv_kind']} gamma={c['gamma']} lambda={c['lam']} whiten={c['whiten']} "
@@ -317,6 +330,11 @@ def run_ours(args):
     if not args.no_next1 and world == 1 and not pooled:
         next1 = run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok_rank)
 
+    # ---- NEXT-4: the same iteration from final hidden states (LM head fused) ---
+    next4 = None
+    if args.next4 and world == 1 and not pooled:
+        next4 = run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok_rank)
+
     # ---- e2e: host buffers, H2D/D2H inside the timed region --------------------
     e2e = None
     if not args.no_e2e and not pooled:
@@ -346,7 +364,7 @@ def run_ours(args):
                                       "(full batch does not fit)" % (pool_mb, n_mb)) if pooled else "resident"},
                 "status": status, "stats": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in st.items()},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
-                "next1_logits_grad": next1,
+                "next1_logits_grad": next1, "next4_lmhead": next4,
                 "per_gpu_tokens_per_s": round(value / world, 1)}
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -415,6 +433,70 @@ def run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok):
             "fused_actor_pass": {"api": "orl_ppo_loss_and_grad", "tokens_per_s": round(n_tok / (ms_f / 1e3), 1),
                                  "ms": round(ms_f, 4),
                                  "algorithmic_GBps": round(byts / (ms_f / 1e3) / 1e9, 1)}}
+
+
+def run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok):
+    """NEXT-4 leg (not part of `value`): the whole iteration with every S1 pass computed
+    from the model's final hidden states through its LM head, [R, d] x [V, d]^T on the
+    tcgen05 tensor cores fused with the online log-sum-exp (K6, orl_lmhead_*), against
+    the unfused baseline: cuBLAS bf16 GEMM (torch.matmul) writing each micro-batch's
+    logits to HBM, then K1.  d = 4096 (Llama-3-8B hidden size)."""
+    from paper_2405_11143_b200 import synth
+    from paper_2405_11143_b200.pipeline import LmHeadRows, run_iteration
+
+    B, T, V, d = batch["tokens"].shape[0], c["T"], c["V"], args.hidden
+    R = B * T
+    g = torch.Generator(device=dev).manual_seed(synth.role_seed(4321, 30_000, 0))
+    # as synth.make_lmhead_batch: hidden_old = s_r N(0, I), ref = old + 0.05 N, new = old + 0.03 N
+    hid = {r: torch.empty(R, d, dtype=torch.bfloat16, device=dev) for r in synth.ROLES}
+    for s in range(0, R, 16384):
+        e = min(R, s + 16384)
+        base = torch.randn(e - s, d, generator=g, device=dev) * (torch.rand(e - s, 1, generator=g, device=dev) + 0.5)
+        for r, sd in zip(synth.ROLES, (0.0, 0.05, 0.03)):
+            hid[r][s:e] = (base + sd * torch.randn(e - s, d, generator=g, device=dev)).to(torch.bfloat16)
+    W = torch.empty(V, d, dtype=torch.bfloat16, device=dev)
+    for s in range(0, V, 8192):
+        e = min(V, s + 8192)
+        W[s:e] = (torch.randn(e - s, d, generator=g, device=dev) * (3.0 / d ** 0.5)).to(torch.bfloat16)
+    fused_src = lambda role, s, e: LmHeadRows(hid[role][s * T:e * T], W)  # noqa: E731
+    scratch = torch.empty(mb * T, V, dtype=torch.bfloat16, device=dev)
+
+    def unfused_src(role, s, e):
+        out = scratch[: (e - s) * T]
+        torch.matmul(hid[role][s * T:e * T], W.t(), out=out)
+        return out.view(e - s, T, V)
+
+    def timed(src, reps):
+        for _ in range(2):
+            run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            status, st = run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps, status, st
+
+    reps = max(2, args.steps // 5)
+    l0 = ctx.launch_count
+    ms_f, status, st = timed(fused_src, reps)
+    launches = (ctx.launch_count - l0) // (reps + 2)
+    ms_u, status_u, st_u = timed(unfused_src, reps)
+    flops = 3 * 2.0 * R * d * V
+    peak, peak_src = _bf16_peak(sustained=True)
+    ach = flops / (ms_f / 1e3) / 1e12
+    del hid, W, scratch
+    torch.cuda.empty_cache()
+    return {"tokens_per_s": round(n_tok / (ms_f / 1e3), 1), "ms_per_step": round(ms_f, 3), "status": status,
+            "hidden": d, "reps": reps, "gpu_launches": int(launches),
+            "policy_loss": round(st["policy_loss"], 6), "entropy": round(st["entropy"], 6),
+            "roofline": {"bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
+                         "frac": round(ach / peak, 4), "flops": "3 x 2 R d V per step (old, ref, actor heads)",
+                         "peak_source": peak_src, "kernel": "k6_lmhead_2sm_kernel + k6_merge_kernel (whole step)"},
+            "unfused_cublas_plus_k1": {"tokens_per_s": round(n_tok / (ms_u / 1e3), 1), "ms_per_step": round(ms_u, 3),
+                                       "status": status_u, "policy_loss": round(st_u["policy_loss"], 6)},
+            "speedup_vs_unfused": round(ms_u / ms_f, 4)}
 
 
 def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank):
@@ -509,6 +591,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-next1", action="store_true")
+    ap.add_argument("--next4", type=int, default=1, help="run the NEXT-4 LM-head leg (1/0)")
+    ap.add_argument("--hidden", type=int, default=4096, help="NEXT-4 hidden size d")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -158,6 +158,22 @@ __device__ int row_target(const K6Params &p, int64_t r) {
     return __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
 }
 
+// Work-unit order: groups of `grp` M units (CTA-pair row blocks, or M-tiles in the
+// 1-SM kernel) walk every vocab split before the next group starts; inside a group
+// the M unit varies fastest, so the units in flight share one or two W splits and
+// only the group's rows of h need to stay in L2.
+__device__ __forceinline__ uint64_t k6_policy(int which) {
+    return which == 1 ? l2_evict_last_policy() : which == 2 ? l2_evict_first_policy() : l2_evict_normal_policy();
+}
+__device__ __forceinline__ void unit_coords(int u, int m_units, int n_split, int grp, int &m, int &split) {
+    const int per_group = grp * n_split;
+    const int g = u / per_group;
+    const int rem = u - g * per_group;
+    const int gm = min(grp, m_units - g * grp);
+    split = rem / gm;
+    m = g * grp + (rem - split * gm);
+}
+
 // Persistent: one CTA per SM walks the work units u = blockIdx.x + k*gridDim.x,
 // unit u = (split u / m_tiles, M-tile u % m_tiles).  Consecutive units share the
 // vocab split, so the ~148 units in flight at any time touch only a few W
@@ -200,12 +216,13 @@ __global__ void __launch_bounds__(kThreads6, 1)
         if (lane == 0) {
             prefetch_tmap(&tmA);
             prefetch_tmap(&tmB);
-            const uint64_t pol_a = l2_evict_last_policy();    // h: re-read for every vocab tile
-            const uint64_t pol_b = l2_evict_normal_policy();  // W: shared by the concurrent M-tiles
+            const uint64_t pol_a = k6_policy(p.pol_a);  // h: re-read for every vocab tile
+            const uint64_t pol_b = k6_policy(p.pol_b);  // W: shared by the concurrent M units
             int stage = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                const int m_tile = u % p.m_tiles, split = u / p.m_tiles;
+                int m_tile, split;
+                unit_coords(u, p.m_tiles, p.n_split, p.m_group, m_tile, split);
                 const int t_end = min(p.n_tiles, (split + 1) * p.tiles_per_split);
                 for (int tile = split * p.tiles_per_split; tile < t_end; ++tile) {
                     for (int kb = 0; kb < kblocks; ++kb) {
@@ -224,7 +241,8 @@ __global__ void __launch_bounds__(kThreads6, 1)
             int stage = 0, i = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
-                const int split = u / p.m_tiles;
+                int m_tile_, split;
+                unit_coords(u, p.m_tiles, p.n_split, p.m_group, m_tile_, split);
                 const int nt = min(p.n_tiles, (split + 1) * p.tiles_per_split) - split * p.tiles_per_split;
                 for (int j = 0; j < nt; ++j, ++i) {
                     const int a = i & 1;
@@ -254,7 +272,8 @@ __global__ void __launch_bounds__(kThreads6, 1)
         const float c2 = p.c2;
         int i = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x) {
-            const int m_tile = u % p.m_tiles, split = u / p.m_tiles;
+            int m_tile, split;
+                unit_coords(u, p.m_tiles, p.n_split, p.m_group, m_tile, split);
             const int t_beg = split * p.tiles_per_split;
             const int nt = min(p.n_tiles, t_beg + p.tiles_per_split) - t_beg;
             const int64_t r = (int64_t)m_tile * kBM + row;
@@ -423,12 +442,13 @@ __global__ void __launch_bounds__(kThreads6, 1)
         if (lane == 0) {
             prefetch_tmap(&tmA);
             prefetch_tmap(&tmB);
-            const uint64_t pol_a = l2_evict_last_policy();
-            const uint64_t pol_b = l2_evict_normal_policy();
+            const uint64_t pol_a = k6_policy(p.pol_a);
+            const uint64_t pol_b = k6_policy(p.pol_b);
             int stage = 0;
             uint32_t phase = 0;
             for (int u = cluster; u < units; u += nclusters) {
-                const int pm = u % m_pairs, split = u / m_pairs;
+                int pm, split;
+                unit_coords(u, m_pairs, p.n_split, p.m_group, pm, split);
                 const int a_row = pm * 2 * kBM + (int)rank * kBM;
                 const int t_end = min(p.n_tiles, (split + 1) * p.tiles_per_split);
                 for (int tile = split * p.tiles_per_split; tile < t_end; ++tile) {
@@ -450,7 +470,8 @@ __global__ void __launch_bounds__(kThreads6, 1)
             int stage = 0, i = 0;
             uint32_t phase = 0;
             for (int u = cluster; u < units; u += nclusters) {
-                const int split = u / m_pairs;
+                int pm_, split;
+                unit_coords(u, m_pairs, p.n_split, p.m_group, pm_, split);
                 const int nt = min(p.n_tiles, (split + 1) * p.tiles_per_split) - split * p.tiles_per_split;
                 for (int j = 0; j < nt; ++j, ++i) {
                     const int a = i & 1;
@@ -480,7 +501,8 @@ __global__ void __launch_bounds__(kThreads6, 1)
         const uint32_t tempty0 = map_to_rank(&bars->tempty[0], 0), tempty1 = map_to_rank(&bars->tempty[1], 0);
         int i = 0;
         for (int u = cluster; u < units; u += nclusters) {
-            const int pm = u % m_pairs, split = u / m_pairs;
+            int pm, split;
+                unit_coords(u, m_pairs, p.n_split, p.m_group, pm, split);
             const int t_beg = split * p.tiles_per_split;
             const int nt = min(p.n_tiles, t_beg + p.tiles_per_split) - t_beg;
             const int64_t r = (int64_t)pm * 2 * kBM + (int64_t)rank * kBM + row;
@@ -589,6 +611,14 @@ void k6_plan(K6Params &p, int num_sms) {
     if (tps > p.n_tiles) tps = p.n_tiles;
     p.tiles_per_split = tps;
     p.n_split = (p.n_tiles + tps - 1) / tps;
+    const int m_units = p.two_sm ? (p.m_tiles + 1) / 2 : p.m_tiles;
+    p.m_group = m_units;  // default: one group (every row block in flight)
+    if (const char *e = getenv("ORL_K6_MGROUP")) p.m_group = atoi(e);
+    if (p.m_group < 1 || p.m_group > m_units) p.m_group = m_units;
+    p.pol_a = 1;  // h evict_last, W evict_normal
+    p.pol_b = 0;
+    if (const char *e = getenv("ORL_K6_POLA")) p.pol_a = atoi(e);
+    if (const char *e = getenv("ORL_K6_POLB")) p.pol_b = atoi(e);
     if (p.two_sm) {
         const int64_t units = (int64_t)((p.m_tiles + 1) / 2) * p.n_split;
         p.grid = 2 * (int)std::min<int64_t>(units, num_sms / 2);

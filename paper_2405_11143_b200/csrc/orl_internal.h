@@ -105,6 +105,8 @@ struct K6Params {
     int64_t R;          // hidden rows (TMA map height)
     int d, V;           // hidden size, vocabulary
     int m_tiles, n_tiles, tiles_per_split, n_split, grid, two_sm;  // filled by k6_plan
+    int m_group;        // M units (pairs / tiles) per schedule group (k6_plan)
+    int pol_a, pol_b;   // L2 policies of the h / W loads: 0 normal, 1 evict_last, 2 evict_first
     float c2;           // inv_temp * log2(e)
     int B, T;
     int64_t seq_offset;

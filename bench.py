@@ -271,6 +271,36 @@ def run_ours(args):
     def step(timing):
         return run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream, on_k1=hook if timing else None)
 
+    # C1/C2 transport at N > 1: the single-kernel peer-memory collectives (orl_peer_open)
+    # when every rank can map the others' exchange buffers, checked against the NCCL
+    # all-gather path on the first warm-up steps (statistics must be bit-identical).
+    coll = "local" if world == 1 else "nccl"
+    if world > 1 and args.collective == "peer":
+        why = ""
+        try:
+            ctx.enable_peer()
+            ok = 1.0
+        except Exception as exc:  # mapping failed on this rank
+            ok, why = 0.0, str(exc)[:80]
+        t = torch.tensor([ok], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if t.item() == 1.0:
+            try:
+                ctx.set_collective("nccl")
+                _, st_nccl = step(False)
+                ctx.set_collective("peer")
+                _, st_peer = step(False)
+                same = 1.0 if st_nccl == st_peer else 0.0
+                why = "" if same else "peer stats differed from NCCL"
+            except Exception as exc:
+                same, why = 0.0, str(exc)[:80]
+            t = torch.tensor([same], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if t.item() == 1.0:
+            coll = "peer (single-kernel C1/C2 over peer memory; stats bit-identical to NCCL in warm-up)"
+        else:
+            ctx.set_collective("nccl")
+            coll = f"nccl ({why or 'peer path unavailable on another rank'})"
     for _ in range(args.warmup):
         status, st = step(False)
     torch.cuda.synchronize()
@@ -280,13 +310,14 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     l0 = ctx.launch_count
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    t0, t1 = evs[0], evs[-1]
     t0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         status, st = step(True)
-    t1.record(stream)
+        evs[i + 1].record(stream)
     torch.cuda.synchronize()
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     if dist_mode:
         dist.barrier()
     torch.cuda.synchronize()
@@ -352,13 +383,22 @@ def run_ours(args):
         cpu = {"value": toks / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"first {n_seq} sequences x {T} tokens of the same rollout (3 x {n_seq * T} vocab rows), "
                          f"{dt:.1f} s wall"}
+        # the same oracle on one core, first sequence only (1-core and all-core)
+        toks1, dt1 = _oracle_sample(lambda role, n: host_logits[role][:n], {k: v[:1] for k, v in bnp.items()},
+                                    c, 1, 1)
+        cpu["single_core"] = {"value": toks1 / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"first sequence x {T} tokens (3 x {T} vocab rows), {dt1:.1f} s wall"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": round(ms, 4),
+                "ms_per_step_stats": {"mean": round(statistics.mean(per_step), 4),
+                                      "median": round(statistics.median(per_step), 4),
+                                      "min": round(min(per_step), 4), "max": round(max(per_step), 4),
+                                      "rank": "rank 0 (value uses the max over ranks of the mean)"}, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
                 "config": {"workload": _workload_desc(args.config, c, B, world), "global_batch": B * world,
-                           "seq_len": T, "vocab": V, "parallelism": f"dp{world}",
+                           "seq_len": T, "vocab": V, "parallelism": f"dp{world}", "collective": coll,
                            "l2": "inputs larger than L2 (3 x %.1f GB logits per rank vs 126 MB L2)" % (B * T * V * elt / 1e9),
                            "logits": ("pool of %d micro-batch buffers per model reused across the %d micro-batches "
                                       "(full batch does not fit)" % (pool_mb, n_mb)) if pooled else "resident"},
@@ -592,6 +632,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-next1", action="store_true")
     ap.add_argument("--next4", type=int, default=1, help="run the NEXT-4 LM-head leg (1/0)")
+    ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
+                    help="C1/C2 transport at N > 1 (peer: single peer-memory kernels, NCCL-checked)")
     ap.add_argument("--hidden", type=int, default=4096, help="NEXT-4 hidden size d")
     args = ap.parse_args()
     if args.warmup < 3:

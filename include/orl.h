@@ -183,9 +183,12 @@ orl_status orl_get_unique_id(unsigned char *id_out);
 /* Create a context on CUDA `device` for rank `rank` of `world` ranks.
  * world == 1: `id` may be NULL (no communicator; the collectives reduce to
  * local merges) or a unique id (a 1-rank NCCL communicator).  world > 1: `id`
- * (host, ORL_UNIQUE_ID_BYTES) from orl_get_unique_id; collective (all ranks
- * must call).  The context owns the NCCL communicator, fp64 partial buffers,
- * device error counters and a pinned host stats slot. */
+ * (host, ORL_UNIQUE_ID_BYTES) from orl_get_unique_id creates an NCCL
+ * communicator (collective: all ranks must call); with id == NULL the context
+ * has no communicator and orl_peer_open must be called before the first
+ * orl_whiten_stats (ORL_E_STATE otherwise).  The context owns the NCCL
+ * communicator, the peer exchange buffer, fp64 partial buffers, device error
+ * counters and a pinned host stats slot. */
 orl_status orl_create(int device, int world, int rank, const unsigned char *id, orl_ctx **out);
 
 /* Destroy a context (synchronises its device first).  NULL is a no-op. */
@@ -366,6 +369,36 @@ orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_lmh
                                const float *v_new, const float *v_old, float *logp_new,
                                float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
                                void *stream);
+
+/* ---- C1 / C2 as single kernels over peer memory (NVLink / NVSwitch) ---- */
+
+/* The two exchanges of the path (C1 = every rank's whitening
+ * partial before the actor pass; C2 = every rank's loss/stat partial,
+ * S:216) can run as ONE kernel each instead of local kernel + NCCL
+ * all-gather + merge kernel: the kernel forms the rank's partial, stores it
+ * into its slot of every rank's exchange buffer through peer (NVLink)
+ * mappings, publishes an epoch flag with a release store, waits until every
+ * rank's flag has arrived, and merges the slots in rank order (the same
+ * merge code as the NCCL path, so all ranks get bit-identical results, equal
+ * to the NCCL path's).  Setup, once per context, collective over the ranks:
+ *   orl_peer_handle  -> ORL_PEER_HANDLE_BYTES (host) naming this context's
+ *                       exchange buffer (a cudaIpcMemHandle_t); the caller
+ *                       all-gathers the handles (e.g. torch.distributed);
+ *   orl_peer_open    <- the world handles in rank order (host); maps the
+ *                       peers' buffers and switches C1/C2 to this transport.
+ * Requires world <= 8 (one NVLink domain; ORL_E_INVALID_ARG otherwise) and
+ * peer access between the ranks' devices (ORL_E_CUDA if a mapping fails; the
+ * context then keeps its NCCL transport).  A wait that exceeds the spin limit
+ * (env ORL_PEER_SPIN_LIMIT polls, default ~40 M) gives NaN statistics and
+ * orl_finalize returns ORL_E_NCCL. */
+#define ORL_PEER_HANDLE_BYTES 64
+orl_status orl_peer_handle(orl_ctx *ctx, unsigned char *handle_out);
+orl_status orl_peer_open(orl_ctx *ctx, const unsigned char *handles);
+/* Select the C1/C2 transport: 0 = NCCL all-gather (needs a communicator),
+ * 1 = peer-memory kernels (needs orl_peer_open).  world == 1 ignores it. */
+orl_status orl_set_collective(orl_ctx *ctx, int mode);
+/* Current transport (0 or 1), -1 for a NULL ctx. */
+int orl_get_collective(const orl_ctx *ctx);
 
 /* ---- NEXT-3: adaptive KL coefficient and early stop (host only) -------- */
 

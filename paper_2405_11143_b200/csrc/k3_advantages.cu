@@ -177,7 +177,9 @@ __device__ __forceinline__ void chan_merge(double &n, double &mean, double &M2, 
     n = nt;
 }
 
-__global__ void whiten_local_kernel(const double *seq_part, int B, double *slot) {
+// Rank-local whitening partial (n, mean, M2, sequences with L_b > 0) of the
+// per-sequence partials, 256 threads; thread 0 returns it in out[0..3].
+__device__ void whiten_local_block(const double *seq_part, int B, double *out) {
     __shared__ double sn[256], sm[256], s2[256], sc[256];
     const int tid = threadIdx.x;
     const int per = (B + 255) / 256;
@@ -200,9 +202,13 @@ __global__ void whiten_local_kernel(const double *seq_part, int B, double *slot)
         __syncthreads();
     }
     if (tid == 0) {
-        slot[0] = sn[0]; slot[1] = sm[0]; slot[2] = s2[0];
-        slot[3] = sc[0];   // sequences with L_b > 0
+        out[0] = sn[0]; out[1] = sm[0]; out[2] = s2[0];
+        out[3] = sc[0];   // sequences with L_b > 0
     }
+}
+
+__global__ void whiten_local_kernel(const double *seq_part, int B, double *slot) {
+    whiten_local_block(seq_part, B, slot);
 }
 
 cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_slot, cudaStream_t s) {
@@ -210,8 +216,8 @@ cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_sl
     return cudaGetLastError();
 }
 
-__global__ void whiten_merge_kernel(const double *gather, int world, int want, double *whiten,
-                                    double *flags) {
+// Rank-ordered Chan merge of the gathered [world][4] partials (one thread).
+__device__ void whiten_merge_body(const double *gather, int world, int want, double *whiten, double *flags) {
     double N = 0.0, mu = 0.0, M2 = 0.0, S = 0.0;
     for (int r = 0; r < world; ++r) {
         chan_merge(N, mu, M2, gather[4 * r], gather[4 * r + 1], gather[4 * r + 2]);
@@ -226,6 +232,11 @@ __global__ void whiten_merge_kernel(const double *gather, int world, int want, d
     flags[0] = (want && N < 2.0) ? 1.0 : 0.0;
 }
 
+__global__ void whiten_merge_kernel(const double *gather, int world, int want, double *whiten,
+                                    double *flags) {
+    whiten_merge_body(gather, world, want, whiten, flags);
+}
+
 cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten, double *whiten,
                                 double *flags, cudaStream_t s) {
     whiten_merge_kernel<<<1, 1, 0, s>>>(gather, world, want_whiten, whiten, flags);
@@ -233,13 +244,13 @@ cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten
 }
 
 // ---------------------------------------------------------------- statistics
+__device__ __forceinline__ double stats_pack_value(const double *acc, const unsigned long long *err, int k) {
+    return k < kNumPartials ? acc[k] : (k >= 16 && k <= 18) ? (double)err[k - 16] : 0.0;
+}
+
 __global__ void stats_pack_kernel(const double *acc, const unsigned long long *err, double *out) {
     const int k = threadIdx.x;
-    if (k < kNumPartials) out[k] = acc[k];
-    else if (k == 16) out[16] = (double)err[0];
-    else if (k == 17) out[17] = (double)err[1];
-    else if (k == 18) out[18] = (double)err[2];
-    else if (k < kStatsSlots) out[k] = 0.0;
+    if (k < kStatsSlots) out[k] = stats_pack_value(acc, err, k);
 }
 
 cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, double *out,
@@ -251,9 +262,9 @@ cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, 
 // S10: rank-ordered sum of the gathered partials, then the means.
 // loss_agg = 1 (NEXT-2, Z31): policy/value/entropy/kl are means over the N_seq
 // sequences of per-sequence token means; shares and ratio stay token means.
-__global__ void stats_final_kernel(const double *gather, int world, const double *whiten,
-                                   double *flags, double c1, double c2, double beta_loss,
-                                   int kl_in_loss, int loss_agg, double *st) {
+__device__ void stats_final_body(const double *gather, int world, const double *whiten,
+                                 double *flags, double c1, double c2, double beta_loss,
+                                 int kl_in_loss, int loss_agg, double *st) {
     double t[kStatsSlots];
     for (int k = 0; k < kStatsSlots; ++k) t[k] = 0.0;
     for (int r = 0; r < world; ++r)
@@ -280,11 +291,115 @@ __global__ void stats_final_kernel(const double *gather, int world, const double
     flags[1] = t[18];  // invalid lengths (ORL_E_MASK)
 }
 
+__global__ void stats_final_kernel(const double *gather, int world, const double *whiten,
+                                   double *flags, double c1, double c2, double beta_loss,
+                                   int kl_in_loss, int loss_agg, double *st) {
+    stats_final_body(gather, world, whiten, flags, c1, c2, beta_loss, kl_in_loss, loss_agg, st);
+}
+
 cudaError_t launch_stats_final(const double *gather, int world, const double *whiten,
                                const double *flags, double c1, double c2, double beta_loss,
                                int kl_in_loss, int loss_agg, double *stats_out, cudaStream_t s) {
     stats_final_kernel<<<1, 1, 0, s>>>(gather, world, whiten, const_cast<double *>(flags), c1, c2,
                                        beta_loss, kl_in_loss, loss_agg, stats_out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------- C1 / C2 over peer memory
+// Each collective is ONE kernel: the rank's partial is formed (S6: Chan merge of
+// the per-sequence moments; S10: the packed loss accumulators), stored into slot
+// [parity][rank] of every rank's exchange buffer over NVLink (plain 64-bit
+// stores to peer memory), published with a release store of the epoch into the
+// peer's flag [parity][rank]; the kernel then waits (acquire loads of its own
+// flags) until every rank's epoch has arrived and merges the slots in rank order
+// with the same code as the NCCL path -- every rank computes bit-identical
+// results.  Slots alternate by epoch parity: a rank can only write epoch e + 2
+// after all ranks published e + 1, i.e. after they finished reading epoch e.
+static_assert(kXS - kXW == 2 * kPeerMax * 4 && kXFW - kXS == 2 * kPeerMax * kStatsSlots, "exchange layout");
+
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Thread-0 exchange: push `n` words of `mine` to slot (par, rank) of every rank,
+// publish, wait for every rank, copy the world x n gathered words into `gath`
+// (rank-major).  Returns false on timeout (the missing slots read as NaN).
+__device__ bool peer_exchange(const PeerArgs &pa, int data_off, int flag_off, int n, const double *mine,
+                              double *gath) {
+    const int par = (int)(pa.epoch & 1ull);
+    const int slot = data_off + par * kPeerMax * n;
+    for (int r = 0; r < pa.world; ++r)
+        for (int k = 0; k < n; ++k)
+            st_relaxed_sys(pa.x[r] + slot + pa.rank * n + k, (unsigned long long)__double_as_longlong(mine[k]));
+    __threadfence_system();
+    for (int r = 0; r < pa.world; ++r) st_release_sys(pa.x[r] + flag_off + par * kPeerMax + pa.rank, pa.epoch);
+    bool ok = true;
+    const unsigned long long *own = pa.x[pa.rank];
+    for (int r = 0; r < pa.world; ++r) {
+        long long spins = 0;
+        bool arrived = true;
+        while (ld_acquire_sys(own + flag_off + par * kPeerMax + r) != pa.epoch) {
+            if (++spins > pa.spin_limit) { arrived = false; break; }
+            __nanosleep(256);
+        }
+        ok = ok && arrived;
+        for (int k = 0; k < n; ++k)
+            gath[r * n + k] = arrived ? __longlong_as_double((long long)ld_relaxed_sys(own + slot + r * n + k))
+                                      : __longlong_as_double(0x7ff8000000000000ll);
+    }
+    return ok;
+}
+
+__global__ void whiten_peer_kernel(const double *seq_part, int B, const PeerArgs pa, int want, double *whiten,
+                                   double *flags) {
+    __shared__ double mine[4];
+    __shared__ double gath[kPeerMax * 4];
+    whiten_local_block(seq_part, B, mine);
+    if (threadIdx.x == 0) {
+        const bool ok = peer_exchange(pa, kXW, kXFW, 4, mine, gath);
+        whiten_merge_body(gath, pa.world, want, whiten, flags);
+        if (!ok) flags[2] += 1.0;
+    }
+}
+
+cudaError_t launch_whiten_peer(const double *seq_part, int B, const PeerArgs &pa, int want, double *whiten,
+                               double *flags, cudaStream_t s) {
+    whiten_peer_kernel<<<1, 256, 0, s>>>(seq_part, B, pa, want, whiten, flags);
+    return cudaGetLastError();
+}
+
+__global__ void stats_peer_kernel(const double *acc, const unsigned long long *err, const PeerArgs pa,
+                                  const double *whiten, double *flags, double c1, double c2, double beta_loss,
+                                  int kl_in_loss, int loss_agg, double *st) {
+    __shared__ double mine[kStatsSlots];
+    __shared__ double gath[kPeerMax * kStatsSlots];
+    if (threadIdx.x < kStatsSlots) mine[threadIdx.x] = stats_pack_value(acc, err, threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const bool ok = peer_exchange(pa, kXS, kXFS, kStatsSlots, mine, gath);
+        stats_final_body(gath, pa.world, whiten, flags, c1, c2, beta_loss, kl_in_loss, loss_agg, st);
+        if (!ok) flags[2] += 1.0;
+    }
+}
+
+cudaError_t launch_stats_peer(const double *acc, const unsigned long long *err, const PeerArgs &pa,
+                              const double *whiten, double *flags, double c1, double c2, double beta_loss,
+                              int kl_in_loss, int loss_agg, double *stats_out, cudaStream_t s) {
+    stats_peer_kernel<<<1, 32, 0, s>>>(acc, err, pa, whiten, flags, c1, c2, beta_loss, kl_in_loss, loss_agg,
+                                       stats_out);
     return cudaGetLastError();
 }
 

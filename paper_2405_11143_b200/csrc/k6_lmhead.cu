@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(kThreads6, 1)
     }
     tc_fence_before();
     cluster_sync_all();
+    __syncthreads();  // CTA-scope order for the tmem_base read (racecheck does not model the cluster barrier)
     tc_fence_after();
     const uint32_t tmem_base = bars->tmem_base;
 

@@ -53,6 +53,11 @@ struct orl_ctx {
     int64_t cum_cap = 0;
     float4 *d_lm_parts = nullptr;      // NEXT-4 split partials
     int64_t lm_cap = 0;
+    unsigned long long *d_x = nullptr;  // C1/C2 peer exchange buffer [kXWords] (IPC-shared)
+    PeerArgs peer{};                    // every rank's exchange buffer, mapped here
+    bool peer_open = false;
+    int coll = 0;                       // 0 NCCL all-gather, 1 peer-memory kernels
+    unsigned long long epoch_w = 0, epoch_s = 0;
     bool have_adv = false, have_whiten = false;
     int imported_w = 0, imported_s = 0;
     uint64_t launches = 0;
@@ -220,7 +225,6 @@ extern "C" orl_status orl_create(int device, int world, int rank, const unsigned
     *out = nullptr;
     if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
         return fail(nullptr, ORL_E_INVALID_ARG, "world=%d rank=%d invalid", world, rank);
-    if (world > 1 && !id) return fail(nullptr, ORL_E_INVALID_ARG, "world > 1 needs a unique id");
     int ndev = 0;
     CUDA_TRY(nullptr, cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(nullptr, ORL_E_INVALID_ARG, "device %d of %d", device, ndev);
@@ -259,7 +263,7 @@ extern "C" orl_status orl_create(int device, int world, int rank, const unsigned
          cudaMemset(ctx->d_flags, 0, 4 * sizeof(double)) == cudaSuccess &&
          cudaDeviceSynchronize() == cudaSuccess;
     if (!ok) return cleanup_fail(fail(nullptr, ORL_E_CUDA, "device init failed"));
-    if (world > 1 || id) {  // world == 1 with an id: a 1-rank communicator (exercises the NCCL path)
+    if (id) {  // world == 1 with an id: a 1-rank communicator (exercises the NCCL path); no id: peer transport
         ncclUniqueId uid;
         std::memcpy(&uid, id, sizeof uid);
         ncclResult_t r = ncclCommInitRank(&ctx->comm, world, uid, rank);
@@ -275,6 +279,10 @@ extern "C" orl_status orl_destroy(orl_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->peer_open)
+        for (int r = 0; r < ctx->world; ++r)
+            if (r != ctx->rank && ctx->peer.x[r]) cudaIpcCloseMemHandle(ctx->peer.x[r]);
+    cudaFree(ctx->d_x);
     cudaFree(ctx->d_acc);
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_ws);
@@ -478,6 +486,17 @@ extern "C" orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream) {
     if (st) return st;
     cudaStream_t s = as_stream(stream);
     int world = ctx->world;
+    if (!ctx->imported_w && ctx->world > 1 && ctx->coll == 1) {  // C1 as one peer-memory kernel
+        PeerArgs pa = ctx->peer;
+        pa.epoch = ++ctx->epoch_w;
+        CUDA_TRY(ctx, launch_whiten_peer(ctx->d_seq_part, (int)ctx->adv_B, pa, whiten ? 1 : 0, ctx->d_whiten,
+                                         ctx->d_flags, s));
+        ctx->launches += 1;
+        ctx->have_whiten = true;
+        return ORL_OK;
+    }
+    if (!ctx->imported_w && ctx->world > 1 && !ctx->comm)
+        return fail(ctx, ORL_E_STATE, "world > 1 without a transport: create with a unique id or call orl_peer_open");
     if (ctx->imported_w) {
         world = ctx->imported_w;
     } else {
@@ -685,7 +704,15 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
     if (st) return st;
     cudaStream_t s = as_stream(stream);
     int world = ctx->world;
-    if (ctx->imported_s) {
+    if (!ctx->imported_s && ctx->world > 1 && ctx->coll == 0 && !ctx->comm)
+        return fail(ctx, ORL_E_STATE, "world > 1 without a transport: create with a unique id or call orl_peer_open");
+    if (!ctx->imported_s && ctx->world > 1 && ctx->coll == 1) {  // C2 as one peer-memory kernel
+        PeerArgs pa = ctx->peer;
+        pa.epoch = ++ctx->epoch_s;
+        CUDA_TRY(ctx, launch_stats_peer(ctx->d_acc, ctx->d_err, pa, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
+                                        cfg->beta_loss, cfg->kl_in_loss, cfg->loss_agg, ctx->d_stats, s));
+        ctx->launches += 1;
+    } else if (ctx->imported_s) {
         world = ctx->imported_s;
     } else {
         CUDA_TRY(ctx, launch_stats_pack(ctx->d_acc, ctx->d_err, ctx->d_gather_s + kStatsSlots * ctx->rank, s));
@@ -694,9 +721,11 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
             NCCL_TRY(ctx, ncclAllGather(ctx->d_gather_s + kStatsSlots * ctx->rank, ctx->d_gather_s,
                                         kStatsSlots, ncclDouble, ctx->comm, s));
     }
-    CUDA_TRY(ctx, launch_stats_final(ctx->d_gather_s, world, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
-                                     cfg->beta_loss, cfg->kl_in_loss, cfg->loss_agg, ctx->d_stats, s));
-    ctx->launches += 1;
+    if (!(ctx->world > 1 && ctx->coll == 1) || ctx->imported_s) {
+        CUDA_TRY(ctx, launch_stats_final(ctx->d_gather_s, world, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
+                                         cfg->beta_loss, cfg->kl_in_loss, cfg->loss_agg, ctx->d_stats, s));
+        ctx->launches += 1;
+    }
     ctx->imported_s = 0;
     if (dev_out)
         CUDA_TRY(ctx, cudaMemcpyAsync(dev_out, ctx->d_stats, kStatsOut * sizeof(double),
@@ -727,6 +756,9 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
         host_out->pad_ = 0;
     }
     const double mask_err = h[kStatsOut + 1];
+    if (h[kStatsOut + 2] > 0)
+        return fail(ctx, ORL_E_NCCL, "peer-memory collective: %lld wait(s) timed out (a rank did not arrive)",
+                    (long long)h[kStatsOut + 2]);
     if (h[14] > 0) return fail(ctx, ORL_E_TOKEN_RANGE, "%lld token(s) outside [0, V)", (long long)h[14]);
     if (mask_err > 0) return fail(ctx, ORL_E_MASK, "%lld invalid length(s)", (long long)mask_err);
     if (h[13] > 0) return fail(ctx, ORL_E_NONFINITE, "%lld non-finite value(s)", (long long)h[13]);
@@ -750,6 +782,72 @@ extern "C" orl_status orl_kl_controller_step(double *beta, double target, double
     *early_stop = observed_kl > max_kl ? 1 : 0;
     return ORL_OK;
 }
+
+// ------------------------------------------------------------------ peer-memory collectives
+extern "C" orl_status orl_peer_handle(orl_ctx *ctx, unsigned char *handle_out) {
+    if (!ctx || !handle_out) return fail(ctx, ORL_E_INVALID_ARG, "ctx/handle_out is NULL");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    if (!ctx->d_x) {
+        CUDA_TRY(ctx, cudaMalloc(&ctx->d_x, kXWords * sizeof(unsigned long long)));
+        CUDA_TRY(ctx, cudaMemset(ctx->d_x, 0, kXWords * sizeof(unsigned long long)));
+        CUDA_TRY(ctx, cudaDeviceSynchronize());
+    }
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(ctx, cudaIpcGetMemHandle(&h, ctx->d_x));
+    std::memcpy(handle_out, &h, sizeof h);
+    return ORL_OK;
+}
+
+extern "C" orl_status orl_peer_open(orl_ctx *ctx, const unsigned char *handles) {
+    if (!ctx || !handles) return fail(ctx, ORL_E_INVALID_ARG, "ctx/handles is NULL");
+    if (ctx->world > kPeerMax)
+        return fail(ctx, ORL_E_INVALID_ARG, "peer collectives need world <= %d (one NVLink domain)", kPeerMax);
+    if (!ctx->d_x) return fail(ctx, ORL_E_STATE, "orl_peer_open before orl_peer_handle");
+    if (ctx->peer_open) return fail(ctx, ORL_E_STATE, "peer buffers already open");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    PeerArgs pa{};
+    pa.world = ctx->world;
+    pa.rank = ctx->rank;
+    pa.spin_limit = 40ll << 20;
+    if (const char *e = getenv("ORL_PEER_SPIN_LIMIT")) pa.spin_limit = atoll(e);
+    for (int r = 0; r < ctx->world; ++r) {
+        if (r == ctx->rank) {
+            pa.x[r] = ctx->d_x;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + (size_t)r * sizeof h, sizeof h);
+        void *ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            for (int q = 0; q < r; ++q)
+                if (q != ctx->rank && pa.x[q]) cudaIpcCloseMemHandle(pa.x[q]);
+            return fail(ctx, ORL_E_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+        }
+        pa.x[r] = static_cast<unsigned long long *>(ptr);
+    }
+    ctx->peer = pa;
+    ctx->peer_open = true;
+    ctx->coll = ctx->world > 1 ? 1 : 0;
+    return ORL_OK;
+}
+
+extern "C" orl_status orl_set_collective(orl_ctx *ctx, int mode) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (mode == 0) {
+        if (ctx->world > 1 && !ctx->comm) return fail(ctx, ORL_E_STATE, "no NCCL communicator (created without an id)");
+    } else if (mode == 1) {
+        if (ctx->world > 1 && !ctx->peer_open) return fail(ctx, ORL_E_STATE, "peer buffers not open (orl_peer_open)");
+    } else {
+        return fail(ctx, ORL_E_INVALID_ARG, "collective mode %d not in {0, 1}", mode);
+    }
+    ctx->coll = mode;
+    return ORL_OK;
+}
+
+extern "C" int orl_get_collective(const orl_ctx *ctx) { return ctx ? ctx->coll : -1; }
 
 // ------------------------------------------------------------------ hooks
 extern "C" orl_status orl_export_partials(orl_ctx *ctx, int which, double *host_out, void *stream) {

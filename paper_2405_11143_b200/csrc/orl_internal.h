@@ -135,6 +135,26 @@ cudaError_t launch_k3(const K3Params &p, cudaStream_t s);
 
 // Whitening: merge per-sequence partials [B][3] in order into the rank partial
 // (count, mean, M2) -> gather[rank*4 ...].
+// ---- C1 / C2 over peer memory (one kernel each: local partial -> NVLink stores
+// into every rank's exchange buffer -> flag wait -> rank-ordered merge).
+constexpr int kPeerMax = 8;  // one NVLink/NVSwitch domain
+// exchange buffer (64-bit words), double-buffered by epoch parity:
+constexpr int kXW = 0;                                   // [2][kPeerMax][4]      whitening partials
+constexpr int kXS = kXW + 2 * kPeerMax * 4;              // [2][kPeerMax][24]     stats partials
+constexpr int kXFW = kXS + 2 * kPeerMax * 24;            // [2][kPeerMax]         C1 flags (= epoch)
+constexpr int kXFS = kXFW + 2 * kPeerMax;                // [2][kPeerMax]         C2 flags
+constexpr int kXWords = kXFS + 2 * kPeerMax;
+struct PeerArgs {
+    unsigned long long *x[kPeerMax];  // every rank's exchange buffer, mapped in this process
+    int world, rank;
+    unsigned long long epoch;         // > 0, identical sequence on every rank
+    long long spin_limit;             // polls before a wait gives up (flags[2] += 1)
+};
+cudaError_t launch_whiten_peer(const double *seq_part, int B, const PeerArgs &pa, int want, double *whiten,
+                               double *flags, cudaStream_t s);
+cudaError_t launch_stats_peer(const double *acc, const unsigned long long *err, const PeerArgs &pa,
+                              const double *whiten, double *flags, double c1, double c2, double beta_loss,
+                              int kl_in_loss, int loss_agg, double *stats_out, cudaStream_t s);
 cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_slot, cudaStream_t s);
 // Merge gathered [world][4] rank partials in rank order -> whiten[4] =
 // {N, mu, sigma, apply}; warn flag into flags[0].

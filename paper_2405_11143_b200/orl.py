@@ -23,6 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 UNIQUE_ID_BYTES = 128
 STATS_N = 16
+PEER_HANDLE_BYTES = 64
 PARTIALS_N = 24
 LOSS_AGG = {"token_mean": 0, "seq_mean_token_mean": 1}
 MAX_SEQ_PER_CALL = 8192
@@ -100,6 +101,11 @@ _lib.orl_lmhead_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Lm
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
+_lib.orl_peer_handle.argtypes = [_P, ctypes.c_char_p]
+_lib.orl_peer_open.argtypes = [_P, ctypes.c_char_p]
+_lib.orl_set_collective.argtypes = [_P, _I32]
+_lib.orl_get_collective.argtypes = [_P]
+_lib.orl_get_collective.restype = ctypes.c_int
 _lib.orl_kl_controller_step.argtypes = [ctypes.POINTER(_F64), _F64, _F64, _F64, _F64, ctypes.POINTER(ctypes.c_int)]
 for _f in ("orl_kl_controller_step", "orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
            "orl_advantages", "orl_whiten_stats", "orl_ppo_loss", "orl_finalize",
@@ -183,6 +189,43 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(_lib.orl_launch_count(self.h))
+
+    @property
+    def collective(self) -> str:
+        return {0: "nccl", 1: "peer"}.get(int(_lib.orl_get_collective(self.h)), "?")
+
+    def enable_peer(self, group=None):
+        """C1/C2 as peer-memory kernels: all-gather the exchange-buffer handles over
+        torch.distributed (`group`), then map them (collective over the ranks)."""
+        handles = exchange_peer_handles(orl_peer_handle(self), self.world, group)
+        orl_peer_open(self, handles)
+
+    def set_collective(self, mode: str):
+        self.check(_lib.orl_set_collective(self.h, {"nccl": 0, "peer": 1}[mode]))
+
+
+def orl_peer_handle(ctx: "Context") -> bytes:
+    buf = ctypes.create_string_buffer(PEER_HANDLE_BYTES)
+    ctx.check(_lib.orl_peer_handle(ctx.h, buf))
+    return buf.raw
+
+
+def orl_peer_open(ctx: "Context", handles) -> None:
+    blob = b"".join(handles)
+    if len(blob) != PEER_HANDLE_BYTES * ctx.world:
+        raise ValueError(f"need {ctx.world} handles of {PEER_HANDLE_BYTES} bytes")
+    ctx.check(_lib.orl_peer_open(ctx.h, blob))
+
+
+def exchange_peer_handles(mine: bytes, world: int, group=None) -> list:
+    """Rank-ordered list of every rank's handle (torch.distributed all_gather_object)."""
+    import torch.distributed as dist
+
+    out = [None] * world
+    dist.all_gather_object(out, mine, group=group)
+    if any(not isinstance(h, bytes) or len(h) != PEER_HANDLE_BYTES for h in out):
+        raise ValueError("malformed peer handle")
+    return out
 
 
 # ----------------------------------------------------------------------------- C-named calls

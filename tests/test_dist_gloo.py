@@ -116,3 +116,42 @@ def test_split_bounds_cover_and_align():
         assert max(sizes) - min(sizes) <= G
     with pytest.raises(ValueError):
         synth.split_bounds(10, 2, 4)
+
+
+def _peer_handle_worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2405_11143_b200 import orl
+        mine = bytes([rank]) * orl.PEER_HANDLE_BYTES         # stands in for a cudaIpcMemHandle_t
+        got = orl.exchange_peer_handles(mine, world)
+        bad = None
+        try:
+            orl.exchange_peer_handles(b"short", world)         # every rank sends a malformed one
+        except ValueError as ex:
+            bad = str(ex)
+        q.put((rank, got, bad))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc(), None))
+
+
+def test_peer_handle_exchange_rank_ordered():
+    """Host side of orl_peer_open's setup (orl.Context.enable_peer): the exchange-buffer
+    handles are all-gathered over torch.distributed in rank order, malformed ones rejected."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_handle_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    from paper_2405_11143_b200 import orl
+    for rank, got, bad in res:
+        assert isinstance(got, list), got
+        assert got == [bytes([r]) * orl.PEER_HANDLE_BYTES for r in range(world)]
+        assert bad and "malformed" in bad

@@ -206,6 +206,31 @@ def test_lmhead_full_size_sampled_rows(ctx):
     assert np.all(np.isfinite(g["logp"]))
 
 
+def test_lmhead_qwen_shape_ragged_sampled_rows(ctx):
+    """Qwen2.5-7B-shaped head (longcot config): d = 3584 (56 k-blocks), V = 152064
+    (594 vocab tiles, 149 splits with a 2-tile tail split), two T = 8192 responses
+    with a ragged second length (16,384 hidden rows, 64 CTA-pair row blocks); 16
+    sampled valid rows vs the oracle, masked rows exact zeros."""
+    B, T, d, V = 2, 8192, 3584, 152064
+    b = synth.make_lmhead_batch(19, B, T, d, V, lengths=[8192, 5000], device=DEV)
+    g = _run_logprobs(ctx, b)
+    L = b["lengths"].cpu().numpy()
+    mask = parity.valid_mask(L, T)
+    assert np.all(g["logp"][~mask] == 0.0) and np.all(g["entropy"][~mask] == 0.0)
+    rng = np.random.default_rng(1)
+    valid = np.flatnonzero(mask.reshape(-1))
+    rows = np.sort(rng.choice(valid, 16, replace=False))
+    rows[0], rows[-1] = valid[0], valid[-1]
+    hb = _bits(b["hidden_old"][torch.as_tensor(rows, device=DEV)])
+    Wb = _bits(b["weight"])
+    y = b["tokens"].reshape(-1).cpu().numpy()[rows]
+    o = oracle.lmhead_rows(hb, Wb, y, 1.0)
+    bound = _bound(hb, Wb, 1.0)
+    for k in ("logp", "entropy", "lse"):
+        err = np.abs(g[k].reshape(-1)[rows].astype(np.float64) - o[k])
+        assert np.all(err <= bound), (k, float(err.max()), float(bound.min()))
+
+
 def test_lmhead_token_range_and_mask_errors(ctx):
     B, T, d, V = 2, 16, 64, 300
     b = synth.make_lmhead_batch(16, B, T, d, V, lengths=[16, 9])

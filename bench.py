@@ -331,6 +331,11 @@ def run_ours(args):
     total_tokens = n_tok_rank * world
     value = total_tokens / (ms / 1e3)
 
+    # ---- the same step captured once as a CUDA graph and replayed ---------------
+    graph = None
+    if args.graph:
+        graph = run_graph(args, ctx, batch, cfg, bufs, src, mb, dev, stream, world, total_tokens, status, st)
+
     # ---- roofline of the dominant kernel (K1) --------------------------------
     side = {"old": 8, "ref": 8 + 12, "new": 8 + 24 + 16}   # side bytes per token (DESIGN 5.1)
     k1_ms = sum(a.elapsed_time(b) for _, _, a, b in events)
@@ -404,12 +409,45 @@ def run_ours(args):
                                       "(full batch does not fit)" % (pool_mb, n_mb)) if pooled else "resident"},
                 "status": status, "stats": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in st.items()},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
-                "next1_logits_grad": next1, "next4_lmhead": next4,
+                "next1_logits_grad": next1, "next4_lmhead": next4, "graph_replay": graph,
                 "per_gpu_tokens_per_s": round(value / world, 1)}
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist_mode:
         dist.destroy_process_group()
+
+
+def run_graph(args, ctx, batch, cfg, bufs, src, mb, dev, stream, world, total_tokens, status_eager, st_eager):
+    """The timed step (all S1..S10 launches, C1/C2 included) captured once into a CUDA
+    graph (pipeline.GraphStep, orl_finalize_async) and replayed K times; the replayed
+    statistics must equal the eager step's bit for bit."""
+    import torch.distributed as dist
+
+    from paper_2405_11143_b200.pipeline import GraphStep
+
+    step = GraphStep(ctx, batch, cfg, bufs, src, mb)
+    gs = torch.cuda.current_stream()
+    for _ in range(2):
+        step.replay()
+    torch.cuda.synchronize()
+    same = step.result() == (status_eager, st_eager)
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(gs)
+    for _ in range(args.steps):
+        step.replay()
+    b.record(gs)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    if dist.is_initialized():
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"tokens_per_s": round(total_tokens / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
+            "kernels_per_graph": int(step.kernels), "graph_launches_per_step": 1,
+            "stats_bit_identical_to_eager": bool(same), "steps": args.steps}
 
 
 def run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok):
@@ -635,6 +673,7 @@ def main():
     ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
                     help="C1/C2 transport at N > 1 (peer: single peer-memory kernels, NCCL-checked)")
     ap.add_argument("--hidden", type=int, default=4096, help="NEXT-4 hidden size d")
+    ap.add_argument("--graph", type=int, default=1, help="time the CUDA-graph replay of the step (1/0)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

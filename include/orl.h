@@ -313,6 +313,21 @@ orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits 
 orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
                         double *dev_out, void *stream);
 
+/* orl_finalize without the host synchronisation, for CUDA-graph capture of a whole
+ * iteration: launches C2 and the final statistics on `stream` and copies the
+ * device stats vector (double[ORL_STATS_N]) followed by the 4 device flags
+ * (whiten_warn, invalid lengths, collective timeouts, 0) into dev_out
+ * (device, double[ORL_FINAL_N], required).  No host memory is touched; the
+ * caller copies dev_out to the host when it needs it and maps it to a status
+ * with orl_stats_decode. */
+#define ORL_FINAL_N 20
+orl_status orl_finalize_async(orl_ctx *ctx, const orl_ppo_cfg *cfg, double *dev_out, void *stream);
+
+/* Host only: fill host_out (optional) from a host copy of orl_finalize_async's
+ * vector (double[ORL_FINAL_N]) and return the status orl_finalize would
+ * return (same priority; ratio_guard only enters the message). */
+orl_status orl_stats_decode(const double *final_vec, double ratio_guard, orl_stats *host_out);
+
 /* orl_ppo_loss and orl_logits_grad in one pass over the actor logits (NEXT-1,
  * fused): every row is streamed from HBM once for the loss epilogue (kept in L2
  * with an evict_last hint) and re-read from L2 one row later for the gradient,

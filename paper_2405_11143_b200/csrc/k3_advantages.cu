@@ -339,19 +339,20 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
 // (rank-major).  Returns false on timeout (the missing slots read as NaN).
 __device__ bool peer_exchange(const PeerArgs &pa, int data_off, int flag_off, int n, const double *mine,
                               double *gath) {
-    const int par = (int)(pa.epoch & 1ull);
+    const unsigned long long epoch = *pa.epoch + 1ull;  // same sequence on every rank
+    const int par = (int)(epoch & 1ull);
     const int slot = data_off + par * kPeerMax * n;
     for (int r = 0; r < pa.world; ++r)
         for (int k = 0; k < n; ++k)
             st_relaxed_sys(pa.x[r] + slot + pa.rank * n + k, (unsigned long long)__double_as_longlong(mine[k]));
     __threadfence_system();
-    for (int r = 0; r < pa.world; ++r) st_release_sys(pa.x[r] + flag_off + par * kPeerMax + pa.rank, pa.epoch);
+    for (int r = 0; r < pa.world; ++r) st_release_sys(pa.x[r] + flag_off + par * kPeerMax + pa.rank, epoch);
     bool ok = true;
     const unsigned long long *own = pa.x[pa.rank];
     for (int r = 0; r < pa.world; ++r) {
         long long spins = 0;
         bool arrived = true;
-        while (ld_acquire_sys(own + flag_off + par * kPeerMax + r) != pa.epoch) {
+        while (ld_acquire_sys(own + flag_off + par * kPeerMax + r) != epoch) {
             if (++spins > pa.spin_limit) { arrived = false; break; }
             __nanosleep(256);
         }
@@ -360,6 +361,7 @@ __device__ bool peer_exchange(const PeerArgs &pa, int data_off, int flag_off, in
             gath[r * n + k] = arrived ? __longlong_as_double((long long)ld_relaxed_sys(own + slot + r * n + k))
                                       : __longlong_as_double(0x7ff8000000000000ll);
     }
+    *pa.epoch = epoch;
     return ok;
 }
 

@@ -57,7 +57,7 @@ struct orl_ctx {
     PeerArgs peer{};                    // every rank's exchange buffer, mapped here
     bool peer_open = false;
     int coll = 0;                       // 0 NCCL all-gather, 1 peer-memory kernels
-    unsigned long long epoch_w = 0, epoch_s = 0;
+    unsigned long long *d_epoch = nullptr;  // [2] C1 / C2 peer epochs (device: graph-replay safe)
     bool have_adv = false, have_whiten = false;
     int imported_w = 0, imported_s = 0;
     uint64_t launches = 0;
@@ -283,6 +283,7 @@ extern "C" orl_status orl_destroy(orl_ctx *ctx) {
         for (int r = 0; r < ctx->world; ++r)
             if (r != ctx->rank && ctx->peer.x[r]) cudaIpcCloseMemHandle(ctx->peer.x[r]);
     cudaFree(ctx->d_x);
+    cudaFree(ctx->d_epoch);
     cudaFree(ctx->d_acc);
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_ws);
@@ -488,7 +489,7 @@ extern "C" orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream) {
     int world = ctx->world;
     if (!ctx->imported_w && ctx->world > 1 && ctx->coll == 1) {  // C1 as one peer-memory kernel
         PeerArgs pa = ctx->peer;
-        pa.epoch = ++ctx->epoch_w;
+        pa.epoch = ctx->d_epoch;
         CUDA_TRY(ctx, launch_whiten_peer(ctx->d_seq_part, (int)ctx->adv_B, pa, whiten ? 1 : 0, ctx->d_whiten,
                                          ctx->d_flags, s));
         ctx->launches += 1;
@@ -696,23 +697,21 @@ extern "C" orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const 
 }
 
 // ------------------------------------------------------------------ S10 + C2
-extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
-                                   double *dev_out, void *stream) {
-    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
-    if (!cfg) return fail(ctx, ORL_E_INVALID_ARG, "cfg is NULL");
-    orl_status st = set_device(ctx);
-    if (st) return st;
-    cudaStream_t s = as_stream(stream);
+// C2 and the final statistics on `s` (no copies, no host synchronisation).
+static orl_status finalize_launch(orl_ctx *ctx, const orl_ppo_cfg *cfg, cudaStream_t s) {
     int world = ctx->world;
     if (!ctx->imported_s && ctx->world > 1 && ctx->coll == 0 && !ctx->comm)
         return fail(ctx, ORL_E_STATE, "world > 1 without a transport: create with a unique id or call orl_peer_open");
     if (!ctx->imported_s && ctx->world > 1 && ctx->coll == 1) {  // C2 as one peer-memory kernel
         PeerArgs pa = ctx->peer;
-        pa.epoch = ++ctx->epoch_s;
+        pa.epoch = ctx->d_epoch + 1;
         CUDA_TRY(ctx, launch_stats_peer(ctx->d_acc, ctx->d_err, pa, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
                                         cfg->beta_loss, cfg->kl_in_loss, cfg->loss_agg, ctx->d_stats, s));
         ctx->launches += 1;
-    } else if (ctx->imported_s) {
+        ctx->imported_s = 0;
+        return ORL_OK;
+    }
+    if (ctx->imported_s) {
         world = ctx->imported_s;
     } else {
         CUDA_TRY(ctx, launch_stats_pack(ctx->d_acc, ctx->d_err, ctx->d_gather_s + kStatsSlots * ctx->rank, s));
@@ -721,21 +720,15 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
             NCCL_TRY(ctx, ncclAllGather(ctx->d_gather_s + kStatsSlots * ctx->rank, ctx->d_gather_s,
                                         kStatsSlots, ncclDouble, ctx->comm, s));
     }
-    if (!(ctx->world > 1 && ctx->coll == 1) || ctx->imported_s) {
-        CUDA_TRY(ctx, launch_stats_final(ctx->d_gather_s, world, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
-                                         cfg->beta_loss, cfg->kl_in_loss, cfg->loss_agg, ctx->d_stats, s));
-        ctx->launches += 1;
-    }
+    CUDA_TRY(ctx, launch_stats_final(ctx->d_gather_s, world, ctx->d_whiten, ctx->d_flags, cfg->c1, cfg->c2,
+                                     cfg->beta_loss, cfg->kl_in_loss, cfg->loss_agg, ctx->d_stats, s));
+    ctx->launches += 1;
     ctx->imported_s = 0;
-    if (dev_out)
-        CUDA_TRY(ctx, cudaMemcpyAsync(dev_out, ctx->d_stats, kStatsOut * sizeof(double),
-                                      cudaMemcpyDeviceToDevice, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, kStatsOut * sizeof(double),
-                                  cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats + kStatsOut, ctx->d_flags, 4 * sizeof(double),
-                                  cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(ctx, cudaStreamSynchronize(s));
-    const double *h = ctx->h_stats;
+    return ORL_OK;
+}
+
+extern "C" orl_status orl_stats_decode(const double *h, double ratio_guard, orl_stats *host_out) {
+    if (!h) return fail(nullptr, ORL_E_INVALID_ARG, "stats vector is NULL");
     if (host_out) {
         host_out->n_tokens = h[0];
         host_out->policy_loss = h[1];
@@ -757,16 +750,50 @@ extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_sta
     }
     const double mask_err = h[kStatsOut + 1];
     if (h[kStatsOut + 2] > 0)
-        return fail(ctx, ORL_E_NCCL, "peer-memory collective: %lld wait(s) timed out (a rank did not arrive)",
+        return fail(nullptr, ORL_E_NCCL, "peer-memory collective: %lld wait(s) timed out (a rank did not arrive)",
                     (long long)h[kStatsOut + 2]);
-    if (h[14] > 0) return fail(ctx, ORL_E_TOKEN_RANGE, "%lld token(s) outside [0, V)", (long long)h[14]);
-    if (mask_err > 0) return fail(ctx, ORL_E_MASK, "%lld invalid length(s)", (long long)mask_err);
-    if (h[13] > 0) return fail(ctx, ORL_E_NONFINITE, "%lld non-finite value(s)", (long long)h[13]);
+    if (h[14] > 0) return fail(nullptr, ORL_E_TOKEN_RANGE, "%lld token(s) outside [0, V)", (long long)h[14]);
+    if (mask_err > 0) return fail(nullptr, ORL_E_MASK, "%lld invalid length(s)", (long long)mask_err);
+    if (h[13] > 0) return fail(nullptr, ORL_E_NONFINITE, "%lld non-finite value(s)", (long long)h[13]);
     if (h[12] > 0)
-        return fail(ctx, ORL_E_NUMERIC_GUARD, "%lld token(s) with |logp_new - logp_old| > %g", (long long)h[12],
-                    cfg->ratio_guard);
-    if (!(h[0] > 0)) return fail(ctx, ORL_E_EMPTY_BATCH, "no valid tokens");
+        return fail(nullptr, ORL_E_NUMERIC_GUARD, "%lld token(s) with |logp_new - logp_old| > %g", (long long)h[12],
+                    ratio_guard);
+    if (!(h[0] > 0)) return fail(nullptr, ORL_E_EMPTY_BATCH, "no valid tokens");
     return ORL_OK;
+}
+
+extern "C" orl_status orl_finalize_async(orl_ctx *ctx, const orl_ppo_cfg *cfg, double *dev_out, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (!cfg || !dev_out) return fail(ctx, ORL_E_INVALID_ARG, "cfg/dev_out is NULL");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    if ((st = finalize_launch(ctx, cfg, s))) return st;
+    CUDA_TRY(ctx, cudaMemcpyAsync(dev_out, ctx->d_stats, kStatsOut * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(dev_out + kStatsOut, ctx->d_flags, 4 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  s));
+    return ORL_OK;
+}
+
+extern "C" orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
+                                   double *dev_out, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (!cfg) return fail(ctx, ORL_E_INVALID_ARG, "cfg is NULL");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    if ((st = finalize_launch(ctx, cfg, s))) return st;
+    if (dev_out)
+        CUDA_TRY(ctx, cudaMemcpyAsync(dev_out, ctx->d_stats, kStatsOut * sizeof(double),
+                                      cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, kStatsOut * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_stats + kStatsOut, ctx->d_flags, 4 * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    st = orl_stats_decode(ctx->h_stats, cfg->ratio_guard, host_out);
+    if (st) ctx->err = g_thread_err;
+    return st;
 }
 
 // ------------------------------------------------------------------ NEXT-3
@@ -791,6 +818,8 @@ extern "C" orl_status orl_peer_handle(orl_ctx *ctx, unsigned char *handle_out) {
     if (!ctx->d_x) {
         CUDA_TRY(ctx, cudaMalloc(&ctx->d_x, kXWords * sizeof(unsigned long long)));
         CUDA_TRY(ctx, cudaMemset(ctx->d_x, 0, kXWords * sizeof(unsigned long long)));
+        CUDA_TRY(ctx, cudaMalloc(&ctx->d_epoch, 2 * sizeof(unsigned long long)));
+        CUDA_TRY(ctx, cudaMemset(ctx->d_epoch, 0, 2 * sizeof(unsigned long long)));
         CUDA_TRY(ctx, cudaDeviceSynchronize());
     }
     cudaIpcMemHandle_t h;

@@ -147,7 +147,8 @@ constexpr int kXWords = kXFS + 2 * kPeerMax;
 struct PeerArgs {
     unsigned long long *x[kPeerMax];  // every rank's exchange buffer, mapped in this process
     int world, rank;
-    unsigned long long epoch;         // > 0, identical sequence on every rank
+    unsigned long long *epoch;        // device counter of this collective (C1: [0], C2: [1]); the
+                                      // kernel uses *epoch + 1 and stores it back (graph-replay safe)
     long long spin_limit;             // polls before a wait gives up (flags[2] += 1)
 };
 cudaError_t launch_whiten_peer(const double *seq_part, int B, const PeerArgs &pa, int want, double *whiten,

@@ -24,6 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 UNIQUE_ID_BYTES = 128
 STATS_N = 16
 PEER_HANDLE_BYTES = 64
+FINAL_N = 20
 PARTIALS_N = 24
 LOSS_AGG = {"token_mean": 0, "seq_mean_token_mean": 1}
 MAX_SEQ_PER_CALL = 8192
@@ -101,6 +102,8 @@ _lib.orl_lmhead_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Lm
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
+_lib.orl_finalize_async.argtypes = [_P, ctypes.POINTER(PpoCfg), _P, _P]
+_lib.orl_stats_decode.argtypes = [_P, _F64, ctypes.POINTER(Stats)]
 _lib.orl_peer_handle.argtypes = [_P, ctypes.c_char_p]
 _lib.orl_peer_open.argtypes = [_P, ctypes.c_char_p]
 _lib.orl_set_collective.argtypes = [_P, _I32]
@@ -391,6 +394,25 @@ def orl_finalize(ctx: Context, cfg: PPOConfig, dev_out=None, stream=None, raise_
     out, c = Stats(), cfg.c()
     st = _lib.orl_finalize(ctx.h, ctypes.byref(c), ctypes.byref(out), _ptr(dev_out), _stream(stream))
     ctx.check(st, allow=() if raise_on_data_error else DATA_ERRORS)
+    return STATUS[st], out.as_dict()
+
+
+def orl_finalize_async(ctx: Context, cfg: PPOConfig, dev_out, stream=None):
+    """S10 + C2 without a host sync (graph-capturable); dev_out: float64 [FINAL_N] on the device."""
+    if dev_out.dtype != torch.float64 or dev_out.numel() < FINAL_N or not dev_out.is_cuda:
+        raise ValueError(f"dev_out must be a float64 CUDA tensor of >= {FINAL_N} elements")
+    c = cfg.c()
+    ctx.check(_lib.orl_finalize_async(ctx.h, ctypes.byref(c), _ptr(dev_out), _stream(stream)))
+
+
+def orl_stats_decode(final_vec, cfg: PPOConfig):
+    """Host: (status_name, stats dict) from a host copy of orl_finalize_async's vector."""
+    import numpy as np
+    v = np.ascontiguousarray(np.asarray(final_vec, dtype=np.float64)[:FINAL_N])
+    out = Stats()
+    st = _lib.orl_stats_decode(v.ctypes.data_as(ctypes.c_void_p), float(cfg.ratio_guard), ctypes.byref(out))
+    if st and st not in DATA_ERRORS:
+        raise OrlError(st, _lib.orl_last_error(None).decode())
     return STATUS[st], out.as_dict()
 
 

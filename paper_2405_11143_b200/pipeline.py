@@ -58,6 +58,7 @@ class Buffers:
         self.dv = f() if grads else None
         self.keep = torch.zeros(max(1, B // max(1, group_size)), dtype=torch.uint8, device=device)
         self.stats_dev = torch.zeros(_orl.STATS_N, dtype=torch.float64, device=device)
+        self.final_dev = torch.zeros(_orl.FINAL_N, dtype=torch.float64, device=device)  # orl_finalize_async
 
 
 class LmHeadRows(NamedTuple):
@@ -133,9 +134,7 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
                                        lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
                                        dlogits=grad_sink(s, e), stream=stream)
             if h: h()
-        if not finalize:
-            return None
-        return _orl.orl_finalize(ctx, cfg.ppo, dev_out=bufs.stats_dev, stream=stream)
+        return _finish(ctx, cfg, bufs, stream, finalize)
     for s, e in mbs:                                   # S1 + S7..S9, actor
         h = hook("new")
         src = logits("new", s, e)
@@ -155,6 +154,46 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
             _orl.orl_logits_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.lse, bufs.entropy, bufs.dlogp,
                                  grad_sink(s, e), seq_offset=s, inv_temp=cfg.inv_temp, stream=stream)
             if h: h()
+    return _finish(ctx, cfg, bufs, stream, finalize)                       # S10 + C2
+
+
+def _finish(ctx, cfg, bufs, stream, finalize):
+    """finalize=True: orl_finalize (synchronises, returns (status, stats)); "async":
+    orl_finalize_async into bufs.final_dev (no host sync, graph-capturable; decode later
+    with orl_stats_decode); False: nothing."""
+    if finalize == "async":
+        _orl.orl_finalize_async(ctx, cfg.ppo, bufs.final_dev, stream=stream)
+        return None
     if not finalize:
         return None
-    return _orl.orl_finalize(ctx, cfg.ppo, dev_out=bufs.stats_dev, stream=stream)  # S10 + C2
+    return _orl.orl_finalize(ctx, cfg.ppo, dev_out=bufs.stats_dev, stream=stream)
+
+
+class GraphStep:
+    """A whole iteration (every launch of run_iteration, C1/C2 included) captured once
+    into a CUDA graph and replayed with a single launch.  The logits source must return
+    the same (resident) tensors every time; their contents may change between replays.
+    The statistics land in bufs.final_dev; result() copies them to the host and decodes."""
+
+    def __init__(self, ctx, batch: dict, cfg: PathConfig, bufs: Buffers, logits: LogitsSource, mb: int,
+                 warmup: int = 1):
+        self.ctx, self.cfg, self.bufs = ctx, cfg, bufs
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):                   # eager warm-up sizes every workspace
+            for _ in range(max(1, warmup)):
+                run_iteration(ctx, batch, cfg, bufs, logits, mb, stream=side, finalize="async")
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        l0 = ctx.launch_count
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            run_iteration(ctx, batch, cfg, bufs, logits, mb, stream=torch.cuda.current_stream(),
+                          finalize="async")
+        self.kernels = ctx.launch_count - l0           # liborl kernels inside the graph
+
+    def replay(self):
+        self.graph.replay()
+
+    def result(self):
+        return _orl.orl_stats_decode(self.bufs.final_dev.cpu().numpy(), self.cfg.ppo)

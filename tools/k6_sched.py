@@ -24,6 +24,7 @@ ap.add_argument("--warm", type=int, default=3)
 ap.add_argument("--mgroup", default="32,16,8,4")
 ap.add_argument("--tps", default="4,8")
 ap.add_argument("--pola", default="1,0")
+ap.add_argument("--polb", default="0")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 B, T = a.R // a.T, a.T
@@ -36,8 +37,9 @@ H = torch.zeros(B, T, device=dev)
 flops = 2.0 * a.R * a.d * a.V
 orl.orl_begin_iteration(ctx)
 ref = None
-for mg, tps, pa in itertools.product(a.mgroup.split(","), a.tps.split(","), a.pola.split(",")):
-    os.environ.update(ORL_K6_MGROUP=mg, ORL_K6_TPS=tps, ORL_K6_POLA=pa)
+for mg, tps, pa, pb in itertools.product(a.mgroup.split(","), a.tps.split(","), a.pola.split(","),
+                                         a.polb.split(",")):
+    os.environ.update(ORL_K6_MGROUP=mg, ORL_K6_TPS=tps, ORL_K6_POLA=pa, ORL_K6_POLB=pb)
     fn = lambda: orl.orl_lmhead_logprobs(ctx, tok, L, h, W, logp, entropy=H)  # noqa: E731
     for _ in range(a.warm):
         fn()
@@ -54,5 +56,5 @@ for mg, tps, pa in itertools.product(a.mgroup.split(","), a.tps.split(","), a.po
         ref = logp.clone()
     else:
         same = bool(torch.equal(ref, logp))
-    print(json.dumps({"mgroup": int(mg), "tps": int(tps), "pol_a": int(pa), "ms": round(ms, 4),
+    print(json.dumps({"mgroup": int(mg), "tps": int(tps), "pol_a": int(pa), "pol_b": int(pb), "ms": round(ms, 4),
                       "tflops": round(flops / ms / 1e9, 1), "bit_identical_to_first": same}), flush=True)

@@ -153,12 +153,15 @@ def run_reference(args):
     from paper_2405_11143_b200 import synth
 
     c = dict(synth.CONFIGS[args.config])
-    n_seq = args.ref_seqs
     T, V = c["T"], c["V"]
+    G = max(1, c["group_size"])
+    n_seq = max(G, (args.ref_seqs // G) * G)               # whole groups (GRPO)
+    cap = min(T, -(-(args.ref_seqs * min(T, 1024)) // n_seq))  # ~ref_seqs x 1024 valid tokens per step
     cores = len(os.sched_getaffinity(0))
     dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
-    batch = synth.make_batch(1234, n_seq, T, V, c["dtype"], "realistic", "full", c["rewards"], c["group_size"],
-                             device=dev)
+    # only the first `cap` positions of each response are in the sample: generate [n_seq, cap, V]
+    batch = synth.make_batch(1234, n_seq, cap, V, c["dtype"], "realistic", "full", c["rewards"],
+                             c["group_size"], device=dev)
     bnp = synth.batch_to_numpy(batch)
     fn = lambda role, n: bnp[f"logits_{role}"][:n]  # noqa: E731
     times, toks = [], 0
@@ -168,7 +171,8 @@ def run_reference(args):
             times.append(dt)
     mean = sum(times) / len(times)
     val = toks / mean
-    sample = f"first {n_seq} sequences x {T} tokens of {args.config} (3 x {n_seq * T} vocab rows), per step"
+    sample = (f"{n_seq} sequences of {args.config} with lengths capped at {cap} ({toks} tokens, 3 x {toks} "
+              f"vocab rows of V={V}), per step")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -379,20 +383,29 @@ def run_ours(args):
     # ---- oracle on the host cores (rank 0, N = 1 only) ------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        n_seq = args.ref_seqs
         cores = len(os.sched_getaffinity(0))
-        n_seq = min(n_seq, mb) if pooled else n_seq
-        bnp = {k: v[:n_seq].detach().cpu().numpy() for k, v in batch.items()}
-        host_logits = {r: synth.to_numpy_logits(src(r, 0, n_seq)) for r in synth.ROLES}
-        toks, dt = _oracle_sample(lambda role, n: host_logits[role][:n], bnp, c, n_seq, cores)
-        cpu = {"value": toks / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"first {n_seq} sequences x {T} tokens of the same rollout (3 x {n_seq * T} vocab rows), "
-                         f"{dt:.1f} s wall"}
-        # the same oracle on one core, first sequence only (1-core and all-core)
-        toks1, dt1 = _oracle_sample(lambda role, n: host_logits[role][:n], {k: v[:1] for k, v in bnp.items()},
-                                    c, 1, 1)
-        cpu["single_core"] = {"value": toks1 / dt1, "unit": UNIT, "cores": 1,
-                              "sample": f"first sequence x {T} tokens (3 x {T} vocab rows), {dt1:.1f} s wall"}
+        G = max(1, c["group_size"])
+
+        def sample(n_want, tok_cap, ncores):
+            """Whole groups of the first sequences, lengths capped so the sample holds
+            about tok_cap valid tokens (the oracle's per-token cost is the 3 V-long rows)."""
+            n = max(G, (n_want // G) * G)
+            n = min(n, mb) if pooled else n
+            n = max(G, (n // G) * G)
+            bnp = {k: v[:n].detach().cpu().numpy() for k, v in batch.items()}
+            cap = max(1, -(-tok_cap // n))
+            bnp["lengths"] = np.minimum(bnp["lengths"], cap).astype(np.int32)
+            hl = {r: synth.to_numpy_logits(src(r, 0, n)) for r in synth.ROLES}
+            toks, dt = _oracle_sample(lambda role, k: hl[role][:k], bnp, c, n, ncores)
+            desc = (f"first {n} sequences of the same rollout, lengths capped at {min(cap, T)} "
+                    f"({toks} tokens, 3 x {toks} vocab rows), {dt:.1f} s wall")
+            return toks / dt, desc
+
+        v_all, d_all = sample(args.ref_seqs, args.ref_seqs * min(T, 1024), cores)
+        cpu = {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": d_all}
+        # the same oracle on one core (SURVEY 8(d): 1-core and all-core)
+        v_one, d_one = sample(1, 1024, 1)
+        cpu["single_core"] = {"value": v_one, "unit": UNIT, "cores": 1, "sample": d_one}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,

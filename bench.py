@@ -193,12 +193,21 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ORL_BENCH_SHARED_GPU=1 (functional test of the N > 1 code path on a one-GPU box; its
+    # timings are not measurements): every rank on cuda:0, gloo process group, no NCCL
+    # communicator (two ranks cannot share a GPU in NCCL), C1/C2 over the peer kernels.
+    shared = os.environ.get("ORL_BENCH_SHARED_GPU") == "1" and world > 1
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     # under torchrun (even with one rank) use the distributed plumbing: NCCL process
     # group, unique-id broadcast, liborl NCCL communicator, barriers, max over ranks
     dist_mode = "WORLD_SIZE" in os.environ
-    if dist_mode:
+    if shared:
+        dist.init_process_group("gloo")
+        ctx = orl.Context(local, world, rank, None)
+    elif dist_mode:
         dist.init_process_group("nccl", device_id=dev)
         uid = [orl.orl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -279,7 +288,10 @@ def run_ours(args):
     # when every rank can map the others' exchange buffers, checked against the NCCL
     # all-gather path on the first warm-up steps (statistics must be bit-identical).
     coll = "local" if world == 1 else "nccl"
-    if world > 1 and args.collective == "peer":
+    if shared:
+        ctx.enable_peer()
+        coll = "peer (shared-GPU functional test: no NCCL reference)"
+    elif world > 1 and args.collective == "peer":
         why = ""
         try:
             ctx.enable_peer()
@@ -424,6 +436,8 @@ def run_ours(args):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
                 "next1_logits_grad": next1, "next4_lmhead": next4, "graph_replay": graph,
                 "per_gpu_tokens_per_s": round(value / world, 1)}
+        if shared:
+            line["test_mode"] = "ORL_BENCH_SHARED_GPU: all ranks on one GPU (functional test, not a measurement)"
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist_mode:

@@ -367,8 +367,9 @@ def run_ours(args):
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("V") == V and pj.get("T") == T and pj.get("mb") == mb:
-                traffic = pj["dram_bytes_per_launch"]
+            for e in pj.get("configs", [pj]):   # one ncu capture per (V, T, micro-batch) shape
+                if e.get("V") == V and e.get("T") == T and e.get("mb") == mb:
+                    traffic = e["dram_bytes_per_launch"]
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -592,7 +592,9 @@ def run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok):
     flops = 3 * 2.0 * R * d * V
     peak, peak_src = _bf16_peak(sustained=True)
     ach = flops / (ms_f / 1e3) / 1e12
-    del hid, W, scratch
+    del scratch
+    e2e = None if args.no_e2e else _next4_e2e(ctx, cfg, batch, bufs, mb, hid, W, T, n_tok, reps)
+    del hid, W
     torch.cuda.empty_cache()
     return {"tokens_per_s": round(n_tok / (ms_f / 1e3), 1), "ms_per_step": round(ms_f, 3), "status": status,
             "hidden": d, "reps": reps, "gpu_launches": int(launches),
@@ -602,7 +604,81 @@ def run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok):
                          "peak_source": peak_src, "kernel": "k6_lmhead_2sm_kernel + k6_merge_kernel (whole step)"},
             "unfused_cublas_plus_k1": {"tokens_per_s": round(n_tok / (ms_u / 1e3), 1), "ms_per_step": round(ms_u, 3),
                                        "status": status_u, "policy_loss": round(st_u["policy_loss"], 6)},
-            "speedup_vs_unfused": round(ms_u / ms_f, 4)}
+            "speedup_vs_unfused": round(ms_u / ms_f, 4), "e2e_from_host_hidden_states": e2e}
+
+
+def _next4_e2e(ctx, cfg, batch, bufs, mb, hid, W, T, n_tok, steps):
+    """NEXT-4 end to end through the public API with the step's inputs in pinned HOST
+    memory: every step copies the LM-head weight and each micro-batch's final hidden
+    states of the three roles host -> device (double-buffered on a copy stream, the
+    copies overlapping the tensor-core work) plus the per-token inputs, and
+    orl_finalize reads the statistics back and synchronises (host clock)."""
+    from paper_2405_11143_b200.pipeline import LmHeadRows, run_iteration
+
+    B = batch["tokens"].shape[0]
+    hh = {r: v.cpu().pin_memory() for r, v in hid.items()}
+    hW = W.cpu().pin_memory()
+    small = {k: v.cpu().pin_memory() for k, v in batch.items()}
+    dW = torch.empty_like(W)
+    stage = [torch.empty(mb * T, W.shape[1], dtype=W.dtype, device=W.device) for _ in range(2)]
+    dbatch = {k: torch.empty_like(v) for k, v in batch.items()}
+    comp, copy = torch.cuda.current_stream(), torch.cuda.Stream()
+    order = [(r, s) for r in ("old", "ref", "new") for s in range(0, B, mb)]
+    h2d = sum(v.numel() * v.element_size() for v in small.values()) + hW.numel() * hW.element_size()
+    h2d += sum(v.numel() * v.element_size() for v in hh.values())
+
+    def one_step():
+        for k, v in small.items():
+            dbatch[k].copy_(v, non_blocking=True)
+        with torch.cuda.stream(copy):
+            dW.copy_(hW, non_blocking=True)
+            ew = torch.cuda.Event()
+            ew.record(copy)
+        slot_free, pending, counter = [None, None], {}, {"i": 0}
+
+        def fetch(i):
+            r, s = order[i]
+            e = min(B, s + mb)
+            with torch.cuda.stream(copy):
+                if slot_free[i % 2] is not None:
+                    copy.wait_event(slot_free[i % 2])
+                stage[i % 2][: (e - s) * T].copy_(hh[r][s * T:e * T], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            pending[i] = ev
+
+        def src(role, s, e):
+            i = counter["i"]
+            counter["i"] += 1
+            if i == 0:
+                comp.wait_event(ew)
+            comp.wait_event(pending.pop(i))
+            if i + 1 < len(order):
+                fetch(i + 1)
+            return LmHeadRows(stage[i % 2][: (e - s) * T], dW)
+
+        def hook(tag):
+            def after():
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                slot_free[(counter["i"] - 1) % 2] = ev
+            return after
+
+        fetch(0)
+        return run_iteration(ctx, dbatch, cfg, bufs, src, mb, stream=comp, on_k1=hook)
+
+    one_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        status, _ = one_step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    del hh, hW, dW, stage
+    return {"value": round(n_tok / dt, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": 16 * 8 + 4 * 8, "steps": steps, "status": status,
+            "note": "final hidden states (3 roles) + LM-head weight streamed from pinned host memory each step; "
+                    "host clock"}
 
 
 def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank):

@@ -17,6 +17,10 @@
  *   orl_whiten_stats                             S6 + collective C1
  *   for each micro-batch: orl_ppo_loss           S1+S7+S8+S9
  *   orl_finalize                                 S10 + collective C2
+ * C1/C2 run over NCCL or, after orl_peer_open, as single peer-memory kernels;
+ * orl_finalize_async + orl_stats_decode split S10 for CUDA-graph capture;
+ * NEXT-1 (orl_logits_grad, orl_ppo_loss_and_grad), NEXT-3
+ * (orl_kl_controller_step) and NEXT-4 (orl_lmhead_*) are declared below.
  *
  * Conventions shared by every call
  *  - Pointers are DEVICE pointers on the context's device unless a comment

@@ -19,6 +19,11 @@ VARIANTS = {
     "k6_epi20k": ["ORL_K6_EPI_SLEEP_NS=20000"],
     "k6_epi20k_prod1k": ["ORL_K6_EPI_SLEEP_NS=20000", "ORL_K6_PROD_SLEEP_NS=1000"],
     "k6_nomath": ["ORL_K6_EPI_NOMATH=1"],
+    # K1 launch shapes for the power-capped (sustained) regime
+    "cw8": ["ORL_K1_CONSUMER_WARPS=8"],
+    "cw8_c16k": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=16384", "ORL_K1_STAGES=12"],
+    "cw8_mb2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_MINBLOCKS=2", "ORL_K1_STAGES=3"],
+    "s4": ["ORL_K1_STAGES=4"],
 }
 OUT = os.path.join(ROOT, "build", "tune")
 

@@ -205,6 +205,16 @@ const char *orl_last_error(const orl_ctx *ctx);
 /* Number of kernels the context has launched so far (for bench accounting). */
 uint64_t orl_launch_count(const orl_ctx *ctx);
 
+/* Pre-size the context's workspaces (host call, synchronises the device):
+ * per-sequence whitening partials and the length prefix for up to max_seqs
+ * responses per rank-local batch / call, and the NEXT-4 split partials for
+ * LM-head calls of up to max_lm_rows hidden rows at vocabulary max_vocab (0:
+ * none).  Calls within these sizes then never allocate, which is what CUDA-graph
+ * capture of an iteration needs (otherwise the first call of each size
+ * allocates; capture after one eager warm-up iteration).  Sizes < 0:
+ * ORL_E_SHAPE. */
+orl_status orl_reserve(orl_ctx *ctx, int64_t max_seqs, int64_t max_lm_rows, int64_t max_vocab);
+
 /* Start an iteration: zero the loss accumulators, error counters and
  * advantage partials on `stream`. */
 orl_status orl_begin_iteration(orl_ctx *ctx, void *stream);

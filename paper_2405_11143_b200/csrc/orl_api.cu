@@ -810,6 +810,47 @@ extern "C" orl_status orl_kl_controller_step(double *beta, double target, double
     return ORL_OK;
 }
 
+// ------------------------------------------------------------------ workspace
+extern "C" orl_status orl_reserve(orl_ctx *ctx, int64_t max_seqs, int64_t max_lm_rows, int64_t max_vocab) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (max_seqs < 0 || max_lm_rows < 0 || max_vocab < 0)
+        return fail(ctx, ORL_E_SHAPE, "orl_reserve: negative size");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    if (max_seqs > ctx->seq_cap) {
+        cudaFree(ctx->d_seq_part);
+        ctx->d_seq_part = nullptr;
+        ctx->seq_cap = 0;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->d_seq_part, (size_t)max_seqs * 3 * sizeof(double)));
+        ctx->seq_cap = max_seqs;
+    }
+    if (max_seqs > kSmemPrefixMax && max_seqs > ctx->cum_cap) {
+        cudaFree(ctx->d_cum);
+        ctx->d_cum = nullptr;
+        ctx->cum_cap = 0;
+        CUDA_TRY(ctx, cudaMalloc(&ctx->d_cum, (size_t)max_seqs * sizeof(int32_t)));
+        ctx->cum_cap = max_seqs;
+    }
+    if (max_lm_rows > 0 && max_vocab > 0) {
+        K6Params q;
+        std::memset(&q, 0, sizeof q);
+        q.R = max_lm_rows;
+        q.V = (int)max_vocab;
+        q.d = 64;
+        k6_plan(q, ctx->num_sms);
+        const int64_t need = (int64_t)q.n_split * q.R;
+        if (need > ctx->lm_cap) {
+            cudaFree(ctx->d_lm_parts);
+            ctx->d_lm_parts = nullptr;
+            ctx->lm_cap = 0;
+            CUDA_TRY(ctx, cudaMalloc(&ctx->d_lm_parts, (size_t)need * sizeof(float4)));
+            ctx->lm_cap = need;
+        }
+    }
+    CUDA_TRY(ctx, cudaDeviceSynchronize());
+    return ORL_OK;
+}
+
 // ------------------------------------------------------------------ peer-memory collectives
 extern "C" orl_status orl_peer_handle(orl_ctx *ctx, unsigned char *handle_out) {
     if (!ctx || !handle_out) return fail(ctx, ORL_E_INVALID_ARG, "ctx/handle_out is NULL");

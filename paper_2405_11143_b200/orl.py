@@ -102,6 +102,7 @@ _lib.orl_lmhead_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Lm
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
+_lib.orl_reserve.argtypes = [_P, _I64, _I64, _I64]
 _lib.orl_finalize_async.argtypes = [_P, ctypes.POINTER(PpoCfg), _P, _P]
 _lib.orl_stats_decode.argtypes = [_P, _F64, ctypes.POINTER(Stats)]
 _lib.orl_peer_handle.argtypes = [_P, ctypes.c_char_p]
@@ -249,6 +250,11 @@ def _logits(x):
     if x.dim() != 3 or x.stride(2) != 1:
         raise ValueError("logits must be a [B,T,V] view with unit stride along V")
     return Logits(x.data_ptr(), DTYPE[x.dtype], 0, x.shape[2], x.stride(0), x.stride(1))
+
+
+def orl_reserve(ctx: Context, max_seqs: int, max_lm_rows: int = 0, max_vocab: int = 0):
+    """Pre-size the workspaces so later calls within these sizes never allocate."""
+    return ctx.check(_lib.orl_reserve(ctx.h, int(max_seqs), int(max_lm_rows), int(max_vocab)))
 
 
 def orl_begin_iteration(ctx: Context, stream=None):

@@ -88,3 +88,30 @@ def test_finalize_async_decode_matches_finalize():
     with pytest.raises(ValueError):
         orl.orl_finalize_async(ctx, cfg.ppo, torch.zeros(4, dtype=torch.float64, device=DEV))
     ctx.close()
+
+
+def test_reserve_then_strict_capture_without_warmup():
+    """orl_reserve pre-sizes every workspace, so an iteration can be captured in CUDA's
+    strict (global) capture mode with no eager warm-up; the replay equals eager."""
+    B, T, V = 5, 80, 3000
+    cfg = _cfg("gae")
+    g = _batch(54, B, T, V, "gae")
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    ctx = orl.Context(0)
+    orl.orl_reserve(ctx, B)
+    gb = Buffers(B, T, DEV, cfg.group_size)
+    graph = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph):          # capture_error_mode="global"
+        run_iteration(ctx, g, cfg, gb, src, mb=2, stream=torch.cuda.current_stream(), finalize="async")
+    graph.replay()
+    torch.cuda.synchronize()
+    got = orl.orl_stats_decode(gb.final_dev.cpu().numpy(), cfg.ppo)
+    eager = Buffers(B, T, DEV, cfg.group_size)
+    want = run_iteration(ctx, g, cfg, eager, src, mb=2)
+    assert got == want
+    for k in KEYS:
+        assert torch.equal(getattr(gb, k), getattr(eager, k)), k
+    with pytest.raises(orl.OrlError):
+        orl.orl_reserve(ctx, -1)
+    ctx.close()

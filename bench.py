@@ -355,6 +355,12 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (K1) --------------------------------
     side = {"old": 8, "ref": 8 + 12, "new": 8 + 24 + 16}   # side bytes per token (DESIGN 5.1)
     k1_ms = sum(a.elapsed_time(b) for _, _, a, b in events)
+    stage = {}
+    for tag, _, a, b in events:
+        stage[tag] = stage.get(tag, 0.0) + a.elapsed_time(b) / args.steps
+    stage_ms = {"S1_old": round(stage.get("old", 0.0), 4), "S1-S3_ref": round(stage.get("ref", 0.0), 4),
+                "S1_S7-S9_actor": round(stage.get("new", 0.0), 4),
+                "S4-S6_C1_S10_C2_and_gaps": round(ms - sum(stage.values()), 4)}
     k1_bytes = 0
     for tag, n, _, _ in events:
         k1_bytes += n * (mb * T) * (V * elt + side[tag])
@@ -423,7 +429,7 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms, 4),
-                "ms_per_step_stats": {"mean": round(statistics.mean(per_step), 4),
+                "stage_ms_per_step": stage_ms, "ms_per_step_stats": {"mean": round(statistics.mean(per_step), 4),
                                       "median": round(statistics.median(per_step), 4),
                                       "min": round(min(per_step), 4), "max": round(max(per_step), 4),
                                       "rank": "rank 0 (value uses the max over ranks of the mean)"}, "higher_is_better": True, "scaling": "weak",

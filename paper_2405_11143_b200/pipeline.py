@@ -90,6 +90,7 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
     B, T = tok.shape
     mbs = microbatches(B, mb)
     hook = on_k1 or (lambda tag: None)
+    nvtx = torch.cuda.nvtx.range                       # per-stage ranges for nsys / ncu --nvtx
     _orl.orl_begin_iteration(ctx, stream)
 
     def s1(src, s, e, out, **kw):
@@ -100,41 +101,56 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
         return _orl.orl_logprobs(ctx, tok, L, src, out, seq_offset=s, inv_temp=cfg.inv_temp, stream=stream,
                                  **kw)
 
-    for s, e in mbs:                                   # S1, old policy
-        h = hook("old")
-        s1(logits("old", s, e), s, e, bufs.logp_old)
-        if h: h()
-    if cfg.use_ref:
+    with nvtx("orl S1 old"):
+        for s, e in mbs:                               # S1, old policy
+            h = hook("old")
+            s1(logits("old", s, e), s, e, bufs.logp_old)
+            if h: h()
+    if not cfg.use_ref:
+        raise NotImplementedError("the paper's PPO loop always has a reference model (P:193)")
+    with nvtx("orl S1-S3 ref"):
         for s, e in mbs:                               # S1+S2+S3, reference
             h = hook("ref")
             s1(logits("ref", s, e), s, e, bufs.logp_ref, partner_logp=bufs.logp_old, kl_est=cfg.kl_est_reward,
                beta_reward=cfg.beta_reward if cfg.kl_mode == "reward" else 0.0,
                seq_reward=batch["seq_reward"], kl=bufs.kl, shaped_reward=bufs.shaped)
             if h: h()
-    else:
-        raise NotImplementedError("the paper's PPO loop always has a reference model (P:193)")
-    _orl.orl_advantages(ctx, L, bufs.adv, kind=cfg.adv_kind, gamma=cfg.gamma, lam=cfg.lam,   # S4/S4'/S5
-                        group_size=cfg.group_size, shaped_reward=bufs.shaped,
-                        values=batch.get("values_old") if cfg.critic else None,
-                        seq_reward=batch["seq_reward"], ret=bufs.ret,
-                        group_keep=bufs.keep if cfg.adv_kind in ("grpo", "rpp_baseline") else None,
-                        stream=stream)
-    _orl.orl_whiten_stats(ctx, cfg.whiten and cfg.adv_kind != "grpo", stream)         # S6 + C1
+    with nvtx("orl S4-S6 advantages + C1"):
+        _orl.orl_advantages(ctx, L, bufs.adv, kind=cfg.adv_kind, gamma=cfg.gamma, lam=cfg.lam,   # S4/S4'/S5
+                            group_size=cfg.group_size, shaped_reward=bufs.shaped,
+                            values=batch.get("values_old") if cfg.critic else None,
+                            seq_reward=batch["seq_reward"], ret=bufs.ret,
+                            group_keep=bufs.keep if cfg.adv_kind in ("grpo", "rpp_baseline") else None,
+                            stream=stream)
+        _orl.orl_whiten_stats(ctx, cfg.whiten and cfg.adv_kind != "grpo", stream)     # S6 + C1
     critic = cfg.critic and batch.get("values_new") is not None
     if grad_sink is not None and isinstance(logits("new", 0, min(B, mb)), LmHeadRows):
         raise NotImplementedError("dL/dlogits needs materialised logits; the LM-head path (NEXT-4) is forward-only")
     if grad_sink is not None and fused_grad:           # S1 + S7..S9 + NEXT-1 in one pass
-        for s, e in mbs:
-            h = hook("new+grad")
-            _orl.orl_ppo_loss_and_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.logp_old, bufs.adv,
-                                       bufs.logp_new, seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
-                                       ret=bufs.ret if critic else None,
-                                       v_new=batch["values_new"] if critic else None,
-                                       v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
-                                       lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
-                                       dlogits=grad_sink(s, e), stream=stream)
-            if h: h()
-        return _finish(ctx, cfg, bufs, stream, finalize)
+        with nvtx("orl S1 S7-S9 actor + dL/dlogits"):
+            _actor_fused(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, stream)
+        with nvtx("orl S10 + C2"):
+            return _finish(ctx, cfg, bufs, stream, finalize)
+    with nvtx("orl S1 S7-S9 actor"):
+        _actor(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, stream)
+    with nvtx("orl S10 + C2"):
+        return _finish(ctx, cfg, bufs, stream, finalize)                   # S10 + C2
+
+
+def _actor_fused(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, stream):
+    for s, e in mbs:
+        h = hook("new+grad")
+        _orl.orl_ppo_loss_and_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.logp_old, bufs.adv,
+                                   bufs.logp_new, seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
+                                   ret=bufs.ret if critic else None,
+                                   v_new=batch["values_new"] if critic else None,
+                                   v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
+                                   lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
+                                   dlogits=grad_sink(s, e), stream=stream)
+        if h: h()
+
+
+def _actor(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, stream):
     for s, e in mbs:                                   # S1 + S7..S9, actor
         h = hook("new")
         src = logits("new", s, e)
@@ -154,7 +170,6 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
             _orl.orl_logits_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.lse, bufs.entropy, bufs.dlogp,
                                  grad_sink(s, e), seq_offset=s, inv_temp=cfg.inv_temp, stream=stream)
             if h: h()
-    return _finish(ctx, cfg, bufs, stream, finalize)                       # S10 + C2
 
 
 def _finish(ctx, cfg, bufs, stream, finalize):

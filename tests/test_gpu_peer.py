@@ -77,7 +77,17 @@ def _worker(rank, world, port, kind, mode, q):
         s, e = synth.split_bounds(B, world, c["group_size"])[rank]
         gs = {k: v[s:e] for k, v in g.items()}
         out = []
-        if mode == "timeout":
+        if mode == "graph":  # the whole iteration, peer kernels included, as one CUDA graph per rank
+            from paper_2405_11143_b200.pipeline import Buffers, GraphStep
+            status, st, _ = _iterate(ctx, gs, cfg)
+            gb = Buffers(e - s, T, torch.device("cuda", 0), cfg.group_size, grads=True)
+            step = GraphStep(ctx, gs, cfg, gb, lambda role, a, z: gs[f"logits_{role}"][a:z], mb=3)
+            for _ in range(3):  # epochs advance on the device across replays
+                step.replay()
+                torch.cuda.synchronize()
+                out.append((status, st, step.result()))
+            dist.barrier()
+        elif mode == "timeout":
             if rank == 0:  # rank 1 never runs an iteration: both waits of rank 0 time out
                 try:
                     status, st, _ = _iterate(ctx, gs, cfg)
@@ -161,3 +171,12 @@ def test_peer_collective_missing_rank_times_out():
     res = _spawn(2, "gae", "timeout")
     status, st = res[0][1][0]
     assert status == "ORL_E_NCCL", status
+
+
+def test_peer_collectives_inside_cuda_graph_replays():
+    res = _spawn(2, "gae", "graph")
+    first = res[0][1][0][1]
+    for r in range(2):
+        for status, st, (gstatus, gst) in res[r][1]:
+            assert status == "ORL_OK" and gstatus == "ORL_OK"
+            assert st == first and gst == first      # eager == replay, bit for bit, on every rank

@@ -368,7 +368,7 @@ def test_run_to_run_bit_reproducible(ctx):
         assert torch.equal(getattr(b1, k), getattr(b2, k)), k
 
 
-@pytest.mark.parametrize("kind,n", [("gae", 2), ("rpp", 4), ("grpo", 2)])
+@pytest.mark.parametrize("kind,n", [("gae", 2), ("rpp", 4), ("grpo", 2), ("gae", 8), ("grpo", 4)])
 def test_shard_emulation_matches_single_rank(kind, n):
     """n virtual ranks on one GPU, partials exchanged through the collective
     boundary hooks (the exact device merges NCCL feeds), vs one rank."""

@@ -301,6 +301,48 @@ def test_neg_inf_entries_and_errors(ctx):
     assert st["n_token_range"] == 1 and st["n_nonfinite"] == 2
 
 
+@pytest.mark.parametrize("V", [128256, 50257])
+def test_extreme_rows_overflow_redo_path(ctx, V):
+    """Rows that force the fast path's exact redo (an element > the thread's seed max +
+    64 log2 units, SURVEY 8(c) S1 pins): +60 / +1000 spikes at non-target and target
+    positions (after each thread's first vector), a +1e4 spike, a uniform row, a row at
+    -1e30 except the target, a very negative spike, wide +-50 noise; TMA (V = 128256)
+    and generic (V = 50257) paths; inv_temp 1 and 1/0.7."""
+    B, T = 2, 8
+    x = torch.randn(B, T, V, device=DEV)
+    tok = synth.tokens_for(B, T, V, 9).to(DEV)
+    tgt = lambda b, t: int(tok[b, t])  # noqa: E731
+    far = lambda b, t: (tgt(b, t) + V // 2) % V  # noqa: E731
+    x[0, 0, far(0, 0)] = 60.0
+    x[0, 1, far(0, 1)] = 1000.0
+    x[0, 2, tgt(0, 2)] = 80.0
+    x[0, 3, far(0, 3)] = 1.0e4
+    x[0, 4, :] = 0.0
+    x[0, 5, :] = -1.0e30
+    x[0, 5, tgt(0, 5)] = 0.0
+    x[0, 6, far(0, 6)] = -1.0e4
+    x[0, 7] = (torch.rand(V, device=DEV) - 0.5) * 100.0
+    x[1, 0, V - 1] = 200.0                            # spike in the last (tail) element
+    x[1, 1, :64] = 90.0                               # spikes inside the first vectors
+    xb = x.to(torch.bfloat16)
+    L = torch.tensor([T, T], dtype=torch.int32, device=DEV)
+    for inv_temp in (1.0, 1 / 0.7):
+        logp, ent, lse = (torch.zeros(B, T, device=DEV) for _ in range(3))
+        orl.orl_begin_iteration(ctx)
+        orl.orl_logprobs(ctx, tok, L, xb, logp, entropy=ent, lse=lse, inv_temp=inv_temp)
+        torch.cuda.synchronize()
+        o = oracle.logprobs(synth.to_numpy_logits(xb), _np(tok), _np(L), inv_temp)
+        m = np.ones((B, T), bool)
+        for name, g in (("logp", logp), ("entropy", ent), ("lse", lse)):
+            # the 2e-3 bar everywhere; the 1e-4 alarm scaled by the fp32 output format at these
+            # magnitudes (|logp| up to 1.4e4 here, whose fp32 ulp is ~1e-3)
+            parity.check_abs(f"{name} (inv_temp {inv_temp:.3f})", _np(g), o[name], m, alarm=parity.LOGP_ABS)
+            err = np.abs(_np(g).astype(np.float64) - o[name])
+            assert np.all(err <= np.maximum(parity.LOGP_ALARM, 4 * 2.0 ** -24 * np.abs(o[name]))), (name, err.max())
+        status, st = orl.orl_finalize(ctx, orl.PPOConfig())
+        assert st["n_nonfinite"] == 0 and st["n_token_range"] == 0, st
+
+
 def test_ratio_guard_and_empty_batch(ctx):
     B, T, V = 2, 4, 256
     x = torch.randn(B, T, V, device=DEV)

@@ -343,6 +343,33 @@ def test_extreme_rows_overflow_redo_path(ctx, V):
         assert st["n_nonfinite"] == 0 and st["n_token_range"] == 0, st
 
 
+def test_logits_beyond_fp32_range_are_flagged(ctx):
+    """Reading Z34: a finite bf16 logit whose scaled value x * inv_temp * log2(e) exceeds
+    the fp32 range (|x| >~ 2.4e38 at inv_temp = 1) cannot be represented by the kernel:
+    a large positive one makes the row NaN and counts as non-finite (never a silent wrong
+    value); a large negative one is an exp of -inf, i.e. an ordinary zero-probability entry."""
+    for V in (128256, 50257):
+        B, T = 1, 4
+        x = torch.randn(B, T, V, device=DEV)
+        tok = synth.tokens_for(B, T, V, 3).to(DEV)
+        x[0, 0, (int(tok[0, 0]) + 7) % V] = 3.0e38
+        x[0, 1, int(tok[0, 1])] = 3.0e38
+        x[0, 2, (int(tok[0, 2]) + 5) % V] = -3.0e38
+        xb = x.to(torch.bfloat16)
+        L = torch.tensor([T], dtype=torch.int32, device=DEV)
+        logp, ent = torch.zeros(B, T, device=DEV), torch.zeros(B, T, device=DEV)
+        orl.orl_begin_iteration(ctx)
+        orl.orl_logprobs(ctx, tok, L, xb, logp, entropy=ent)
+        torch.cuda.synchronize()
+        lp = _np(logp)
+        assert np.isnan(lp[0, 0]) and np.isnan(lp[0, 1])
+        o = oracle.logprobs(synth.to_numpy_logits(xb), _np(tok), _np(L))
+        ok = np.array([[False, False, True, True]])
+        parity.check_abs("logp", np.where(ok, lp, 0), np.where(ok, o["logp"], 0), ok)
+        status, st = orl.orl_finalize(ctx, orl.PPOConfig())
+        assert status == "ORL_E_NONFINITE" and st["n_nonfinite"] == 2
+
+
 def test_ratio_guard_and_empty_batch(ctx):
     B, T, V = 2, 4, 256
     x = torch.randn(B, T, V, device=DEV)

@@ -53,6 +53,16 @@ def _bf16_peak(sustained: bool):
         (1590.0, "fallback burst (B200_PROFILING.md 1.59 PFLOP/s)")
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def _workload_desc(name, c, B, world):
     return (f"{name}: B={B}/rank T={c['T']} V={c['V']} {c['dtype']} logits x3 models resident in HBM, "
             f"adv={c['adv_kind']} gamma={c['gamma']} lambda={c['lam']} whiten={c['whiten']} "
@@ -178,7 +188,8 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": _workload_desc(args.config, c, n_seq, 1) + " (oracle sample)",
                        "global_batch": n_seq, "seq_len": T, "parallelism": "host threads"},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -421,7 +432,8 @@ def run_ours(args):
             return toks / dt, desc
 
         v_all, d_all = sample(args.ref_seqs, args.ref_seqs * min(T, 1024), cores)
-        cpu = {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": d_all}
+        cpu = {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": d_all,
+               "cpu_model": _cpu_model()}
         # the same oracle on one core (1-core and all-core)
         v_one, d_one = sample(1, 1024, 1)
         cpu["single_core"] = {"value": v_one, "unit": UNIT, "cores": 1, "sample": d_one}

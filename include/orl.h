@@ -205,6 +205,15 @@ const char *orl_last_error(const orl_ctx *ctx);
 /* Number of kernels the context has launched so far (for bench accounting). */
 uint64_t orl_launch_count(const orl_ctx *ctx);
 
+/* Attention-mask input (Z10, "attention masks"): lengths[b] = the number of
+ * leading ones of mask[b, 0..T) (device, u8 [B, T] row-major; nonzero = valid).
+ * The path's masks are right-padded prefixes: a valid position after the first
+ * padded one is counted as a mask error (orl_finalize -> ORL_E_MASK; the row
+ * keeps its leading prefix).  Call after orl_begin_iteration (which clears the
+ * counters).  Stream-ordered; B = 0 is a no-op; T < 1: ORL_E_SHAPE. */
+orl_status orl_lengths_from_mask(orl_ctx *ctx, int64_t B, int64_t T, const uint8_t *mask, int32_t *lengths,
+                                 void *stream);
+
 /* Pre-size the context's workspaces (host call, synchronises the device):
  * per-sequence whitening partials and the length prefix for up to max_seqs
  * responses per rank-local batch / call, and the NEXT-4 split partials for

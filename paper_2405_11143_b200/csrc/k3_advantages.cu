@@ -405,4 +405,39 @@ cudaError_t launch_stats_peer(const double *acc, const unsigned long long *err, 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ masks -> lengths
+// Z10: the path's masks are right-padded prefixes.  One CTA per row: L_b = index of the
+// first 0 (T if none); a 1 after that is a non-prefix mask, counted in err[2] (reported
+// by orl_finalize as ORL_E_MASK) -- the row then keeps its leading prefix.
+__global__ void __launch_bounds__(256) mask_lengths_kernel(const uint8_t *mask, int64_t T, int32_t *lengths,
+                                                           unsigned long long *err) {
+    __shared__ int first_zero, last_one;
+    const int64_t b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        first_zero = (int)T;
+        last_one = -1;
+    }
+    __syncthreads();
+    const uint8_t *row = mask + b * T;
+    int fz = (int)T, lo = -1;
+    for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+        if (row[t]) lo = (int)t;
+        else if (fz == (int)T) fz = (int)t;
+    }
+    if (fz < (int)T) atomicMin(&first_zero, fz);
+    if (lo >= 0) atomicMax(&last_one, lo);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        lengths[b] = first_zero;
+        if (last_one > first_zero && err) atomicAdd(&err[2], 1ull);
+    }
+}
+
+cudaError_t launch_mask_lengths(const uint8_t *mask, int64_t B, int64_t T, int32_t *lengths,
+                                unsigned long long *err, cudaStream_t s) {
+    if (B <= 0) return cudaSuccess;
+    mask_lengths_kernel<<<(unsigned)B, 256, 0, s>>>(mask, T, lengths, err);
+    return cudaGetLastError();
+}
+
 }  // namespace orl

@@ -810,6 +810,20 @@ extern "C" orl_status orl_kl_controller_step(double *beta, double target, double
     return ORL_OK;
 }
 
+// ------------------------------------------------------------------ masks
+extern "C" orl_status orl_lengths_from_mask(orl_ctx *ctx, int64_t B, int64_t T, const uint8_t *mask,
+                                            int32_t *lengths, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (B < 0 || T < 1 || T > INT32_MAX) return fail(ctx, ORL_E_SHAPE, "B=%lld T=%lld", (long long)B, (long long)T);
+    if (B > 0 && (!mask || !lengths)) return fail(ctx, ORL_E_INVALID_ARG, "mask/lengths is NULL");
+    if (!aligned4(lengths)) return fail(ctx, ORL_E_ALIGN, "lengths must be 4-byte aligned");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    CUDA_TRY(ctx, launch_mask_lengths(mask, B, T, lengths, ctx->d_err, as_stream(stream)));
+    ctx->launches += B > 0 ? 1 : 0;
+    return ORL_OK;
+}
+
 // ------------------------------------------------------------------ workspace
 extern "C" orl_status orl_reserve(orl_ctx *ctx, int64_t max_seqs, int64_t max_lm_rows, int64_t max_vocab) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");

@@ -156,6 +156,8 @@ cudaError_t launch_whiten_peer(const double *seq_part, int B, const PeerArgs &pa
 cudaError_t launch_stats_peer(const double *acc, const unsigned long long *err, const PeerArgs &pa,
                               const double *whiten, double *flags, double c1, double c2, double beta_loss,
                               int kl_in_loss, int loss_agg, double *stats_out, cudaStream_t s);
+cudaError_t launch_mask_lengths(const uint8_t *mask, int64_t B, int64_t T, int32_t *lengths,
+                                unsigned long long *err, cudaStream_t s);
 cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_slot, cudaStream_t s);
 // Merge gathered [world][4] rank partials in rank order -> whiten[4] =
 // {N, mu, sigma, apply}; warn flag into flags[0].

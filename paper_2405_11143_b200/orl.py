@@ -103,6 +103,7 @@ _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats),
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
 _lib.orl_reserve.argtypes = [_P, _I64, _I64, _I64]
+_lib.orl_lengths_from_mask.argtypes = [_P, _I64, _I64, _P, _P, _P]
 _lib.orl_finalize_async.argtypes = [_P, ctypes.POINTER(PpoCfg), _P, _P]
 _lib.orl_stats_decode.argtypes = [_P, _F64, ctypes.POINTER(Stats)]
 _lib.orl_peer_handle.argtypes = [_P, ctypes.c_char_p]
@@ -255,6 +256,17 @@ def _logits(x):
 def orl_reserve(ctx: Context, max_seqs: int, max_lm_rows: int = 0, max_vocab: int = 0):
     """Pre-size the workspaces so later calls within these sizes never allocate."""
     return ctx.check(_lib.orl_reserve(ctx.h, int(max_seqs), int(max_lm_rows), int(max_vocab)))
+
+
+def orl_lengths_from_mask(ctx: Context, mask, lengths, stream=None):
+    """lengths[b] = leading ones of the u8/bool [B, T] right-padded mask (non-prefix rows
+    are counted as ORL_E_MASK at orl_finalize)."""
+    if mask.dtype not in (torch.uint8, torch.bool) or mask.dim() != 2 or not mask.is_contiguous():
+        raise TypeError("mask must be a contiguous [B, T] uint8/bool tensor")
+    if lengths.dtype != torch.int32 or lengths.numel() < mask.shape[0]:
+        raise TypeError("lengths must be int32 [B]")
+    B, T = mask.shape
+    return ctx.check(_lib.orl_lengths_from_mask(ctx.h, B, T, _ptr(mask), _ptr(lengths), _stream(stream)))
 
 
 def orl_begin_iteration(ctx: Context, stream=None):

@@ -689,3 +689,42 @@ def test_next1_fused_forward_backward_matches_two_passes(ctx, agg):
     assert torch.equal(out[True][1], out[False][1])
     for k in ("logp_new", "entropy", "lse", "dlogp", "dv"):
         assert torch.equal(getattr(out[True][2], k), getattr(out[False][2], k)), k
+
+
+def test_lengths_from_attention_mask(ctx):
+    """orl_lengths_from_mask (Z10): leading-ones count of right-padded masks, bit-exact
+    against numpy; a non-prefix mask is reported as ORL_E_MASK; an iteration on
+    mask-derived lengths equals the one on the true lengths bit for bit."""
+    rng = np.random.default_rng(7)
+    B, T = 37, 300
+    L = rng.integers(0, T + 1, size=B).astype(np.int32)
+    L[0], L[1] = 0, T
+    mask = (np.arange(T)[None, :] < L[:, None]).astype(np.uint8)
+    got = torch.full((B,), -5, dtype=torch.int32, device=DEV)
+    orl.orl_begin_iteration(ctx)
+    orl.orl_lengths_from_mask(ctx, torch.from_numpy(mask).to(DEV), got)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(got), L)
+    bad = mask.copy()
+    bad[5, L[5] + 3 if L[5] + 3 < T else 0] = 1 if L[5] + 3 < T else 0
+    bad[9, :] = 0
+    bad[9, 7] = 1                                       # a hole-y row: leading prefix 0, error
+    orl.orl_begin_iteration(ctx)
+    orl.orl_lengths_from_mask(ctx, torch.from_numpy(bad).to(DEV).bool(), got)
+    status, st = orl.orl_finalize(ctx, orl.PPOConfig())
+    assert status == "ORL_E_MASK"
+    lead = np.array([int(np.argmin(np.append(r, 0))) for r in bad])
+    assert np.array_equal(_np(got), lead)
+    # whole iteration on mask-derived lengths == on the true lengths
+    c = dict(synth.CONFIGS["llama8b"])
+    g = _gpu_batch(71, 6, 96, 2048, "mixed")
+    cfg = PathConfig.from_synth(c)
+    _, st1, b1 = _run(ctx, g, cfg, mb=4)
+    m6 = (torch.arange(96, device=DEV)[None, :] < g["lengths"][:, None]).to(torch.uint8)
+    g2 = dict(g, lengths=torch.empty_like(g["lengths"]))
+    orl.orl_begin_iteration(ctx)
+    orl.orl_lengths_from_mask(ctx, m6, g2["lengths"])
+    _, st2, b2 = _run(ctx, g2, cfg, mb=4)
+    assert st1 == st2 and torch.equal(b1.adv, b2.adv) and torch.equal(b1.logp_new, b2.logp_new)
+    with pytest.raises(TypeError):
+        orl.orl_lengths_from_mask(ctx, m6.float(), g2["lengths"])

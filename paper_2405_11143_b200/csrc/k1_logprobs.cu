@@ -106,6 +106,8 @@ struct __align__(128) K1Smem {
     uint64_t row_full[kSlots];
     uint64_t row_empty[kSlots];
     int32_t row_y[kRowInfo];
+    int32_t row_h[kRowInfo];        // unaligned rows: head bytes before the 16-byte aligned interior
+    float row_x[kRowInfo][16];      // unaligned rows: raw head elements, then tail elements
     uint64_t grad_full[kGradRows];
     GradRow grad[kGradRows];
     RowSlot slot[kSlots];
@@ -551,6 +553,27 @@ __device__ __forceinline__ void process_words(ThreadAcc &a, uint32_t (&w)[kW], b
     }
 }
 
+// One scalar logit (an unaligned row's head or tail element) folded exactly into the
+// thread's state: clamp -inf as the exact path does, rescale to a new max if needed,
+// accumulate into the even lane of the packed sums.
+template <bool ENT>
+__device__ __forceinline__ void acc_scalar(ThreadAcc &a, float x, float c2) {
+    x = fmax_nan(x, kNegClampF32);
+    const float mn = fmax_nan(a.m, x * c2);
+    const float d = a.m - mn, r = ex2(d);
+    const uint64_t d2 = pack2(d, d), r2 = pack2(r, r);
+    if (ENT) {
+        a.uA = fmul2(r2, ffma2(d2, a.sA, a.uA));
+        a.uB = fmul2(r2, ffma2(d2, a.sB, a.uB));
+    }
+    a.sA = fmul2(r2, a.sA);
+    a.sB = fmul2(r2, a.sB);
+    a.m = mn;
+    const float t = fmaf(x, c2, -a.m), e = ex2(t);
+    a.sA = fadd2(a.sA, pack2(e, 0.f));
+    if (ENT) a.uA = ffma2(pack2(e, 0.f), pack2(t, 0.f), a.uA);
+}
+
 // Warp-level variant for the TMA kernel (epilogue warp 0 owns the partials).
 // The last CTA loads every CTA's partials at once (all loads in flight), then
 // sums each column in a fixed order: lane-strided CTA order, then a fixed
@@ -654,12 +677,27 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 locate_row(cum, p.B, blockIdx.x, b, t);
                 y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
             }
+            // unaligned rows: TMA streams the 16-byte aligned interior [h, h + ib) of the row;
+            // this lane loads the < 16-byte head and tail (<= 7 + 7 bf16 / 3 + 3 fp32 elements)
+            // before it waits for the row's first stage and publishes them with the row info
+            int h = 0;
+            int64_t ib = row_bytes;
+            float hx[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) hx[k] = 0.f;
             auto issue = [&](const char *src, int64_t c0, int64_t c1, uint64_t pol, int64_t publish_rl) {
                 for (int64_t c = c0; c < c1; ++c) {
                     const int64_t off = c * kChunk;
-                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
+                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, ib - off);
                     mbar_wait(&S.empty[stage], phase ^ 1u);
-                    if (c == 0 && publish_rl >= 0) S.row_y[publish_rl % kRowInfo] = y;  // released by the arrive
+                    if (c == 0 && publish_rl >= 0) {  // released by the arrive below
+                        S.row_y[publish_rl % kRowInfo] = y;
+                        S.row_h[publish_rl % kRowInfo] = h;
+                        if (MODE != kModeLossGrad && p.unaligned) {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) S.row_x[publish_rl % kRowInfo][k] = hx[k];
+                        }
+                    }
                     mbar_arrive_expect_tx(&S.full[stage], bytes);
                     tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
                     if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -677,11 +715,28 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
                     }
                     src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
-                    issue(src, 0, ksplit, pol_fwd, rl);
+                    if (MODE != kModeLossGrad && p.unaligned) {
+                        h = (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15u)) & 15u);
+                        ib = (row_bytes - h) & ~(int64_t)15;
+                        const int head_e = h / (int)sizeof(Tin);
+                        const int tail_e = (int)((row_bytes - h - ib) / (int64_t)sizeof(Tin));
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const int idx = k < head_e ? k : (k - head_e < tail_e ? (int)p.V - tail_e + (k - head_e) : -1);
+                            if (idx >= 0)
+                                hx[k] = sizeof(Tin) == 2
+                                    ? __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short *>(src) + idx)) << 16)
+                                    : __ldg(reinterpret_cast<const float *>(src) + idx);
+                        }
+                        src += h;
+                        issue(src, 0, (ib + kChunk - 1) / kChunk, pol_fwd, rl);
+                    } else {
+                        issue(src, 0, ksplit, pol_fwd, rl);
+                    }
                 }
                 if (MODE == kModeLossGrad && rl > 0) issue(prev_src, 0, nch, pol_bwd, -1);
                 if (rl < n_rows) {
-                    issue(src, ksplit, nch, pol_fwd, -1);
+                    if (!(MODE != kModeLossGrad && p.unaligned)) issue(src, ksplit, nch, pol_fwd, -1);
                     b = bn; t = tn; y = yn;
                 }
                 prev_src = src;
@@ -778,21 +833,33 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     int64_t tchunk = -1;
     int tin = 0;
     bool towner = false;
+    // unaligned rows (p.unaligned, not in the fused mode): the chunks cover the aligned
+    // interior [h, h + ib) of the row; its < 16-byte head and tail are folded in by
+    // scalar loads after the first chunk
+    const bool unal = MODE != kModeLossGrad && p.unaligned;
+    int64_t ib = row_bytes, row_nch = nch;
+    int row_h = 0, row_yv = -1;
     auto fwd_chunks = [&](int64_t rl, int64_t c0, int64_t c1) {
-        for (int64_t ci = c0; ci < c1; ++ci) {
-            const int64_t off = ci * kChunk;
-            const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
+        for (int64_t ci = c0; ci < (unal ? (ci == 0 ? 1 : row_nch) : c1); ++ci) {
             mbar_wait(&S.full[stage], phase);
             if (ci == 0) {  // row start: which chunk / thread holds the target logit
                 acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
                 have_tgt = false;
                 const int y = S.row_y[rl % kRowInfo];
+                row_yv = y;
+                if (unal) {
+                    row_h = S.row_h[rl % kRowInfo];
+                    ib = (row_bytes - row_h) & ~(int64_t)15;
+                    row_nch = (ib + kChunk - 1) / kChunk;
+                }
                 const bool y_ok = (y >= 0) && ((int64_t)y < p.V);
-                const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin);
-                tchunk = y_ok ? ybyte / kChunk : -1;
+                const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin) - row_h;  // offset in the interior
+                tchunk = (y_ok && ybyte >= 0 && ybyte < ib) ? ybyte / kChunk : -1;
                 tin = (int)(ybyte % kChunk);
                 towner = ((tin >> 4) % kConsumers) == ct;
             }
+            const int64_t off = ci * kChunk;
+            const int bytes = (int)min((int64_t)kChunk, ib - off);
             const uint8_t *sb = S.stage[stage];
             if (ci == tchunk && towner) {  // raw target value, before any clamping
                 tgt = sizeof(Tin) == 2
@@ -810,6 +877,22 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
             if (ent) process_words<Tin, true, POLY>(acc, w, ci == 0, p.c2, c2p);
             else process_words<Tin, false, POLY>(acc, w, ci == 0, p.c2, c2p);
+            if (unal && ci == 0) {  // the row's head and tail elements, one per thread
+                const int head_e = row_h / (int)sizeof(Tin);
+                const int tail_e = (int)((row_bytes - row_h - ib) / (int64_t)sizeof(Tin));
+                int idx = -1;
+                if (ct < head_e) idx = ct;
+                else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
+                if (idx >= 0) {
+                    const float x = S.row_x[rl % kRowInfo][ct];  // published with the row info
+                    if (ent) acc_scalar<true>(acc, x, p.c2);
+                    else acc_scalar<false>(acc, x, p.c2);
+                    if (idx == row_yv) {
+                        tgt = x;
+                        have_tgt = true;
+                    }
+                }
+            }
         }
     };
     auto fwd_publish = [&](int64_t rl) {  // row end: this thread's state into the row slot

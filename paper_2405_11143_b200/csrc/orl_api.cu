@@ -160,6 +160,17 @@ static bool tma_eligible(const orl_logits *lg) {
            ((lg->stride_b * elt) % 16 == 0);
 }
 
+// K1 streaming layout: 1 = TMA, aligned rows; 2 = TMA over each row's 16-byte aligned
+// interior with scalar head/tail loads (rows naturally aligned, >= 64 bytes, e.g.
+// V = 50257 bf16 or padded pitches); 0 = the generic kernel.
+static int k1_layout(const orl_logits *lg) {
+    if (tma_eligible(lg)) return 1;
+    if (getenv("ORL_FORCE_GENERIC") || getenv("ORL_K1_NO_UNALIGNED_TMA")) return 0;
+    const int64_t elt = lg->dtype == ORL_BF16 ? 2 : 4;
+    const uintptr_t base = reinterpret_cast<uintptr_t>(lg->ptr);
+    return (base % elt == 0) && lg->V * elt >= 64 ? 2 : 0;
+}
+
 static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const orl_logits *lg,
                         float inv_temp) {
     std::memset(&p, 0, sizeof p);
@@ -395,7 +406,9 @@ static orl_status logprobs_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     p.shaped = shaped_reward;
     if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
     if (head) return run_lmhead(ctx, p, head, kModeLogprob, as_stream(stream));
-    CUDA_TRY(ctx, launch_k1(p, tma_eligible(logits), kModeLogprob, ctx->num_sms, as_stream(stream)));
+    const int lay = k1_layout(logits);
+    p.unaligned = lay == 2;
+    CUDA_TRY(ctx, launch_k1(p, lay != 0, kModeLogprob, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
     return ORL_OK;
 }
@@ -576,9 +589,11 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     p.loss_agg = cfg->loss_agg;
     if ((st = prepare_prefix(ctx, rows, true, as_stream(stream), &p.cum_global))) return st;
     if (head) return run_lmhead(ctx, p, head, kModeLoss, as_stream(stream));
-    const bool tma = tma_eligible(actor);
+    const int lay = k1_layout(actor);
+    const bool tma = lay == 1;
+    p.unaligned = lay == 2;
     if (!grad) {
-        CUDA_TRY(ctx, launch_k1(p, tma, kModeLoss, ctx->num_sms, as_stream(stream)));
+        CUDA_TRY(ctx, launch_k1(p, lay != 0, kModeLoss, ctx->num_sms, as_stream(stream)));
         ctx->launches += 1;
         return ORL_OK;
     }
@@ -588,6 +603,7 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     const bool out_ok = (reinterpret_cast<uintptr_t>(grad->dlogits) % 16 == 0) &&
                         ((grad->stride_t * elt) % 16 == 0) && ((grad->stride_b * elt) % 16 == 0);
     if (tma && out_ok) {
+        p.unaligned = 0;
         p.dlogits = grad->dlogits;
         p.out_stride_b = grad->stride_b;
         p.out_stride_t = grad->stride_t;
@@ -597,7 +613,7 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
         ctx->launches += 1;
         return ORL_OK;
     }
-    CUDA_TRY(ctx, launch_k1(p, tma, kModeLoss, ctx->num_sms, as_stream(stream)));
+    CUDA_TRY(ctx, launch_k1(p, lay != 0, kModeLoss, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;
     return orl_logits_grad(ctx, rows, actor, inv_temp, cfg, lse, entropy, dloss_dlogp, grad->dlogits,
                            grad->stride_b, grad->stride_t, grad->zero_masked, stream);

@@ -27,6 +27,8 @@ struct K1Params {
     int64_t V, stride_b, stride_t;  // elements
     int64_t row_bytes;
     int elt;            // 2 (bf16) or 4 (fp32)
+    int unaligned;      // TMA kernel, rows not 16-byte aligned / sized: stream each row's aligned
+                        // interior, load the < 16-byte head and tail with scalar loads
     float inv_temp;
     float c2;           // inv_temp * log2(e)
     int poly;           // MUFU offload: every poly-th element pair uses the FMA-pipe exp2 (0 = off)

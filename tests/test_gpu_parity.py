@@ -233,10 +233,18 @@ def test_full_size_sampled(ctx, name, B):
 
 
 # --------------------------------------------------------------------------- edge cases / errors
-def test_generic_path_unaligned_vocab(ctx):
-    """V = 50257 bf16 rows are not 16-byte multiples -> generic (non-TMA) kernel."""
+@pytest.mark.parametrize("path", ["unaligned_tma", "generic"])
+def test_generic_path_unaligned_vocab(ctx, path, monkeypatch):
+    """V = 50257 bf16 rows are not 16-byte multiples: by default the TMA kernel streams
+    each row's 16-byte aligned interior and loads the head/tail elements singly;
+    ORL_K1_NO_UNALIGNED_TMA selects the generic (non-TMA) kernel."""
+    if path == "generic":
+        monkeypatch.setenv("ORL_K1_NO_UNALIGNED_TMA", "1")
     B, T, V = 3, 40, 50257
     g = _gpu_batch(3, B, T, V, "mixed")
+    # targets in the rows' unaligned heads and tails too
+    g["tokens"][0, :8] = torch.arange(8, device=DEV, dtype=torch.int32)
+    g["tokens"][1, :8] = torch.arange(V - 8, V, device=DEV, dtype=torch.int32)
     cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V))
     status, st, bufs = _run(ctx, g, cfg, mb=2)
     assert status == "ORL_OK"
@@ -245,6 +253,42 @@ def test_generic_path_unaligned_vocab(ctx):
     o = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"])
     parity.check_abs("logp_new", _np(bufs.logp_new), o["logp"], m)
     parity.check_abs("entropy", _np(bufs.entropy), o["entropy"], m)
+
+
+@pytest.mark.parametrize("dtype,V,pad", [("bf16", 50257, 0), ("bf16", 32000, 3), ("f32", 50257, 0),
+                                         ("f32", 1001, 1), ("bf16", 33, 0)])
+def test_unaligned_tma_matches_generic_and_oracle(ctx, monkeypatch, dtype, V, pad):
+    """Unaligned rows through the TMA kernel (aligned interior + scalar head/tail) vs the
+    generic kernel and the oracle; gathered raw logits bit-exact; targets placed in
+    heads and tails; a +80 spike in a head forces the scalar rescale."""
+    B, T = 3, 24
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    x = torch.randn(B, T, V + pad, device=DEV) * 2
+    x[0, 3, 1] = 80.0
+    x = x.to(tdt)[..., :V]
+    tok = synth.tokens_for(B, T, V, 5).to(DEV)
+    tok[0, :4] = torch.tensor([0, 1, 2, 3], dtype=torch.int32, device=DEV)
+    tok[1, :4] = torch.tensor([V - 1, V - 2, V - 3, V - 4], dtype=torch.int32, device=DEV) % V
+    L = torch.tensor([T, T - 5, 7], dtype=torch.int32, device=DEV)
+    outs = {}
+    for mode in ("tma", "generic"):
+        if mode == "generic":
+            monkeypatch.setenv("ORL_K1_NO_UNALIGNED_TMA", "1")
+        o = {k: torch.full((B, T), 7.0, device=DEV) for k in ("logp", "entropy", "lse", "gathered")}
+        orl.orl_begin_iteration(ctx)
+        orl.orl_logprobs(ctx, tok, L, x, o["logp"], entropy=o["entropy"], lse=o["lse"], gathered=o["gathered"],
+                         inv_temp=1 / 0.7)
+        torch.cuda.synchronize()
+        outs[mode] = {k: _np(v) for k, v in o.items()}
+    monkeypatch.delenv("ORL_K1_NO_UNALIGNED_TMA")
+    xn = x.float().cpu().numpy() if dtype == "f32" else synth.to_numpy_logits(x)
+    ora = oracle.logprobs(xn, _np(tok), _np(L), 1 / 0.7)
+    m = parity.valid_mask(_np(L), T)
+    for mode in ("tma", "generic"):
+        for k in ("logp", "entropy", "lse"):
+            parity.check_abs(f"{mode} {k}", outs[mode][k], ora[k], m)
+        assert np.array_equal(outs[mode]["gathered"][m], ora["gathered"][m].astype(np.float32)), mode
+    np.testing.assert_allclose(outs["tma"]["logp"][m], outs["generic"]["logp"][m], atol=2e-6)
 
 
 def test_forced_generic_matches_tma(ctx, monkeypatch):

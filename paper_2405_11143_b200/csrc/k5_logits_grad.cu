@@ -38,7 +38,9 @@ struct RowInfo {
     float A1;   // inv_temp * a * ln2
     float A0;   // inv_temp * (a H - w)
     float wt;   // inv_temp * w   (the delta term at v = y)
-    int32_t pad[3];
+    int32_t h;  // unaligned rows: head bytes before the 16-byte aligned interior
+    int32_t pad[2];
+    float hx[16];  // unaligned rows: raw head elements, then tail elements
 };
 
 struct __align__(128) Smem {
@@ -99,6 +101,30 @@ __device__ __forceinline__ uint32_t f32x2_to_bf16x2(float lo, float hi) {
     return r;
 }
 
+// One gradient element written singly (unaligned heads / tails, the target's delta term).
+template <typename Tin>
+__device__ __forceinline__ void st_elem(Tin *orow, int64_t v, float g) {
+    if (sizeof(Tin) == 2) {
+        const uint32_t hb = f32x2_to_bf16x2(g, 0.f) & 0xffffu;
+        asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + v), "h"((unsigned short)hb) : "memory");
+    } else {
+        reinterpret_cast<float *>(orow)[v] = g;
+    }
+}
+
+// Zero one output row of row_bytes at any element-aligned address: scalar head and tail,
+// 16-byte stores for the aligned interior; threads ct of nthr share it.
+template <typename Tin>
+__device__ void zero_row(char *orow, int64_t row_bytes, int ct, int nthr) {
+    const int h = (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(orow) & 15u)) & 15u);
+    const int hb = (int)min((int64_t)h, row_bytes);
+    const int64_t ib = (row_bytes - hb) & ~(int64_t)15;
+    for (int64_t e = ct; e < hb / (int64_t)sizeof(Tin); e += nthr) reinterpret_cast<Tin *>(orow)[e] = Tin(0);
+    for (int64_t o = (int64_t)ct * 16; o < ib; o += (int64_t)nthr * 16) stg128(orow + hb + o, make_uint4(0u, 0u, 0u, 0u));
+    const int64_t tail0 = (hb + ib) / (int64_t)sizeof(Tin), V = row_bytes / (int64_t)sizeof(Tin);
+    for (int64_t e = tail0 + ct; e < V; e += nthr) reinterpret_cast<Tin *>(orow)[e] = Tin(0);
+}
+
 // Row constants from the saved forward quantities.  a = c2/N (token mean) or
 // c2/(N_seq L_b) (NEXT-2 sequence mean).
 __device__ __forceinline__ k5::RowInfo row_info(const K5Params &p, int64_t gi, int y, int L) {
@@ -149,12 +175,30 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                 locate_row(cum, p.B, j, b, t);
                 const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
                 const RowInfo ri = row_info(p, gi, __ldg(p.tokens + gi), cum[b] - (b > 0 ? cum[b - 1] : 0));
+                RowInfo rix = ri;
                 const char *src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b,
                                                              p.stride_t) * (int64_t)sizeof(Tin);
-                for (int64_t off = 0; off < row_bytes; off += kChunk) {
-                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, row_bytes - off);
+                int64_t ib = row_bytes;
+                rix.h = 0;
+                if (p.unaligned) {  // stream the aligned interior; load the head / tail here
+                    rix.h = (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15u)) & 15u);
+                    ib = (row_bytes - rix.h) & ~(int64_t)15;
+                    const int head_e = rix.h / (int)sizeof(Tin);
+                    const int tail_e = (int)((row_bytes - rix.h - ib) / (int64_t)sizeof(Tin));
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const int idx = k < head_e ? k : (k - head_e < tail_e ? (int)p.V - tail_e + (k - head_e) : -1);
+                        rix.hx[k] = idx < 0 ? 0.f
+                                    : sizeof(Tin) == 2
+                                        ? __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short *>(src) + idx)) << 16)
+                                        : __ldg(reinterpret_cast<const float *>(src) + idx);
+                    }
+                    src += rix.h;
+                }
+                for (int64_t off = 0; off < ib; off += kChunk) {
+                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, ib - off);
                     mbar_wait(&S.empty[stage], phase ^ 1u);
-                    if (off == 0) S.info[rl % kRowInfo] = ri;
+                    if (off == 0) S.info[rl % kRowInfo] = rix;
                     mbar_arrive_expect_tx(&S.full[stage], bytes);
                     tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
                     if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -175,20 +219,36 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                     logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.out_stride_b, p.out_stride_t);
         RowInfo ri;
         uint64_t nl2 = 0, A1p = 0, A0p = 0;
-        for (int64_t off = 0; off < row_bytes; off += kChunk) {
-            const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
-            const int nvec = bytes >> 4;
+        int64_t ib = row_bytes;  // interior bytes of an unaligned row (set at its first chunk)
+        for (int64_t off = 0; off < ib; off += kChunk) {
             mbar_wait(&S.full[stage], phase);
             if (off == 0) {
                 ri = S.info[rl % kRowInfo];
                 nl2 = pack2(-ri.l2, -ri.l2);
                 A1p = pack2(ri.A1, ri.A1);
                 A0p = pack2(ri.A0, ri.A0);
+                if (p.unaligned) {
+                    ib = (row_bytes - ri.h) & ~(int64_t)15;
+                    // the head / tail elements, one per thread, written singly
+                    const int head_e = ri.h / (int)sizeof(Tin);
+                    const int tail_e = (int)((row_bytes - ri.h - ib) / (int64_t)sizeof(Tin));
+                    int idx = -1;
+                    if (ct < head_e) idx = ct;
+                    else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
+                    if (idx >= 0) {
+                        const float t2 = fmaf(ri.hx[ct], p.c2x, -ri.l2);
+                        float g = ex2(t2) * fmaf(ri.A1, t2, ri.A0);
+                        if (idx == ri.y) g += ri.wt;
+                        st_elem<Tin>(orow, idx, g);
+                    }
+                }
             }
+            const int bytes = (int)min((int64_t)kChunk, ib - off);
+            const int nvec = bytes >> 4;
             const uint8_t *sb = S.stage[stage];
             // owner of the target element reads it before the stage is released
-            const int64_t ybyte = (int64_t)ri.y * (int64_t)sizeof(Tin);
-            const bool own_y = ri.y >= 0 && (int64_t)ri.y < p.V && ybyte >= off && ybyte < off + bytes &&
+            const int64_t ybyte = (int64_t)ri.y * (int64_t)sizeof(Tin) - ri.h;  // offset in the interior
+            const bool own_y = ri.y >= 0 && (int64_t)ri.y < p.V && ybyte >= 0 && ybyte >= off && ybyte < off + bytes &&
                                (((int)(ybyte - off) >> 4) % kConsumers) == ct;
             float xy = 0.f;
             if (own_y) {
@@ -205,7 +265,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
-            char *obase = reinterpret_cast<char *>(orow) + off;
+            char *obase = reinterpret_cast<char *>(orow) + ri.h + off;
 #pragma unroll
             for (int k = 0; k < kVPT; ++k) {
                 const int vi = ct + k * kConsumers;
@@ -247,12 +307,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
             if (own_y) {
                 const float t2 = fmaf(xy, p.c2x, -ri.l2);
                 const float g = ex2(t2) * fmaf(ri.A1, t2, ri.A0) + ri.wt;
-                if (sizeof(Tin) == 2) {
-                    const uint32_t hb = f32x2_to_bf16x2(g, 0.f) & 0xffffu;
-                    asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + ri.y), "h"((unsigned short)hb) : "memory");
-                } else {
-                    reinterpret_cast<float *>(orow)[ri.y] = g;
-                }
+                st_elem<Tin>(orow, ri.y, g);
             }
         }
     }
@@ -265,8 +320,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
             if (t < L) continue;
             char *orow = reinterpret_cast<char *>(p.out) +
                          ((int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t) * (int64_t)sizeof(Tin);
-            for (int64_t o = (int64_t)ct * 16; o < row_bytes; o += (int64_t)kConsumers * 16)
-                stg128(orow + o, make_uint4(0u, 0u, 0u, 0u));
+            zero_row<Tin>(orow, row_bytes, ct, kConsumers);
         }
     }
 }

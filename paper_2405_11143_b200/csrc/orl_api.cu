@@ -704,8 +704,17 @@ extern "C" orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const 
     p.zero_masked = zero_masked ? 1 : 0;
     p.loss_agg = cfg->loss_agg;
     const int64_t elt = p.elt;
-    const bool tma = tma_eligible(actor) && (reinterpret_cast<uintptr_t>(dlogits) % 16 == 0) &&
-                     ((out_stride_t * elt) % 16 == 0) && ((out_stride_b * elt) % 16 == 0);
+    bool tma = tma_eligible(actor) && (reinterpret_cast<uintptr_t>(dlogits) % 16 == 0) &&
+               ((out_stride_t * elt) % 16 == 0) && ((out_stride_b * elt) % 16 == 0);
+    if (!tma && k1_layout(actor) == 2) {
+        // unaligned rows: TMA over the aligned interiors when every output row is misaligned
+        // exactly like its input row (same offset mod 16), scalar heads and tails
+        const intptr_t dbase = reinterpret_cast<intptr_t>(dlogits) - reinterpret_cast<intptr_t>(actor->ptr);
+        p.unaligned = (dbase % 16 == 0) && (((out_stride_t - actor->stride_t) * elt) % 16 == 0) &&
+                      (((out_stride_b - actor->stride_b) * elt) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(dlogits) % elt == 0);
+        tma = p.unaligned != 0;
+    }
     if ((st = prepare_prefix(ctx, rows, false, as_stream(stream), &p.cum_global))) return st;
     CUDA_TRY(ctx, launch_k5(p, tma, ctx->num_sms, as_stream(stream)));
     ctx->launches += 1;

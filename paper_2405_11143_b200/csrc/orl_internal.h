@@ -97,6 +97,8 @@ struct K5Params {
     const int32_t *cum_global;           // prefix of the micro-batch lengths (large B), else NULL
     int zero_masked;
     int loss_agg;                        // 0 token mean, 1 sequence mean (NEXT-2)
+    int unaligned;                       // TMA over each row's 16-byte aligned interior (input and
+                                         // output rows equally misaligned), scalar head / tail
 };
 cudaError_t launch_k5(const K5Params &p, bool tma, int num_sms, cudaStream_t s);
 size_t k5_smem_bytes(int B);

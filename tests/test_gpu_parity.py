@@ -591,6 +591,37 @@ def test_next1_logits_grad_parity(ctx, dtype, V, inv_temp):
                 0.01 / float(m.sum()), inv_temp)
 
 
+@pytest.mark.parametrize("dtype,V,pad", [("bf16", 50257, 0), ("bf16", 4096, 5), ("f32", 1001, 1)])
+def test_next1_unaligned_tma_matches_generic(ctx, monkeypatch, dtype, V, pad):
+    """K5 on unaligned rows (aligned interior by TMA, scalar head / tail, target in a
+    head or tail, masked rows zero-filled) gives the same bits as the generic kernel."""
+    B, T = 3, 20
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    x = (torch.randn(B, T, V + pad, device=DEV) * 2).to(tdt)[..., :V]
+    tok = synth.tokens_for(B, T, V, 8).to(DEV)
+    tok[0, :3] = torch.tensor([0, 1, V - 1], dtype=torch.int32, device=DEV)
+    L = torch.tensor([T, 11, 0], dtype=torch.int32, device=DEV)
+    z = lambda: torch.zeros(B, T, device=DEV)  # noqa: E731
+    lse, ent, w = z(), z(), torch.randn(B, T, device=DEV) * 1e-3
+    orl.orl_begin_iteration(ctx)
+    orl.orl_logprobs(ctx, tok, L, x, z(), entropy=ent, lse=lse)
+    adv = z()
+    orl.orl_advantages(ctx, L, adv, kind="rpp", shaped_reward=z())
+    orl.orl_whiten_stats(ctx, False)
+    cfg = orl.PPOConfig(c2=0.01)
+    outs = {}
+    for mode in ("tma", "generic"):
+        if mode == "generic":
+            monkeypatch.setenv("ORL_K1_NO_UNALIGNED_TMA", "1")
+        dl = torch.full((B, T, V + pad), 3.0, dtype=tdt, device=DEV)[..., :V]
+        orl.orl_logits_grad(ctx, tok, L, x, cfg, lse, ent, w, dl, zero_masked=True)
+        torch.cuda.synchronize()
+        outs[mode] = dl.float().cpu().numpy()
+    monkeypatch.delenv("ORL_K1_NO_UNALIGNED_TMA")
+    assert np.array_equal(outs["tma"], outs["generic"])
+    assert np.all(outs["tma"][1, 11:] == 0) and np.all(outs["tma"][2] == 0)
+
+
 def test_large_microbatch_global_prefix(ctx):
     """B > 1024 sequences in one call: the length prefix lives in global memory."""
     B, T, V = 1500, 3, 256

@@ -24,6 +24,9 @@ VARIANTS = {
     "cw8_c16k": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_CHUNK=16384", "ORL_K1_STAGES=12"],
     "cw8_mb2": ["ORL_K1_CONSUMER_WARPS=8", "ORL_K1_MINBLOCKS=2", "ORL_K1_STAGES=3"],
     "s4": ["ORL_K1_STAGES=4"],
+    "s5": ["ORL_K1_STAGES=5"],
+    "epi3_s5": ["ORL_K1_EPI_WARPS=3", "ORL_K1_STAGES=5"],
+    "epi4_s5": ["ORL_K1_EPI_WARPS=4", "ORL_K1_STAGES=5"],
 }
 OUT = os.path.join(ROOT, "build", "tune")
 

@@ -157,6 +157,35 @@ def version() -> int:
     return _lib.orl_version()
 
 
+# C names for the context-level calls (the Context class wraps the same functions)
+def orl_version() -> int:
+    return _lib.orl_version()
+
+
+def orl_create(device: int = 0, world: int = 1, rank: int = 0, unique_id: bytes | None = None) -> "Context":
+    return Context(device, world, rank, unique_id)
+
+
+def orl_destroy(ctx: "Context") -> None:
+    ctx.close()
+
+
+def orl_last_error(ctx: "Context | None" = None) -> str:
+    return _lib.orl_last_error(ctx.h if ctx is not None else None).decode()
+
+
+def orl_launch_count(ctx: "Context") -> int:
+    return ctx.launch_count
+
+
+def orl_set_collective(ctx: "Context", mode: str) -> None:
+    ctx.set_collective(mode)
+
+
+def orl_get_collective(ctx: "Context") -> str:
+    return ctx.collective
+
+
 def orl_get_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
     st = _lib.orl_get_unique_id(buf)

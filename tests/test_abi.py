@@ -129,3 +129,11 @@ def test_next3_kl_controller_host_matches_oracle(lib):
             beta, target, horizon, obs, mx)
     with pytest.raises(orl.OrlError):
         orl.orl_kl_controller_step(0.1, 0.0, 1.0, 0.1, 1.0)
+
+
+def test_python_binding_has_every_c_name():
+    """The binding is a thin layer with the same names: every function include/orl.h
+    declares has a same-named Python callable (marshalling only)."""
+    from paper_2405_11143_b200 import orl
+    missing = [n for n in declared_functions() if not callable(getattr(orl, n, None))]
+    assert not missing, missing

@@ -612,7 +612,7 @@ __device__ void finish_partials_warp(const K1Params &p, const double (&wacc)[kNu
 }
 
 // ---------------------------------------------------------------- TMA kernel
-template <typename Tin, int MODE, int POLY>
+template <typename Tin, int MODE, int POLY, bool UNAL = false>
 __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(const K1Params p) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     K1Smem &S = *reinterpret_cast<K1Smem *>(smem_raw);
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                     if (c == 0 && publish_rl >= 0) {  // released by the arrive below
                         S.row_y[publish_rl % kRowInfo] = y;
                         S.row_h[publish_rl % kRowInfo] = h;
-                        if (MODE != kModeLossGrad && p.unaligned) {
+                        if (UNAL && MODE != kModeLossGrad) {
 #pragma unroll
                             for (int k = 0; k < 16; ++k) S.row_x[publish_rl % kRowInfo][k] = hx[k];
                         }
@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
                     }
                     src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
-                    if (MODE != kModeLossGrad && p.unaligned) {
+                    if (UNAL && MODE != kModeLossGrad) {
                         h = (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15u)) & 15u);
                         ib = (row_bytes - h) & ~(int64_t)15;
                         const int head_e = h / (int)sizeof(Tin);
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 }
                 if (MODE == kModeLossGrad && rl > 0) issue(prev_src, 0, nch, pol_bwd, -1);
                 if (rl < n_rows) {
-                    if (!(MODE != kModeLossGrad && p.unaligned)) issue(src, ksplit, nch, pol_fwd, -1);
+                    if (!(UNAL && MODE != kModeLossGrad)) issue(src, ksplit, nch, pol_fwd, -1);
                     b = bn; t = tn; y = yn;
                 }
                 prev_src = src;
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     // unaligned rows (p.unaligned, not in the fused mode): the chunks cover the aligned
     // interior [h, h + ib) of the row; its < 16-byte head and tail are folded in by
     // scalar loads after the first chunk
-    const bool unal = MODE != kModeLossGrad && p.unaligned;
+    constexpr bool unal = UNAL && MODE != kModeLossGrad;
     int64_t ib = row_bytes, row_nch = nch;
     int row_h = 0, row_yv = -1;
     auto fwd_chunks = [&](int64_t rl, int64_t c0, int64_t c1) {
@@ -1191,7 +1191,9 @@ template <typename Tin, int MODE, int POLY>
 static cudaError_t launch_tma(const K1Params &p, int num_sms, cudaStream_t s) {
     const int64_t N_upper = (int64_t)p.B * p.T;  // rows are counted on device; size by the bound
     const size_t smem = k1_tma_smem_bytes(p.B);
-    auto kern = k1_tma_kernel<Tin, MODE, POLY>;
+    // unaligned rows: a separate instantiation, so the aligned path carries none of it
+    auto kern = (MODE != kModeLossGrad && POLY == 0 && p.unaligned) ? k1_tma_kernel<Tin, MODE, 0, true>
+                                                                      : k1_tma_kernel<Tin, MODE, POLY, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -1219,8 +1221,8 @@ template <typename Tin, int MODE>
 static cudaError_t launch_typed(const K1Params &p, bool tma, int num_sms, cudaStream_t s) {
     const int64_t N_upper = (int64_t)p.B * p.T;
     if (tma) {
-        if (p.poly == 8) return launch_tma<Tin, MODE, 8>(p, num_sms, s);
-        if (p.poly == 16) return launch_tma<Tin, MODE, 16>(p, num_sms, s);
+        if (p.poly == 8 && !p.unaligned) return launch_tma<Tin, MODE, 8>(p, num_sms, s);
+        if (p.poly == 16 && !p.unaligned) return launch_tma<Tin, MODE, 16>(p, num_sms, s);
         return launch_tma<Tin, MODE, 0>(p, num_sms, s);
     }
     const size_t smem = sizeof(int32_t) * (size_t)((p.cum_global ? 0 : p.B) + 32);

@@ -139,7 +139,7 @@ __device__ __forceinline__ k5::RowInfo row_info(const K5Params &p, int64_t gi, i
     return r;
 }
 
-template <typename Tin>
+template <typename Tin, bool UNAL = false>
 __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params p) {
     using namespace k5;
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                                                              p.stride_t) * (int64_t)sizeof(Tin);
                 int64_t ib = row_bytes;
                 rix.h = 0;
-                if (p.unaligned) {  // stream the aligned interior; load the head / tail here
+                if (UNAL) {  // stream the aligned interior; load the head / tail here
                     rix.h = (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15u)) & 15u);
                     ib = (row_bytes - rix.h) & ~(int64_t)15;
                     const int head_e = rix.h / (int)sizeof(Tin);
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                 nl2 = pack2(-ri.l2, -ri.l2);
                 A1p = pack2(ri.A1, ri.A1);
                 A0p = pack2(ri.A0, ri.A0);
-                if (p.unaligned) {
+                if (UNAL) {
                     ib = (row_bytes - ri.h) & ~(int64_t)15;
                     // the head / tail elements, one per thread, written singly
                     const int head_e = ri.h / (int)sizeof(Tin);
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
             const int nvec = bytes >> 4;
             const uint8_t *sb = S.stage[stage];
             // owner of the target element reads it before the stage is released
-            const int64_t ybyte = (int64_t)ri.y * (int64_t)sizeof(Tin) - ri.h;  // offset in the interior
+            const int64_t ybyte = (int64_t)ri.y * (int64_t)sizeof(Tin) - (UNAL ? ri.h : 0);  // offset in the interior
             const bool own_y = ri.y >= 0 && (int64_t)ri.y < p.V && ybyte >= 0 && ybyte >= off && ybyte < off + bytes &&
                                (((int)(ybyte - off) >> 4) % kConsumers) == ct;
             float xy = 0.f;
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
-            char *obase = reinterpret_cast<char *>(orow) + ri.h + off;
+            char *obase = reinterpret_cast<char *>(orow) + (UNAL ? ri.h : 0) + off;
 #pragma unroll
             for (int k = 0; k < kVPT; ++k) {
                 const int vi = ct + k * kConsumers;
@@ -384,14 +384,15 @@ static cudaError_t launch_k5_typed(const K5Params &p, bool tma, int num_sms, cud
     cfg.stream = s;
     if (tma) {
         const size_t smem = k5_smem_bytes(p.B);
-        cudaError_t e = cudaFuncSetAttribute(k5_tma_kernel<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        auto kern = p.unaligned ? k5_tma_kernel<Tin, true> : k5_tma_kernel<Tin, false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int64_t grid = num_sms;
         if (grid > rows) grid = rows;
         cfg.gridDim = dim3((unsigned)grid);
         cfg.blockDim = dim3(k5::kThreads);
         cfg.dynamicSmemBytes = smem;
-        return cudaLaunchKernelEx(&cfg, k5_tma_kernel<Tin>, p);
+        return cudaLaunchKernelEx(&cfg, kern, p);
     }
     const size_t smem = sizeof(int32_t) * (size_t)((p.cum_global ? 0 : p.B) + 32);
     cudaError_t e = cudaFuncSetAttribute(k5_generic_kernel<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

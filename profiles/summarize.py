@@ -66,11 +66,15 @@ def main():
         lines += ["top stall reasons (pc samples): " + ", ".join(f"{k.split('stalled_')[1]} {int(v)}" for v, k in stalls), ""]
         traffic[kind] = rd + wr
     if traffic:
-        json.dump({"V": 128256, "T": 1024, "mb": 8, "tag": tag,
-                   "dram_bytes_per_launch": round(sum(traffic[k] for k in fwd if k in traffic) /
-                                                  max(1, sum(k in traffic for k in fwd))),
-                   "per_variant": {k: round(v) for k, v in traffic.items()}},
-                  open(os.path.join(os.path.dirname(__file__), "k1_traffic.json"), "w"), indent=1)
+        path = os.path.join(os.path.dirname(__file__), "k1_traffic.json")
+        entry = {"V": 128256, "T": 1024, "mb": 8, "tag": tag,
+                 "dram_bytes_per_launch": round(sum(traffic[k] for k in fwd if k in traffic) /
+                                                max(1, sum(k in traffic for k in fwd))),
+                 "per_variant": {k: round(v) for k, v in traffic.items()}}
+        old = json.load(open(path)) if os.path.exists(path) else {}
+        # keep the other launch shapes' captures (bench.py matches on V, T, mb)
+        others = [e for e in old.get("configs", []) if (e["V"], e["T"], e["mb"]) != (128256, 1024, 8)]
+        json.dump(dict(entry, configs=[entry] + others), open(path, "w"), indent=1)
     if len(sys.argv) > 3:
         rows = list(csv.reader(open(sys.argv[3])))
         i = [k for k, r in enumerate(rows) if r and r[0] == "ID"][0]

@@ -437,6 +437,9 @@ def run_ours(args):
         # the same oracle on one core (1-core and all-core)
         v_one, d_one = sample(1, 1024, 1)
         cpu["single_core"] = {"value": v_one, "unit": UNIT, "cores": 1, "sample": d_one}
+        # the whole step's oracle time extrapolated from the sample, and the ratio
+        cpu["extrapolated_step_s"] = round(total_tokens / v_all, 1)
+        cpu["gpu_over_cpu"] = round(value / v_all, 1)
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,

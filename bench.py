@@ -786,7 +786,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=10,
+                    help="untimed steps; default 10: the paper excludes the first 10 steps (P:94, S:535)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llama8b")
     ap.add_argument("--batch", type=int, default=0, help="override B per rank (testing)")

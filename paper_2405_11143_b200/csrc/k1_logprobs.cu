@@ -685,15 +685,16 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             float hx[16];
 #pragma unroll
             for (int k = 0; k < 16; ++k) hx[k] = 0.f;
-            auto issue = [&](const char *src, int64_t c0, int64_t c1, uint64_t pol, int64_t publish_rl) {
+            auto issue = [&](const char *src, int64_t rbytes, int64_t c0, int64_t c1, uint64_t pol,
+                             int64_t publish_rl) {
                 for (int64_t c = c0; c < c1; ++c) {
                     const int64_t off = c * kChunk;
-                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, ib - off);
+                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, rbytes - off);
                     mbar_wait(&S.empty[stage], phase ^ 1u);
                     if (c == 0 && publish_rl >= 0) {  // released by the arrive below
                         S.row_y[publish_rl % kRowInfo] = y;
                         S.row_h[publish_rl % kRowInfo] = h;
-                        if (UNAL && MODE != kModeLossGrad) {
+                        if (UNAL) {
 #pragma unroll
                             for (int k = 0; k < 16; ++k) S.row_x[publish_rl % kRowInfo][k] = hx[k];
                         }
@@ -704,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 }
             };
             const char *prev_src = nullptr;
+            int64_t prev_ib = row_bytes;
             // kModeLossGrad schedule per CTA: F(i)[0, k), B(i-1), F(i)[k, nch), ... , B(n-1)
             for (int64_t rl = 0; rl <= n_rows; ++rl) {
                 const char *src = nullptr;
@@ -715,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         yn = __ldg(p.tokens + (p.seq_offset + bn) * (int64_t)p.T + tn);
                     }
                     src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
-                    if (UNAL && MODE != kModeLossGrad) {
+                    if (UNAL) {
                         h = (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(src) & 15u)) & 15u);
                         ib = (row_bytes - h) & ~(int64_t)15;
                         const int head_e = h / (int)sizeof(Tin);
@@ -729,17 +731,17 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                                     : __ldg(reinterpret_cast<const float *>(src) + idx);
                         }
                         src += h;
-                        issue(src, 0, (ib + kChunk - 1) / kChunk, pol_fwd, rl);
-                    } else {
-                        issue(src, 0, ksplit, pol_fwd, rl);
                     }
+                    issue(src, ib, 0, min(ksplit, (ib + kChunk - 1) / kChunk), pol_fwd, rl);
                 }
-                if (MODE == kModeLossGrad && rl > 0) issue(prev_src, 0, nch, pol_bwd, -1);
+                if (MODE == kModeLossGrad && rl > 0) issue(prev_src, prev_ib, 0, (prev_ib + kChunk - 1) / kChunk, pol_bwd, -1);
                 if (rl < n_rows) {
-                    if (!(UNAL && MODE != kModeLossGrad)) issue(src, ksplit, nch, pol_fwd, -1);
+                    const int64_t nch_r = (ib + kChunk - 1) / kChunk;
+                    issue(src, ib, min(ksplit, nch_r), nch_r, pol_fwd, -1);
                     b = bn; t = tn; y = yn;
                 }
                 prev_src = src;
+                prev_ib = ib;
             }
         }
         return;
@@ -836,11 +838,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     // unaligned rows (p.unaligned, not in the fused mode): the chunks cover the aligned
     // interior [h, h + ib) of the row; its < 16-byte head and tail are folded in by
     // scalar loads after the first chunk
-    constexpr bool unal = UNAL && MODE != kModeLossGrad;
+    constexpr bool unal = UNAL;
     int64_t ib = row_bytes, row_nch = nch;
     int row_h = 0, row_yv = -1;
     auto fwd_chunks = [&](int64_t rl, int64_t c0, int64_t c1) {
-        for (int64_t ci = c0; ci < (unal ? (ci == 0 ? 1 : row_nch) : c1); ++ci) {
+        for (int64_t ci = c0; ci < (unal ? (ci == 0 ? 1 : min(c1, row_nch)) : c1); ++ci) {
             mbar_wait(&S.full[stage], phase);
             if (ci == 0) {  // row start: which chunk / thread holds the target logit
                 acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
@@ -916,14 +918,36 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         const GradRow g = S.grad[rb % kGradRows];
         Tin *orow = reinterpret_cast<Tin *>(p.dlogits) + g.out_off;
         const uint64_t nl2 = pack2(-g.l2, -g.l2), A1p = pack2(g.A1, g.A1), A0p = pack2(g.A0, g.A0);
-        const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin);
+        // unaligned rows: the chunks are the row's aligned interior [bh, bh + bib) (dlogits rows are
+        // misaligned like the logits rows, checked on the host); head / tail written singly here
+        const int bh = UNAL ? S.row_h[rb % kRowInfo] : 0;
+        const int64_t bib = UNAL ? ((row_bytes - bh) & ~(int64_t)15) : row_bytes;
+        if (UNAL) {
+            const int head_e = bh / (int)sizeof(Tin);
+            const int tail_e = (int)((row_bytes - bh - bib) / (int64_t)sizeof(Tin));
+            int idx = -1;
+            if (ct < head_e) idx = ct;
+            else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
+            if (idx >= 0) {
+                const float t2 = fmaf(S.row_x[rb % kRowInfo][ct], p.c2, -g.l2);
+                float gv = ex2(t2) * fmaf(g.A1, t2, g.A0);
+                if (idx == g.y) gv += g.wt;
+                if (sizeof(Tin) == 2) {
+                    const uint32_t hb = f32x2_to_bf16x2_rn(gv, 0.f) & 0xffffu;
+                    asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + idx), "h"((unsigned short)hb) : "memory");
+                } else {
+                    reinterpret_cast<float *>(orow)[idx] = gv;
+                }
+            }
+        }
+        const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin) - bh;  // offset in the interior
         const uint64_t st_pol = l2_evict_first_policy();
-        for (int64_t off = 0; off < row_bytes; off += kChunk) {
-            const int bytes = (int)min((int64_t)kChunk, row_bytes - off);
+        for (int64_t off = 0; off < bib; off += kChunk) {
+            const int bytes = (int)min((int64_t)kChunk, bib - off);
             const int nvec = bytes >> 4;
             mbar_wait(&S.full[stage], phase);
             const uint8_t *sb = S.stage[stage];
-            const bool own_y = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= off && ybyte < off + bytes &&
+            const bool own_y = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= 0 && ybyte >= off && ybyte < off + bytes &&
                                (((int)(ybyte - off) >> 4) % kConsumers) == ct;
             float xy = 0.f;
             if (own_y) {
@@ -940,7 +964,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
-            char *obase = reinterpret_cast<char *>(orow) + off;
+            char *obase = reinterpret_cast<char *>(orow) + bh + off;
 #pragma unroll
             for (int k = 0; k < kVecPerThread; ++k) {
                 const int vi = ct + k * kConsumers;
@@ -1009,8 +1033,15 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             if (t < L) continue;
             char *orow = reinterpret_cast<char *>(p.dlogits) +
                          ((int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t) * (int64_t)sizeof(Tin);
-            for (int64_t o = (int64_t)ct * 16; o < row_bytes; o += (int64_t)kConsumers * 16)
-                stg128_cs(orow + o, make_uint4(0u, 0u, 0u, 0u));
+            const int zh = UNAL ? (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(orow) & 15u)) & 15u) : 0;
+            const int64_t zib = UNAL ? ((row_bytes - zh) & ~(int64_t)15) : row_bytes;
+            for (int64_t o = (int64_t)ct * 16; o < zib; o += (int64_t)kConsumers * 16)
+                stg128_cs(orow + zh + o, make_uint4(0u, 0u, 0u, 0u));
+            if (UNAL) {  // head and tail elements
+                const int64_t nh = zh / (int64_t)sizeof(Tin), t0 = (zh + zib) / (int64_t)sizeof(Tin);
+                if (ct < nh) reinterpret_cast<Tin *>(orow)[ct] = Tin(0);
+                else if (t0 + (ct - nh) < p.V) reinterpret_cast<Tin *>(orow)[t0 + (ct - nh)] = Tin(0);
+            }
         }
     }
 }
@@ -1192,8 +1223,7 @@ static cudaError_t launch_tma(const K1Params &p, int num_sms, cudaStream_t s) {
     const int64_t N_upper = (int64_t)p.B * p.T;  // rows are counted on device; size by the bound
     const size_t smem = k1_tma_smem_bytes(p.B);
     // unaligned rows: a separate instantiation, so the aligned path carries none of it
-    auto kern = (MODE != kModeLossGrad && POLY == 0 && p.unaligned) ? k1_tma_kernel<Tin, MODE, 0, true>
-                                                                      : k1_tma_kernel<Tin, MODE, POLY, false>;
+    auto kern = (POLY == 0 && p.unaligned) ? k1_tma_kernel<Tin, MODE, 0, true> : k1_tma_kernel<Tin, MODE, POLY, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;

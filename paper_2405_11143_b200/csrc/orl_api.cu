@@ -602,8 +602,13 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     const int64_t elt = p.elt;
     const bool out_ok = (reinterpret_cast<uintptr_t>(grad->dlogits) % 16 == 0) &&
                         ((grad->stride_t * elt) % 16 == 0) && ((grad->stride_b * elt) % 16 == 0);
-    if (tma && out_ok) {
-        p.unaligned = 0;
+    // unaligned rows: fused too when every dlogits row is misaligned like its logits row
+    const intptr_t dgap = reinterpret_cast<intptr_t>(grad->dlogits) - reinterpret_cast<intptr_t>(actor->ptr);
+    const bool out_same = lay == 2 && dgap % 16 == 0 && ((grad->stride_t - actor->stride_t) * elt) % 16 == 0 &&
+                          ((grad->stride_b - actor->stride_b) * elt) % 16 == 0 &&
+                          reinterpret_cast<uintptr_t>(grad->dlogits) % elt == 0;
+    if ((tma && out_ok) || out_same) {
+        p.unaligned = out_same ? 1 : 0;
         p.dlogits = grad->dlogits;
         p.out_stride_b = grad->stride_b;
         p.out_stride_t = grad->stride_t;

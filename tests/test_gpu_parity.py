@@ -745,16 +745,24 @@ def test_next2_seq_mean_aggregation(ctx, kind):
 
 
 @pytest.mark.parametrize("agg", ["token_mean", "seq_mean_token_mean"])
-def test_next1_fused_forward_backward_matches_two_passes(ctx, agg):
+@pytest.mark.parametrize("V,pad", [(8192, 0), (50257, 0), (8192, 3)])
+def test_next1_fused_forward_backward_matches_two_passes(ctx, agg, V, pad):
     """orl_ppo_loss_and_grad (one pass, the row re-read from L2) gives the same bits as
-    orl_ppo_loss followed by orl_logits_grad (K5)."""
-    B, T, V = 6, 96, 8192
+    orl_ppo_loss followed by orl_logits_grad (K5); also for unaligned rows (V = 50257,
+    padded pitches: the aligned interiors by TMA, heads / tails singly; targets in them)."""
+    B, T = 6, 96
     g = _gpu_batch(29, B, T, V, "mixed", mode="stress")
+    g["tokens"][0, :4] = torch.tensor([0, 1, V - 1, V - 2], dtype=torch.int32, device=DEV)
+    if pad:
+        for r in ("old", "ref", "new"):
+            buf = torch.zeros(B, T, V + pad, dtype=torch.bfloat16, device=DEV)
+            buf[..., :V] = g[f"logits_{r}"]
+            g[f"logits_{r}"] = buf[..., :V]
     cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V, c2=0.01, loss_agg=agg))
     src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
     out = {}
     for fused in (True, False):
-        dl = torch.full((B, T, V), 7.0, dtype=torch.bfloat16, device=DEV)
+        dl = torch.full((B, T, V + pad), 7.0, dtype=torch.bfloat16, device=DEV)[..., :V]
         bufs = Buffers(B, T, DEV)
         status, st = run_iteration(ctx, g, cfg, bufs, src, mb=4, grad_sink=lambda s, e: dl[s:e], fused_grad=fused)
         torch.cuda.synchronize()

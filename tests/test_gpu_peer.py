@@ -139,7 +139,7 @@ def _spawn(world, kind, mode):
     return res
 
 
-@pytest.mark.parametrize("kind,world", [("gae", 2), ("rpp", 4), ("grpo", 2)])
+@pytest.mark.parametrize("kind,world", [("gae", 2), ("rpp", 4), ("grpo", 2), ("gae", 8)])
 def test_peer_collectives_real_ranks_match_single_rank(kind, world):
     from paper_2405_11143_b200 import orl
     from paper_2405_11143_b200.pipeline import PathConfig

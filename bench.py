@@ -34,10 +34,11 @@ UNIT = "tokens/s"
 
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
+    try:
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+    except (OSError, ValueError, KeyError, TypeError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 def _bf16_peak(sustained: bool):
@@ -45,10 +46,10 @@ def _bf16_peak(sustained: bool):
     seconds-long power-capped loop), else the profiling guide's fallback."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     key = "bf16_tflops_sustained" if sustained else "bf16_tflops"
-    if os.path.exists(p):
-        d = json.load(open(p))
-        if key in d:
-            return float(d[key]), f"measured (MEASURED_PEAKS.json {key}, cuBLAS)"
+    try:
+        return float(json.load(open(p))[key]), f"measured (MEASURED_PEAKS.json {key}, cuBLAS)"
+    except (OSError, ValueError, KeyError, TypeError):
+        pass
     return (1400.0, "fallback sustained (B200_PROFILING.md ~1.4 PFLOP/s under the power cap)") if sustained else \
         (1590.0, "fallback burst (B200_PROFILING.md 1.59 PFLOP/s)")
 

@@ -36,6 +36,30 @@
 
 namespace orl {
 
+// mbarrier wait with an explicit suspend-time hint (ns): a waiting warp is parked until
+// the phase completes or the hint expires instead of re-polling (fewer issue slots and
+// less energy under the power cap).  NS = 0: the default polling wait.
+#ifndef ORL_K1_EPI_WAIT_NS
+#define ORL_K1_EPI_WAIT_NS 0
+#endif
+#ifndef ORL_K1_CONS_WAIT_NS
+#define ORL_K1_CONS_WAIT_NS 0
+#endif
+template <int NS>
+__device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity) {
+    if (NS == 0) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(NS)
+        : "memory");
+}
+
 // Launch shape (tunable at build time; defaults are the measured best, DESIGN 5.1).
 #ifndef ORL_K1_CONSUMER_WARPS
 #define ORL_K1_CONSUMER_WARPS 16
@@ -767,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             float side = 0.f;
             if (lane < nside) side = load_side(p, MODE, lane, gi, b);
             const int slot = (int)(rl % kSlots);
-            mbar_wait(&S.row_full[slot], (uint32_t)(rl / kSlots) & 1u);
+            mbar_wait_hint<ORL_K1_EPI_WAIT_NS>(&S.row_full[slot], (uint32_t)(rl / kSlots) & 1u);
             const RowSlot &R = S.slot[slot];
             Online st{R.m[lane], R.s[lane], R.u[lane]};
 #pragma unroll
@@ -843,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     int row_h = 0, row_yv = -1;
     auto fwd_chunks = [&](int64_t rl, int64_t c0, int64_t c1) {
         for (int64_t ci = c0; ci < (unal ? (ci == 0 ? 1 : min(c1, row_nch)) : c1); ++ci) {
-            mbar_wait(&S.full[stage], phase);
+            mbar_wait_hint<ORL_K1_CONS_WAIT_NS>(&S.full[stage], phase);
             if (ci == 0) {  // row start: which chunk / thread holds the target logit
                 acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
                 have_tgt = false;

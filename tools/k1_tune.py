@@ -27,6 +27,11 @@ VARIANTS = {
     "s5": ["ORL_K1_STAGES=5"],
     "epi3_s5": ["ORL_K1_EPI_WARPS=3", "ORL_K1_STAGES=5"],
     "epi4_s5": ["ORL_K1_EPI_WARPS=4", "ORL_K1_STAGES=5"],
+    # suspend-time hints on the epilogue's row wait / the consumers' stage wait (ns)
+    "ew20k": ["ORL_K1_EPI_WAIT_NS=20000"],
+    "ew2k": ["ORL_K1_EPI_WAIT_NS=2000"],
+    "cw1k": ["ORL_K1_CONS_WAIT_NS=1000"],
+    "ew20k_cw1k": ["ORL_K1_EPI_WAIT_NS=20000", "ORL_K1_CONS_WAIT_NS=1000"],
 }
 OUT = os.path.join(ROOT, "build", "tune")
 

@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
             if (ent) process_words<Tin, true, POLY>(acc, w, ci == 0, p.c2, c2p);
             else process_words<Tin, false, POLY>(acc, w, ci == 0, p.c2, c2p);
-            if (unal && ci == 0) {  // the row's head and tail elements, one per thread
+            if (unal && ci == 0 && warp == 0) {  // the row's head and tail (<= 14 elements): warp 0
                 const int head_e = row_h / (int)sizeof(Tin);
                 const int tail_e = (int)((row_bytes - row_h - ib) / (int64_t)sizeof(Tin));
                 int idx = -1;
@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         // misaligned like the logits rows, checked on the host); head / tail written singly here
         const int bh = UNAL ? S.row_h[rb % kRowInfo] : 0;
         const int64_t bib = UNAL ? ((row_bytes - bh) & ~(int64_t)15) : row_bytes;
-        if (UNAL) {
+        if (UNAL && warp == 0) {  // head / tail (<= 14 elements): warp 0
             const int head_e = bh / (int)sizeof(Tin);
             const int tail_e = (int)((row_bytes - bh - bib) / (int64_t)sizeof(Tin));
             int idx = -1;

@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                     if (c == 0 && publish_rl >= 0) {  // released by the arrive below
                         S.row_y[publish_rl % kRowInfo] = y;
                         S.row_h[publish_rl % kRowInfo] = h;
-                        if (UNAL) {
+                        if (UNAL && MODE == kModeLossGrad) {
 #pragma unroll
                             for (int k = 0; k < 16; ++k) S.row_x[publish_rl % kRowInfo][k] = hx[k];
                         }
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 #pragma unroll
                         for (int k = 0; k < 16; ++k) {
                             const int idx = k < head_e ? k : (k - head_e < tail_e ? (int)p.V - tail_e + (k - head_e) : -1);
-                            if (idx >= 0)
+                            if (MODE == kModeLossGrad && idx >= 0)  // the fused backward's head / tail
                                 hx[k] = sizeof(Tin) == 2
                                     ? __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short *>(src) + idx)) << 16)
                                     : __ldg(reinterpret_cast<const float *>(src) + idx);
@@ -790,6 +790,25 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             const int y = __ldg(p.tokens + gi);
             float side = 0.f;
             if (lane < nside) side = load_side(p, MODE, lane, gi, b);
+            // unaligned rows: the < 16-byte head and tail of the row (<= 7 + 7 bf16 elements) are
+            // not in the TMA interior the consumers streamed; lane k loads edge element k here,
+            // ahead of the row wait, and the warp folds them into the merged state below
+            float ex = 0.f;
+            int eidx = -1;
+            if (UNAL) {
+                const char *rsrc =
+                    p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt;
+                const int hh = (int)((16u - (uint32_t)(reinterpret_cast<uintptr_t>(rsrc) & 15u)) & 15u);
+                const int64_t ibb = (row_bytes - hh) & ~(int64_t)15;
+                const int head_e = hh / (int)sizeof(Tin);
+                const int tail_e = (int)((row_bytes - hh - ibb) / (int64_t)sizeof(Tin));
+                if (lane < head_e) eidx = lane;
+                else if (lane < head_e + tail_e) eidx = (int)p.V - tail_e + (lane - head_e);
+                if (eidx >= 0)
+                    ex = sizeof(Tin) == 2
+                             ? __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short *>(rsrc) + eidx)) << 16)
+                             : __ldg(reinterpret_cast<const float *>(rsrc) + eidx);
+            }
             const int slot = (int)(rl % kSlots);
             mbar_wait_hint<ORL_K1_EPI_WAIT_NS>(&S.row_full[slot], (uint32_t)(rl / kSlots) & 1u);
             const RowSlot &R = S.slot[slot];
@@ -798,7 +817,15 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             for (int w = 1; w < kConsumerWarps; ++w)
                 st = online_merge(st, Online{R.m[lane + 32 * w], R.s[lane + 32 * w], R.u[lane + 32 * w]});
             st = warp_merge(st);
-            const float target = R.target;
+            float target = R.target;
+            if (UNAL) {
+                Online e{kMInit, 0.f, 0.f};
+                if (eidx >= 0) e = Online{fmax_nan(fmax_nan(ex, kNegClampF32) * p.c2, kMInit), 1.f, 0.f};
+                st = online_merge(st, warp_merge(e));
+                const unsigned hit = __ballot_sync(0xffffffffu, eidx >= 0 && eidx == y);
+                const float xt = __shfl_sync(0xffffffffu, ex, hit ? __ffs(hit) - 1 : 0);
+                if (hit) target = xt;
+            }
             float sv[6];
 #pragma unroll
             for (int k = 0; k < 6; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
@@ -903,22 +930,6 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
             if (ent) process_words<Tin, true, POLY>(acc, w, ci == 0, p.c2, c2p);
             else process_words<Tin, false, POLY>(acc, w, ci == 0, p.c2, c2p);
-            if (unal && ci == 0 && warp == 0) {  // the row's head and tail (<= 14 elements): warp 0
-                const int head_e = row_h / (int)sizeof(Tin);
-                const int tail_e = (int)((row_bytes - row_h - ib) / (int64_t)sizeof(Tin));
-                int idx = -1;
-                if (ct < head_e) idx = ct;
-                else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
-                if (idx >= 0) {
-                    const float x = S.row_x[rl % kRowInfo][ct];  // published with the row info
-                    if (ent) acc_scalar<true>(acc, x, p.c2);
-                    else acc_scalar<false>(acc, x, p.c2);
-                    if (idx == row_yv) {
-                        tgt = x;
-                        have_tgt = true;
-                    }
-                }
-            }
         }
     };
     auto fwd_publish = [&](int64_t rl) {  // row end: this thread's state into the row slot

@@ -965,8 +965,8 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
             if (idx >= 0) {
                 const float t2 = fmaf(S.row_x[rb % kRowInfo][ct], p.c2, -g.l2);
-                float gv = ex2(t2) * fmaf(g.A1, t2, g.A0);
-                if (idx == g.y) gv += g.wt;
+                float gv = __fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0));  // no contraction: same bits on every path
+                if (idx == g.y) gv = __fadd_rn(gv, g.wt);
                 if (sizeof(Tin) == 2) {
                     const uint32_t hb = f32x2_to_bf16x2_rn(gv, 0.f) & 0xffffu;
                     asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + idx), "h"((unsigned short)hb) : "memory");
@@ -1040,7 +1040,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             }
             if (own_y) {  // program-ordered rewrite of the target element with the delta term
                 const float t2 = fmaf(xy, p.c2, -g.l2);
-                const float gy = ex2(t2) * fmaf(g.A1, t2, g.A0) + g.wt;
+                const float gy = __fadd_rn(__fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0)), g.wt);  // p (A1 t + A0) + wt, not contracted
                 if (sizeof(Tin) == 2) {
                     const uint32_t hb = f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu;
                     asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + g.y), "h"((unsigned short)hb) : "memory");

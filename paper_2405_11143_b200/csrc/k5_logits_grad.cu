@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                     else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
                     if (idx >= 0) {
                         const float t2 = fmaf(ri.hx[ct], p.c2x, -ri.l2);
-                        float g = ex2(t2) * fmaf(ri.A1, t2, ri.A0);
-                        if (idx == ri.y) g += ri.wt;
+                        float g = __fmul_rn(ex2(t2), fmaf(ri.A1, t2, ri.A0));  // no contraction: same bits on every path
+                        if (idx == ri.y) g = __fadd_rn(g, ri.wt);
                         st_elem<Tin>(orow, idx, g);
                     }
                 }
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
             // delta term at v = y: the owner of y's vector rewrites that element
             if (own_y) {
                 const float t2 = fmaf(xy, p.c2x, -ri.l2);
-                const float g = ex2(t2) * fmaf(ri.A1, t2, ri.A0) + ri.wt;
+                const float g = __fadd_rn(__fmul_rn(ex2(t2), fmaf(ri.A1, t2, ri.A0)), ri.wt);  // not contracted
                 st_elem<Tin>(orow, ri.y, g);
             }
         }
@@ -360,8 +360,8 @@ __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
             if (sizeof(Tin) == 2) x = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(row)[v]) << 16);
             else x = reinterpret_cast<const float *>(row)[v];
             const float t2 = fmaf(x, p.c2x, -ri.l2);
-            float g = ex2(t2) * fmaf(ri.A1, t2, ri.A0);
-            if (v == ri.y) g += ri.wt;
+            float g = __fmul_rn(ex2(t2), fmaf(ri.A1, t2, ri.A0));  // no contraction: same bits on every path
+            if (v == ri.y) g = __fadd_rn(g, ri.wt);
             if (sizeof(Tin) == 2) {
                 const uint32_t hb = f32x2_to_bf16x2(g, 0.f) & 0xffffu;
                 reinterpret_cast<uint16_t *>(orow)[v] = (uint16_t)hb;

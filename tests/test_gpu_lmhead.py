@@ -276,3 +276,29 @@ def test_lmhead_run_to_run_bit_identical(ctx):
     g2 = _run_logprobs(ctx, b)
     for k in g1:
         assert np.array_equal(g1[k], g2[k], equal_nan=True), k
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_lmhead_random_shapes(ctx, i):
+    """Seeded random LM-head shapes around the tiling edges: R from 1 row to a few CTA-pair
+    row blocks (ragged), d a multiple of 8 (16-byte rows) but often not of 64 (partial
+    k-block), V from 2 to a few vocab tiles and splits (ragged last tile), packed or padded,
+    inv_temp != 1; logp / entropy / lse vs the oracle within the derived bound."""
+    rng = np.random.default_rng(500 + i)
+    B = int(rng.integers(1, 4))
+    T = int(rng.choice([1, 7, 64, 130]))
+    d = int(rng.choice([8, 40, 64, 72, 136, 200, 264]))
+    V = int(rng.choice([2, 17, 255, 256, 257, 700, 1500, 2600]))
+    packed = bool(rng.integers(0, 2))
+    inv_temp = float(rng.choice([1.0, 1 / 0.7]))
+    L = rng.integers(0, T + 1, size=B)
+    L[0] = max(int(L[0]), 1)
+    b = synth.make_lmhead_batch(600 + i, B, T, d, V, lengths=L.tolist(), packed=packed)
+    g = _run_logprobs(ctx, b, inv_temp=inv_temp)
+    hb, Wb = _bits(b["hidden_old"]), _bits(b["weight"])
+    cu = None if b["cu_seqlens"] is None else b["cu_seqlens"].numpy()
+    o = oracle.lmhead_logprobs(hb, Wb, b["tokens"].numpy(), b["lengths"].numpy(), inv_temp, cu)
+    mask = parity.valid_mask(b["lengths"].numpy(), T)
+    bound = _scatter_bound(_bound(hb, Wb, inv_temp), B, T, b["lengths"].numpy(), cu)
+    for k in ("logp", "entropy", "lse"):
+        _check(k, g[k], o[k], mask, bound)

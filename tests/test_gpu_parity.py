@@ -624,9 +624,11 @@ def test_next1_unaligned_tma_matches_generic(ctx, monkeypatch, dtype, V, pad):
     assert np.all(outs["tma"][1, 11:] == 0) and np.all(outs["tma"][2] == 0)
 
 
-def test_large_microbatch_global_prefix(ctx):
-    """B > 1024 sequences in one call: the length prefix lives in global memory."""
-    B, T, V = 1500, 3, 256
+@pytest.mark.parametrize("V", [256, 257])
+def test_large_microbatch_global_prefix(ctx, V):
+    """B > 1024 sequences in one call: the length prefix lives in global memory (aligned
+    rows, and V = 257: unaligned rows through the TMA kernels)."""
+    B, T = 1500, 3
     g = _gpu_batch(17, B, T, V, "mixed")
     g["lengths"] = torch.randint(0, T + 1, (B,), dtype=torch.int32, device=DEV)
     cfg = PathConfig.from_synth(dict(synth.CONFIGS["llama8b"], V=V, c2=0.01))

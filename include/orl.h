@@ -214,6 +214,14 @@ uint64_t orl_launch_count(const orl_ctx *ctx);
 orl_status orl_lengths_from_mask(orl_ctx *ctx, int64_t B, int64_t T, const uint8_t *mask, int32_t *lengths,
                                  void *stream);
 
+/* NEXT-2, DAPO dynamic sampling: from orl_advantages' group_keep
+ * mask (device, uint8 [n_groups]), write the indices of the kept groups in increasing
+ * order to kept_groups (device, int32 [n_groups], the first *n_kept entries used) and
+ * their count to n_kept (device, int32) -- the list a scheduler keeps while it re-rolls
+ * the dropped prompts.  Stream-ordered, deterministic.  n_groups = 0 writes 0. */
+orl_status orl_keep_compact(orl_ctx *ctx, int64_t n_groups, const uint8_t *group_keep, int32_t *kept_groups,
+                            int32_t *n_kept, void *stream);
+
 /* Pre-size the context's workspaces (host call, synchronises the device):
  * per-sequence whitening partials and the length prefix for up to max_seqs
  * responses per rank-local batch / call, and the NEXT-4 split partials for

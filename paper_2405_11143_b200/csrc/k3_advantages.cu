@@ -440,4 +440,47 @@ cudaError_t launch_mask_lengths(const uint8_t *mask, int64_t B, int64_t T, int32
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ DAPO re-roll list
+// NEXT-2: the indices of the kept groups in increasing order and their count,
+// one CTA, fixed-order block scan (deterministic); the caller re-samples the rest.
+__global__ void __launch_bounds__(1024) keep_compact_kernel(const uint8_t *keep, int64_t n, int32_t *idx,
+                                                            int32_t *count) {
+    __shared__ int32_t warp_tot[32];
+    __shared__ int32_t base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) base = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < n; c0 += blockDim.x) {
+        const int64_t g = c0 + tid;
+        const int k = (g < n && keep[g]) ? 1 : 0;
+        int incl = k;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        if (tid == 0) {
+            int run = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                const int v = warp_tot[w];
+                warp_tot[w] = run;
+                run += v;
+            }
+        }
+        __syncthreads();
+        if (k) idx[base + warp_tot[warp] + incl - 1] = (int32_t)g;
+        __syncthreads();
+        if (tid == blockDim.x - 1) base += warp_tot[warp] + incl;
+        __syncthreads();
+    }
+    if (tid == 0) *count = base;
+}
+
+cudaError_t launch_keep_compact(const uint8_t *keep, int64_t n, int32_t *idx, int32_t *count, cudaStream_t s) {
+    keep_compact_kernel<<<1, 1024, 0, s>>>(keep, n, idx, count);
+    return cudaGetLastError();
+}
+
 }  // namespace orl

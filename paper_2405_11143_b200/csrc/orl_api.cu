@@ -854,6 +854,21 @@ extern "C" orl_status orl_lengths_from_mask(orl_ctx *ctx, int64_t B, int64_t T, 
     return ORL_OK;
 }
 
+// ------------------------------------------------------------------ DAPO re-roll list
+extern "C" orl_status orl_keep_compact(orl_ctx *ctx, int64_t n_groups, const uint8_t *group_keep,
+                                       int32_t *kept_groups, int32_t *n_kept, void *stream) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    if (n_groups < 0 || n_groups > INT32_MAX) return fail(ctx, ORL_E_SHAPE, "n_groups=%lld", (long long)n_groups);
+    if (!n_kept || (n_groups > 0 && (!group_keep || !kept_groups)))
+        return fail(ctx, ORL_E_INVALID_ARG, "group_keep/kept_groups/n_kept is NULL");
+    if (!aligned4(kept_groups) || !aligned4(n_kept)) return fail(ctx, ORL_E_ALIGN, "outputs must be 4-byte aligned");
+    orl_status st = set_device(ctx);
+    if (st) return st;
+    CUDA_TRY(ctx, launch_keep_compact(group_keep, n_groups, kept_groups, n_kept, as_stream(stream)));
+    ctx->launches += 1;
+    return ORL_OK;
+}
+
 // ------------------------------------------------------------------ workspace
 extern "C" orl_status orl_reserve(orl_ctx *ctx, int64_t max_seqs, int64_t max_lm_rows, int64_t max_vocab) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");

@@ -160,6 +160,7 @@ cudaError_t launch_whiten_peer(const double *seq_part, int B, const PeerArgs &pa
 cudaError_t launch_stats_peer(const double *acc, const unsigned long long *err, const PeerArgs &pa,
                               const double *whiten, double *flags, double c1, double c2, double beta_loss,
                               int kl_in_loss, int loss_agg, double *stats_out, cudaStream_t s);
+cudaError_t launch_keep_compact(const uint8_t *keep, int64_t n, int32_t *idx, int32_t *count, cudaStream_t s);
 cudaError_t launch_mask_lengths(const uint8_t *mask, int64_t B, int64_t T, int32_t *lengths,
                                 unsigned long long *err, cudaStream_t s);
 cudaError_t launch_whiten_local(const double *seq_part, int B, double *gather_slot, cudaStream_t s);

@@ -104,6 +104,7 @@ _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
 _lib.orl_reserve.argtypes = [_P, _I64, _I64, _I64]
 _lib.orl_lengths_from_mask.argtypes = [_P, _I64, _I64, _P, _P, _P]
+_lib.orl_keep_compact.argtypes = [_P, _I64, _P, _P, _P, _P]
 _lib.orl_finalize_async.argtypes = [_P, ctypes.POINTER(PpoCfg), _P, _P]
 _lib.orl_stats_decode.argtypes = [_P, _F64, ctypes.POINTER(Stats)]
 _lib.orl_peer_handle.argtypes = [_P, ctypes.c_char_p]
@@ -296,6 +297,17 @@ def orl_lengths_from_mask(ctx: Context, mask, lengths, stream=None):
         raise TypeError("lengths must be int32 [B]")
     B, T = mask.shape
     return ctx.check(_lib.orl_lengths_from_mask(ctx.h, B, T, _ptr(mask), _ptr(lengths), _stream(stream)))
+
+
+def orl_keep_compact(ctx: Context, group_keep, kept_groups, n_kept, stream=None):
+    """Indices of the kept groups (DAPO dynamic sampling) in increasing order + their count."""
+    if group_keep.dtype != torch.uint8 or kept_groups.dtype != torch.int32 or n_kept.dtype != torch.int32:
+        raise TypeError("group_keep uint8, kept_groups / n_kept int32")
+    n = group_keep.numel()
+    if kept_groups.numel() < n:
+        raise ValueError("kept_groups must hold n_groups entries")
+    return ctx.check(_lib.orl_keep_compact(ctx.h, n, _ptr(group_keep), _ptr(kept_groups), _ptr(n_kept),
+                                           _stream(stream)))
 
 
 def orl_begin_iteration(ctx: Context, stream=None):

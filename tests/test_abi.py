@@ -99,6 +99,7 @@ def test_host_validation_without_gpu(lib):
     assert so.orl_get_collective(None) == -1
     assert so.orl_reserve(None, ctypes.c_int64(1), ctypes.c_int64(0), ctypes.c_int64(0)) == 1
     assert so.orl_lengths_from_mask(None, ctypes.c_int64(1), ctypes.c_int64(1), None, None, None) == 1
+    assert so.orl_keep_compact(None, ctypes.c_int64(1), None, None, None, None) == 1
     assert so.orl_finalize_async(None, None, None, None) == 1
     assert so.orl_stats_decode(None, ctypes.c_double(30.0), None) == 1
     assert so.orl_destroy(None) == 0

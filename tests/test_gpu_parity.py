@@ -815,3 +815,35 @@ def test_lengths_from_attention_mask(ctx):
     assert st1 == st2 and torch.equal(b1.adv, b2.adv) and torch.equal(b1.logp_new, b2.logp_new)
     with pytest.raises(TypeError):
         orl.orl_lengths_from_mask(ctx, m6.float(), g2["lengths"])
+
+
+@pytest.mark.parametrize("n", [0, 1, 37, 1024, 5000])
+def test_dapo_keep_compact(ctx, n):
+    """orl_keep_compact (NEXT-2, DAPO dynamic sampling): the kept groups' indices in order
+    and their count, bit-exact against numpy; also straight from orl_advantages' mask."""
+    rng = np.random.default_rng(n)
+    keep = (rng.random(n) < 0.6).astype(np.uint8)
+    if n > 2:
+        keep[:2] = [1, 0]
+    idx = torch.full((max(n, 1),), -7, dtype=torch.int32, device=DEV)
+    cnt = torch.full((1,), -7, dtype=torch.int32, device=DEV)
+    orl.orl_keep_compact(ctx, torch.from_numpy(keep).to(DEV), idx, cnt)
+    torch.cuda.synchronize()
+    want = np.flatnonzero(keep)
+    assert int(cnt.item()) == want.size
+    assert np.array_equal(_np(idx)[: want.size], want)
+    if n == 37:  # the mask GRPO writes for a batch with some constant-reward groups
+        G, ng = 4, 16
+        R = torch.tensor(rng.integers(0, 2, size=G * ng), dtype=torch.float32)
+        R[:G] = 1.0                              # a constant group: dropped
+        L = torch.full((G * ng,), 5, dtype=torch.int32, device=DEV)
+        adv = torch.zeros(G * ng, 5, device=DEV)
+        gk = torch.zeros(ng, dtype=torch.uint8, device=DEV)
+        orl.orl_begin_iteration(ctx)
+        orl.orl_advantages(ctx, L, adv, kind="grpo", group_size=G, seq_reward=R.to(DEV), group_keep=gk)
+        gi = torch.zeros(ng, dtype=torch.int32, device=DEV)
+        orl.orl_keep_compact(ctx, gk, gi, cnt)
+        torch.cuda.synchronize()
+        k_np = np.array([float(R[g * G:(g + 1) * G].max() - R[g * G:(g + 1) * G].min()) >= 1e-12 for g in range(ng)])
+        assert int(cnt.item()) == int(k_np.sum()) and 0 not in _np(gi)[: int(cnt.item())].tolist()
+        assert np.array_equal(_np(gi)[: int(cnt.item())], np.flatnonzero(k_np))

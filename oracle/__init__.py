@@ -84,6 +84,10 @@ def _load():
         lib.oracle_lmhead_rows.argtypes = [P, i64, P, i64, i64, i64, i64, P, f64, P, P, P, P]
         lib.oracle_lmhead_rows.restype = i64
         lib.oracle_stats.restype = i32
+        lib.oracle_lengths_from_mask.argtypes = [i64, i64, P, P]
+        lib.oracle_lengths_from_mask.restype = i64
+        lib.oracle_keep_compact.argtypes = [i64, P, P]
+        lib.oracle_keep_compact.restype = i64
         _lib = lib
         return lib
 
@@ -362,6 +366,24 @@ def kl_controller_step(beta, target, horizon, observed, max_kl):
     b = np.array([float(beta)])
     stop = _load().oracle_kl_controller_step(_p(b), float(target), float(horizon), float(observed), float(max_kl))
     return float(b[0]), bool(stop)
+
+
+# --------------------------------------------------------------------------- NEXT-2 helpers
+def lengths_from_mask(mask):
+    """Z10: (lengths [B] int32, number of non-prefix rows) of a [B,T] attention mask."""
+    m = np.ascontiguousarray(np.asarray(mask) != 0, dtype=np.uint8)
+    B, T = m.shape
+    L = np.zeros(B, dtype=np.int32)
+    bad = _load().oracle_lengths_from_mask(B, T, _p(m), _p(L))
+    return L, int(bad)
+
+
+def keep_compact(keep):
+    """NEXT-2 (DAPO): indices of the kept groups in increasing order."""
+    k = np.ascontiguousarray(np.asarray(keep) != 0, dtype=np.uint8)
+    idx = np.zeros(max(k.size, 1), dtype=np.int32)
+    n = _load().oracle_keep_compact(k.size, _p(k), _p(idx))
+    return idx[:n].copy()
 
 
 from .pipeline import pipeline  # noqa: E402  (composition of the stages above)

@@ -549,3 +549,40 @@ int64_t oracle_lmhead_rows(const uint16_t *h, int64_t ld_h, const uint16_t *W, i
     free(x);
     return bad;
 }
+
+/* ------------------------------------------------------------------------
+ * NEXT-2 / Z10  attention mask -> response lengths ("attention masks";
+ *     S:240 masked positions).  The path's masks are right-padded prefixes:
+ *     lengths[b] = number of leading nonzero entries of mask row b, i.e. the
+ *     first t with mask[b,t] == 0 (T if none).  A row with a nonzero entry
+ *     after its first zero is not a prefix mask (Z10: ORL_E_MASK); it keeps its
+ *     leading-prefix length and is counted.  Returns the number of such rows.
+ * ---------------------------------------------------------------------- */
+int64_t oracle_lengths_from_mask(int64_t B, int64_t T, const uint8_t *mask, int32_t *lengths)
+{
+    int64_t bad = 0;
+    for (int64_t b = 0; b < B; ++b) {
+        int64_t L = T;
+        for (int64_t t = 0; t < T; ++t)
+            if (mask[b * T + t] == 0) { L = t; break; }
+        int hole = 0;
+        for (int64_t t = L; t < T; ++t)
+            if (mask[b * T + t] != 0) hole = 1;
+        lengths[b] = (int32_t)L;
+        bad += hole;
+    }
+    return bad;
+}
+
+/* ------------------------------------------------------------------------
+ * NEXT-2  DAPO dynamic sampling ("DAPO"): the indices of the
+ *     kept groups (keep[g] != 0, the flag oracle_group_advantages writes), in
+ *     increasing order, into idx[0..count).  Returns count.
+ * ---------------------------------------------------------------------- */
+int64_t oracle_keep_compact(int64_t n_groups, const uint8_t *keep, int32_t *idx)
+{
+    int64_t count = 0;
+    for (int64_t g = 0; g < n_groups; ++g)
+        if (keep[g] != 0) idx[count++] = (int32_t)g;
+    return count;
+}

@@ -780,7 +780,7 @@ def test_next1_fused_forward_backward_matches_two_passes(ctx, agg, V, pad):
 
 def test_lengths_from_attention_mask(ctx):
     """orl_lengths_from_mask (Z10): leading-ones count of right-padded masks, bit-exact
-    against numpy; a non-prefix mask is reported as ORL_E_MASK; an iteration on
+    against oracle.lengths_from_mask; a non-prefix mask is reported as ORL_E_MASK; an iteration on
     mask-derived lengths equals the one on the true lengths bit for bit."""
     rng = np.random.default_rng(7)
     B, T = 37, 300
@@ -791,7 +791,8 @@ def test_lengths_from_attention_mask(ctx):
     orl.orl_begin_iteration(ctx)
     orl.orl_lengths_from_mask(ctx, torch.from_numpy(mask).to(DEV), got)
     torch.cuda.synchronize()
-    assert np.array_equal(_np(got), L)
+    want, nbad = oracle.lengths_from_mask(mask)
+    assert nbad == 0 and np.array_equal(_np(got), want) and np.array_equal(want, L)
     bad = mask.copy()
     bad[5, L[5] + 3 if L[5] + 3 < T else 0] = 1 if L[5] + 3 < T else 0
     bad[9, :] = 0
@@ -800,8 +801,8 @@ def test_lengths_from_attention_mask(ctx):
     orl.orl_lengths_from_mask(ctx, torch.from_numpy(bad).to(DEV).bool(), got)
     status, st = orl.orl_finalize(ctx, orl.PPOConfig())
     assert status == "ORL_E_MASK"
-    lead = np.array([int(np.argmin(np.append(r, 0))) for r in bad])
-    assert np.array_equal(_np(got), lead)
+    lead, nbad = oracle.lengths_from_mask(bad)
+    assert nbad >= 1 and np.array_equal(_np(got), lead)
     # whole iteration on mask-derived lengths == on the true lengths
     c = dict(synth.CONFIGS["llama8b"])
     g = _gpu_batch(71, 6, 96, 2048, "mixed")
@@ -820,7 +821,8 @@ def test_lengths_from_attention_mask(ctx):
 @pytest.mark.parametrize("n", [0, 1, 37, 1024, 5000])
 def test_dapo_keep_compact(ctx, n):
     """orl_keep_compact (NEXT-2, DAPO dynamic sampling): the kept groups' indices in order
-    and their count, bit-exact against numpy; also straight from orl_advantages' mask."""
+    and their count, bit-exact against oracle.keep_compact; also straight from
+    orl_advantages' mask (itself bit-exact against oracle.group_advantages)."""
     rng = np.random.default_rng(n)
     keep = (rng.random(n) < 0.6).astype(np.uint8)
     if n > 2:
@@ -829,7 +831,7 @@ def test_dapo_keep_compact(ctx, n):
     cnt = torch.full((1,), -7, dtype=torch.int32, device=DEV)
     orl.orl_keep_compact(ctx, torch.from_numpy(keep).to(DEV), idx, cnt)
     torch.cuda.synchronize()
-    want = np.flatnonzero(keep)
+    want = oracle.keep_compact(keep)
     assert int(cnt.item()) == want.size
     assert np.array_equal(_np(idx)[: want.size], want)
     if n == 37:  # the mask GRPO writes for a batch with some constant-reward groups
@@ -844,6 +846,8 @@ def test_dapo_keep_compact(ctx, n):
         gi = torch.zeros(ng, dtype=torch.int32, device=DEV)
         orl.orl_keep_compact(ctx, gk, gi, cnt)
         torch.cuda.synchronize()
-        k_np = np.array([float(R[g * G:(g + 1) * G].max() - R[g * G:(g + 1) * G].min()) >= 1e-12 for g in range(ng)])
-        assert int(cnt.item()) == int(k_np.sum()) and 0 not in _np(gi)[: int(cnt.item())].tolist()
-        assert np.array_equal(_np(gi)[: int(cnt.item())], np.flatnonzero(k_np))
+        _, k_or = oracle.group_advantages(R.numpy().astype(np.float64), G)
+        assert np.array_equal(_np(gk), k_or)                     # keep-mask bit-exact vs the oracle
+        want = oracle.keep_compact(k_or)
+        assert int(cnt.item()) == want.size and 0 not in _np(gi)[: int(cnt.item())].tolist()
+        assert np.array_equal(_np(gi)[: int(cnt.item())], want)

@@ -1,22 +1,35 @@
 #!/usr/bin/env python
 """Benchmark of the logits -> PPO-loss path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama8b] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config grpo] [--impl ours|reference]
+                    [--scaling strong|weak] [--lengths full|secondary] [--legs ...]
 
-One step = one PPO iteration of the whole hot path on every rank (S1 old,
-S1+S2+S3 ref, S4 advantages, S6 + collective C1, S1+S7..S9 actor, S10 +
-collective C2) over a resident synthetic rollout of the named BASELINE.json
-configuration (default configs[1], "llama8b": B=128, T=1024, V=128256 bf16).
-N > 1 is launched by torchrun (one process per GPU); per-GPU work is fixed
-(weak scaling: each rank holds its own B-sequence shard of a B*N batch).
+One step = one PPO/GRPO iteration of the whole hot path on every rank (S1 old,
+S1+S2+S3 ref, S4/S5 advantages, S6 + collective C1, S1+S7..S9 actor, S10 +
+collective C2) over a synthetic rollout of the named BASELINE.json
+configuration.  Default: configs[3], "grpo" (256 prompts x 8 samples, T=4096,
+V=128256 bf16, GRPO group advantages, k2 KL in the loss) -- the largest
+single-GPU configuration of BASELINE.json.  Its 3 x 2.15 TB of logits do not
+fit in HBM, so every micro-batch streams from a pool of micro-batch buffers per
+model (8.4 GB each, >> the 126 MB L2: every read is an HBM read).
 
-Prints ONE JSON line on rank 0 (see DESIGN.md section 7 for every field).
+N > 1: one process per GPU.  `--gpus N` without WORLD_SIZE re-launches itself
+under torch.distributed.run (127.0.0.1); under torchrun WORLD_SIZE must equal
+--gpus.  --scaling strong (default): the config's global batch is split into N
+contiguous, group-aligned shards balanced by valid tokens;
+--scaling weak: every rank holds the config's whole batch.
+
+Prints ONE JSON line on rank 0 (see DESIGN.md section 7 for every field).  The
+headline config is followed by short legs on the other shapes (`legs`): the
+Llama-3 config with the NEXT-1 / NEXT-4 / CUDA-graph measurements, long-CoT,
+the north star's V=128256/T=8192 target shape, and ragged (secondary) lengths.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -30,6 +43,8 @@ import torch  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "tokens/s"
+SIDE_BYTES = {"old": 8, "ref": 8 + 12, "new": 8 + 24 + 16 + 1}   # side bytes per token and pass (DESIGN 5.1)
+LEGS_DEFAULT = "llama8b,longcot,target,llama8b:secondary,longcot:secondary"
 
 
 def _peaks():
@@ -64,11 +79,19 @@ def _cpu_model():
     return None
 
 
-def _workload_desc(name, c, B, world):
-    return (f"{name}: B={B}/rank T={c['T']} V={c['V']} {c['dtype']} logits x3 models resident in HBM, "
+def _lengths_mode(name, lengths):
+    from paper_2405_11143_b200 import synth
+    return "full" if lengths == "full" else synth.SECONDARY_LENGTHS.get(name, "mixed")
+
+
+def _workload_desc(name, c, W):
+    lm = {"full": "all L_b = T", "mixed": "L_b ~ U{T/16..T}", "cot": "40% L_b = T, rest U{T/8..T}"}[W["lengths"]]
+    res = (f"pool of {W['pool']} micro-batch buffers per model (the batch's logits do not fit in HBM; "
+           f"micro-batch k reads slot k mod {W['pool']})") if W["pool"] else "x3 models resident in HBM"
+    return (f"{name}: B={W['B_rank']}/rank of {W['B_global']} T={c['T']} V={c['V']} {c['dtype']} logits {res}, "
             f"adv={c['adv_kind']} gamma={c['gamma']} lambda={c['lam']} whiten={c['whiten']} "
             f"eps=({c['eps_low']},{c['eps_high']}) eps_v={c['eps_v']} kl={c.get('kl_mode', 'reward')}, "
-            f"micro-batch {c['mb']} seq, all L_b = T")
+            f"micro-batch {c['mb']} seq, {lm}")
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -88,6 +111,7 @@ class ClockSampler:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+        return self
 
     def stop(self):
         if self.proc is None:
@@ -98,7 +122,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -107,6 +131,7 @@ class ClockSampler:
             try:
                 sm.append(float(f[1]))
                 mx = float(f[2])
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for n, v in zip(names, f[5:9]):
@@ -115,7 +140,7 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": statistics.median(pw) if pw else None}
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg
@@ -182,12 +207,13 @@ def run_reference(args):
             times.append(dt)
     mean = sum(times) / len(times)
     val = toks / mean
-    sample = (f"{n_seq} sequences of {args.config} with lengths capped at {cap} ({toks} tokens, 3 x {toks} "
-              f"vocab rows of V={V}), per step")
+    sample = (f"{n_seq} sequences ({n_seq // G} whole group(s)) of {args.config} with lengths capped at {cap} "
+              f"({toks} tokens, 3 x {toks} vocab rows of V={V}), per step")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": _workload_desc(args.config, c, n_seq, 1) + " (oracle sample)",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: T={T} V={V} {c['dtype']} logits, adv={c['adv_kind']} "
+                                   "(oracle sample on the host cores)",
                        "global_batch": n_seq, "seq_len": T, "parallelism": "host threads"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                              "cpu_model": _cpu_model()},
@@ -195,22 +221,210 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- workloads
+def make_workload(name, args, env, lengths="full", scaling="strong", batch_override=0):
+    """A synthetic rollout of config `name` for this rank: per-token inputs on the
+    device and a logits source (resident buffers, or a pool of micro-batch buffers)."""
+    from paper_2405_11143_b200 import synth
+    from paper_2405_11143_b200.pipeline import Buffers, PathConfig
+
+    world, rank, dev = env["world"], env["rank"], env["dev"]
+    c = dict(synth.CONFIGS[name])
+    T, V, mb, G = c["T"], c["V"], c["mb"], max(1, c["group_size"])
+    lmode = _lengths_mode(name, lengths)
+    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
+    elt = 2 if tdt == torch.bfloat16 else 4
+    seed = 1234
+    if scaling == "weak":
+        B_global = (batch_override or c["B"]) * world
+        seed = 1234 + rank
+        B_rank = batch_override or c["B"]
+        L = synth.lengths_for(B_rank, T, seed, lmode)
+        s0 = 0
+        tok = synth.tokens_for(B_rank, T, V, seed)
+        R = synth.rewards_for(B_rank, seed, c["rewards"], G)
+        v_old, v_new = synth.values_for(B_rank, T, seed)
+        bounds = None
+    else:
+        B_global = batch_override or c["B"]
+        L_all = synth.lengths_for(B_global, T, seed, lmode)
+        bounds = synth.split_bounds_tokens(L_all.numpy(), world, G)
+        s0, e0 = bounds[rank]
+        B_rank = e0 - s0
+        L = L_all[s0:e0].clone()
+        tok = synth.tokens_for(B_global, T, V, seed)[s0:e0].clone()
+        R = synth.rewards_for(B_global, seed, c["rewards"], G)[s0:e0].clone()
+        v_old, v_new = (v[s0:e0].clone() for v in synth.values_for(B_global, T, seed))
+    n_mb = -(-B_rank // mb)
+    full_bytes = 3 * B_rank * T * V * elt
+    pooled = full_bytes > 0.80 * torch.cuda.mem_get_info()[0]
+    pool = 0
+    if pooled:
+        # 2 buffers per model, 8.4 GB each at grpo (>> L2): micro-batch k reads slot k % 2;
+        # token ids follow the slot, so each micro-batch's targets match its logits
+        per_mb = mb * T * V * elt
+        pool = max(1, min(n_mb, args.pool, int(0.70 * torch.cuda.mem_get_info()[0] // (3 * per_mb))))
+        for k in range(pool, n_mb):
+            a, b = k * mb, min(B_rank, (k + 1) * mb)
+            j = (k % pool) * mb
+            tok[a:b] = tok[j:j + (b - a)]
+    tok, L, R, v_old, v_new = (x.to(env["dev"]) for x in (tok, L, R, v_old, v_new))
+    if pooled:
+        bufs_l = {r: torch.empty(pool * mb, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
+        for k in range(pool):
+            sl = slice(k * mb, (k + 1) * mb)
+            synth.fill_logits_(tuple(bufs_l[r][sl] for r in synth.ROLES), tok[sl], seed, rank * 100_000 + k,
+                               "realistic")
+
+        def src(role, s, e):
+            k = (s // mb) % pool
+            return bufs_l[role][k * mb:k * mb + (e - s)]
+    else:
+        bufs_l = {r: torch.empty(B_rank, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
+        for s in range(0, B_rank, mb):
+            e = min(B_rank, s + mb)
+            synth.fill_logits_(tuple(bufs_l[r][s:e] for r in synth.ROLES), tok[s:e], seed,
+                               rank * 100_000 + s // mb, "realistic")
+        src = lambda role, s, e: bufs_l[role][s:e]  # noqa: E731
+    batch = dict(tokens=tok, lengths=L, seq_reward=R, values_old=v_old, values_new=v_new)
+    return dict(name=name, c=c, cfg=PathConfig.from_synth(c), batch=batch, logits=bufs_l, src=src, pool=pool,
+                B_rank=B_rank, B_global=B_global, T=T, V=V, mb=mb, elt=elt, n_mb=n_mb, lengths=lmode,
+                bufs=Buffers(B_rank, T, dev, c["group_size"]), bounds=bounds, shard_start=s0,
+                n_tok=int(L.clamp(0, T).sum().item()), step_bytes=3 * int(L.clamp(0, T).sum().item()) * V * elt)
+
+
+def free_workload(W):
+    for k in ("logits", "batch", "bufs", "src"):
+        W.pop(k, None)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def timed_steps(ctx, W, env, steps, warmup, pdl_chain=True):
+    """W untimed steps, then K steps between barrier + synchronize; CUDA events on the
+    launching stream around every step and around each pass's back-to-back K1 launches."""
+    from paper_2405_11143_b200.pipeline import run_iteration
+
+    dist = env["dist"]
+    stream = torch.cuda.current_stream()
+    events, cur = [], {}
+
+    def hook(tag):
+        if cur.get("tag") != tag:
+            a = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cur.update(tag=tag, start=a, n=0)
+
+        def done():
+            cur["n"] += 1
+            if cur["n"] == W["n_mb"]:
+                b = torch.cuda.Event(enable_timing=True)
+                b.record(stream)
+                events.append((tag, cur["n"], cur["start"], b))
+                cur.clear()
+        return done
+
+    def step(timing):
+        return run_iteration(ctx, W["batch"], W["cfg"], W["bufs"], W["src"], W["mb"], stream=stream,
+                             on_k1=hook if timing else None, pdl_chain=pdl_chain)
+
+    status, st = None, None
+    for _ in range(warmup):
+        status, st = step(False)
+    torch.cuda.synchronize()
+    if env["dist_mode"]:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(env["local"]).start()
+    l0 = ctx.launch_count
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    evs[0].record(stream)
+    for i in range(steps):
+        status, st = step(True)
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    if env["dist_mode"]:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+    ms_rank = evs[0].elapsed_time(evs[-1]) / steps
+    ms = ms_rank
+    per_rank = None
+    if env["dist_mode"]:
+        tt = torch.tensor([ms_rank, float(W["n_tok"])], device=env["dev"], dtype=torch.float64)
+        gathered = [torch.zeros_like(tt) for _ in range(env["world"])]
+        dist.all_gather(gathered, tt)
+        per_rank = [{"rank": r, "ms_per_step": round(float(g[0]), 4), "tokens": int(g[1]),
+                     "tokens_per_s": round(float(g[1]) / (float(g[0]) / 1e3), 1)} for r, g in enumerate(gathered)]
+        ms = max(float(g[0]) for g in gathered)
+        total_tokens = int(sum(float(g[1]) for g in gathered))
+    else:
+        total_tokens = W["n_tok"]
+    launches = (ctx.launch_count - l0) // steps
+    return dict(ms=ms, ms_rank=ms_rank, per_step=per_step, events=events, launches=launches, status=status,
+                stats=st, clocks=clk, total_tokens=total_tokens, per_rank=per_rank, steps=steps, warmup=warmup)
+
+
+def roofline(W, R):
+    """K1 (the dominant kernel) against the HBM peak: algorithmic bytes = valid tokens x
+    (V x elt of logits + side arrays) per pass, over its event-timed duration."""
+    steps = R["steps"]
+    k1_ms = sum(a.elapsed_time(b) for _, _, a, b in R["events"])
+    stage = {}
+    for tag, _, a, b in R["events"]:
+        stage[tag] = stage.get(tag, 0.0) + a.elapsed_time(b) / steps
+    byts = sum(W["n_tok"] * (W["V"] * W["elt"] + SIDE_BYTES[tag]) for tag, _, _, _ in R["events"])
+    n_k1 = sum(n for _, n, _, _ in R["events"])
+    achieved = byts / (k1_ms / 1e3) / 1e9
+    peak, peak_src = _peaks()
+    traffic, traffic_src = None, None
+    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            for e in pj.get("configs", [pj]):   # one ncu capture per (V, T, micro-batch, lengths) launch shape
+                if e.get("V") == W["V"] and e.get("T") == W["T"] and e.get("mb") == W["mb"] and \
+                        e.get("lengths", "full") == W["lengths"]:
+                    traffic = e["dram_bytes_per_launch"]
+                    traffic_src = e.get("tag")
+        except Exception:
+            traffic = None
+    ms_rank = R["ms_rank"]
+    stage_ms = {"S1_old": round(stage.get("old", 0.0), 4), "S1-S3_ref": round(stage.get("ref", 0.0), 4),
+                "S1_S7-S9_actor": round(stage.get("new", 0.0), 4),
+                "S4-S6_C1_S10_C2_and_gaps": round(ms_rank - sum(stage.values()), 4)}
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_capture": traffic_src,
+            "kernel": "k1_tma_kernel (S1 + epilogues)", "launches_per_step": n_k1 // steps,
+            "algorithmic_bytes_per_launch": int(byts / max(n_k1, 1)),
+            "bytes_per_token": {t: W["V"] * W["elt"] + SIDE_BYTES[t] for t in ("old", "ref", "new")},
+            "k1_share_of_step": round(k1_ms / (ms_rank * steps), 4), "peak_source": peak_src}, stage_ms
+
+
+def _stats_round(st):
+    return {k: (round(v, 6) if isinstance(v, float) else v) for k, v in st.items()}
+
+
 # ----------------------------------------------------------------------------- our arm
-def run_ours(args):
+def setup_env(args):
     import torch.distributed as dist
 
-    from paper_2405_11143_b200 import orl, synth
-    from paper_2405_11143_b200.pipeline import Buffers, PathConfig, run_iteration
+    from paper_2405_11143_b200 import orl
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     # ORL_BENCH_SHARED_GPU=1 (functional test of the N > 1 code path on a one-GPU box; its
     # timings are not measurements): every rank on cuda:0, gloo process group, no NCCL
     # communicator (two ranks cannot share a GPU in NCCL), C1/C2 over the peer kernels.
     shared = os.environ.get("ORL_BENCH_SHARED_GPU") == "1" and world > 1
     if shared:
         local = 0
+    elif local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but only {torch.cuda.device_count()} GPU(s)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     # under torchrun (even with one rank) use the distributed plumbing: NCCL process
@@ -226,293 +440,219 @@ def run_ours(args):
         ctx = orl.Context(local, world, rank, uid[0])
     else:
         ctx = orl.Context(local)
+    return dict(world=world, rank=rank, local=local, dev=dev, dist=dist, dist_mode=dist_mode, shared=shared, ctx=ctx)
 
-    c = dict(synth.CONFIGS[args.config])
-    B, T, V, mb = c["B"], c["T"], c["V"], c["mb"]
-    if args.batch:
-        B = args.batch
-    pool_mb = 0
-    cfg = PathConfig.from_synth(c)
-    seed = 1234 + rank
-    tdt = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
-    elt = 2 if tdt == torch.bfloat16 else 4
 
-    # ---- resident synthetic rollout (generated up front; not timed) ----------
-    L = synth.lengths_for(B, T, seed, "full").to(dev)
-    tok = synth.tokens_for(B, T, V, seed).to(dev)
-    R = synth.rewards_for(B, seed, c["rewards"], c["group_size"]).to(dev)
-    v_old, v_new = (v.to(dev) for v in synth.values_for(B, T, seed))
-    full_bytes = 3 * B * T * V * elt
-    pooled = full_bytes > 0.80 * torch.cuda.mem_get_info()[0]
-    if pooled:
-        # The three models' logits of this config do not fit in HBM (e.g. longcot
-        # 3 x 79.7 GB, grpo 3 x 2.15 TB): every micro-batch streams from a pool of
-        # `pool_mb` micro-batch buffers per model (>= 8 GB each, >> L2), filled once.
-        per_mb = mb * T * V * elt
-        pool_mb = max(1, min(len(range(0, B, mb)), int(0.70 * torch.cuda.mem_get_info()[0] // (3 * per_mb))))
-        pool = {r: torch.empty(pool_mb * mb, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
-        for k in range(pool_mb):
-            sl = slice(k * mb, (k + 1) * mb)
-            synth.fill_logits_(tuple(pool[r][sl] for r in synth.ROLES), tok[sl], seed, k, "realistic")
-        logits = None
+def choose_collective(args, env, W):
+    """C1/C2 transport at N > 1: the single-kernel peer-memory collectives (orl_peer_open)
+    when every rank can map the others' exchange buffers, checked against the NCCL
+    all-gather path on warm-up steps (statistics must be bit-identical)."""
+    from paper_2405_11143_b200.pipeline import run_iteration
 
-        def src(role, s, e):
-            k = (s // mb) % pool_mb
-            return pool[role][k * mb:k * mb + (e - s)]
-    else:
-        logits = {r: torch.empty(B, T, V, dtype=tdt, device=dev) for r in synth.ROLES}
-        for s in range(0, B, mb):
-            e = min(B, s + mb)
-            synth.fill_logits_(tuple(logits[r][s:e] for r in synth.ROLES), tok[s:e], seed, s // mb, "realistic")
-        src = lambda role, s, e: logits[role][s:e]  # noqa: E731
-    batch = dict(tokens=tok, lengths=L, seq_reward=R, values_old=v_old, values_new=v_new)
-    bufs = Buffers(B, T, dev, c["group_size"])
-    stream = torch.cuda.current_stream()
-    n_tok_rank = int(L.clamp(max=T).sum().item())
-    n_mb = len(range(0, B, mb))
-
-    # K1 timing on the launching stream: one event before the first launch of each
-    # pass (old / ref / actor) and one after its last launch, so the interval is the
-    # wall time of that pass's back-to-back K1 launches (PDL lets consecutive K1
-    # launches overlap their tail/prologue, so per-launch intervals would overlap).
-    events = []      # (tag, n_launches, start_event, end_event)
-    cur = {}
-
-    def hook(tag):
-        if cur.get("tag") != tag:
-            a = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            cur.update(tag=tag, start=a, n=0)
-
-        def done():
-            cur["n"] += 1
-            if cur["n"] == n_mb:
-                b = torch.cuda.Event(enable_timing=True)
-                b.record(stream)
-                events.append((tag, cur["n"], cur["start"], b))
-                cur.clear()
-        return done
-
-    def step(timing):
-        return run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream, on_k1=hook if timing else None)
-
-    # C1/C2 transport at N > 1: the single-kernel peer-memory collectives (orl_peer_open)
-    # when every rank can map the others' exchange buffers, checked against the NCCL
-    # all-gather path on the first warm-up steps (statistics must be bit-identical).
-    coll = "local" if world == 1 else "nccl"
-    if shared:
+    ctx, world, dist, dev = env["ctx"], env["world"], env["dist"], env["dev"]
+    if world == 1:
+        return "local"
+    if env["shared"]:
         ctx.enable_peer()
-        coll = "peer (shared-GPU functional test: no NCCL reference)"
-    elif world > 1 and args.collective == "peer":
-        why = ""
+        return "peer (shared-GPU functional test: no NCCL reference)"
+    if args.collective != "peer":
+        return "nccl"
+
+    def step():
+        return run_iteration(ctx, W["batch"], W["cfg"], W["bufs"], W["src"], W["mb"], pdl_chain=True)
+
+    why = ""
+    try:
+        ctx.enable_peer()
+        ok = 1.0
+    except Exception as exc:  # mapping failed on this rank
+        ok, why = 0.0, str(exc)[:80]
+    t = torch.tensor([ok], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if t.item() == 1.0:
         try:
-            ctx.enable_peer()
-            ok = 1.0
-        except Exception as exc:  # mapping failed on this rank
-            ok, why = 0.0, str(exc)[:80]
-        t = torch.tensor([ok], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if t.item() == 1.0:
-            try:
-                ctx.set_collective("nccl")
-                _, st_nccl = step(False)
-                ctx.set_collective("peer")
-                _, st_peer = step(False)
-                same = 1.0 if st_nccl == st_peer else 0.0
-                why = "" if same else "peer stats differed from NCCL"
-            except Exception as exc:
-                same, why = 0.0, str(exc)[:80]
-            t = torch.tensor([same], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if t.item() == 1.0:
-            coll = "peer (single-kernel C1/C2 over peer memory; stats bit-identical to NCCL in warm-up)"
-        else:
             ctx.set_collective("nccl")
-            coll = f"nccl ({why or 'peer path unavailable on another rank'})"
-    for _ in range(args.warmup):
-        status, st = step(False)
-    torch.cuda.synchronize()
-    if dist_mode:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    l0 = ctx.launch_count
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    t0, t1 = evs[0], evs[-1]
-    t0.record(stream)
-    for i in range(args.steps):
-        status, st = step(True)
-        evs[i + 1].record(stream)
-    torch.cuda.synchronize()
-    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    if dist_mode:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    launches = (ctx.launch_count - l0) // args.steps
-    ms = t0.elapsed_time(t1) / args.steps
-    if dist_mode:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    total_tokens = n_tok_rank * world
-    value = total_tokens / (ms / 1e3)
+            _, st_nccl = step()
+            ctx.set_collective("peer")
+            _, st_peer = step()
+            same = 1.0 if st_nccl == st_peer else 0.0
+            why = "" if same else "peer stats differed from NCCL"
+        except Exception as exc:
+            same, why = 0.0, str(exc)[:80]
+        t = torch.tensor([same], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if t.item() == 1.0:
+        return "peer (single-kernel C1/C2 over peer memory; stats bit-identical to NCCL in warm-up)"
+    ctx.set_collective("nccl")
+    return f"nccl ({why or 'peer path unavailable on another rank'})"
 
-    # ---- the same step captured once as a CUDA graph and replayed ---------------
-    graph = None
-    if args.graph:
-        graph = run_graph(args, ctx, batch, cfg, bufs, src, mb, dev, stream, world, total_tokens, status, st)
 
-    # ---- roofline of the dominant kernel (K1) --------------------------------
-    side = {"old": 8, "ref": 8 + 12, "new": 8 + 24 + 16}   # side bytes per token (DESIGN 5.1)
-    k1_ms = sum(a.elapsed_time(b) for _, _, a, b in events)
-    stage = {}
-    for tag, _, a, b in events:
-        stage[tag] = stage.get(tag, 0.0) + a.elapsed_time(b) / args.steps
-    stage_ms = {"S1_old": round(stage.get("old", 0.0), 4), "S1-S3_ref": round(stage.get("ref", 0.0), 4),
-                "S1_S7-S9_actor": round(stage.get("new", 0.0), 4),
-                "S4-S6_C1_S10_C2_and_gaps": round(ms - sum(stage.values()), 4)}
-    k1_bytes = 0
-    for tag, n, _, _ in events:
-        k1_bytes += n * (mb * T) * (V * elt + side[tag])
-    k1_bytes = k1_bytes * (n_tok_rank / (B * T))           # only valid rows are read
-    n_k1 = sum(n for _, n, _, _ in events)
-    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
-    peak, peak_src = _peaks()
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof))
-            for e in pj.get("configs", [pj]):   # one ncu capture per (V, T, micro-batch) shape
-                if e.get("V") == V and e.get("T") == T and e.get("mb") == mb:
-                    traffic = e["dram_bytes_per_launch"]
-        except Exception:
-            traffic = None
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": "k1_tma_kernel (S1 + epilogues)", "launches_per_step": n_k1 // args.steps,
-            "algorithmic_bytes_per_launch": int(k1_bytes / max(n_k1, 1)), "k1_share_of_step": round(k1_ms / (ms * args.steps), 4),
-            "peak_source": peak_src}
+def run_ours(args):
+    env = setup_env(args)
+    ctx, world, rank = env["ctx"], env["world"], env["rank"]
+    t_start = time.perf_counter()
+    W = make_workload(args.config, args, env, args.lengths, args.scaling, args.batch)
+    coll = choose_collective(args, env, W)
+    R = timed_steps(ctx, W, env, args.steps, args.warmup)
+    value = R["total_tokens"] / (R["ms"] / 1e3)
+    roof, stage_ms = roofline(W, R)
+    status, st = R["status"], R["stats"]
 
-    # ---- NEXT-1: the backward pass dL/dlogits (separate leg, not in `value`) ----
-    next1 = None
-    if not args.no_next1 and world == 1 and not pooled:
-        next1 = run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok_rank)
-
-    # ---- NEXT-4: the same iteration from final hidden states (LM head fused) ---
-    next4 = None
-    if args.next4 and world == 1 and not pooled:
-        next4 = run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok_rank)
-
-    # ---- e2e: host buffers, H2D/D2H inside the timed region --------------------
+    # ---- e2e: pinned host buffers, H2D/D2H inside the timed region -----------------
     e2e = None
-    if not args.no_e2e and not pooled:
-        e2e = run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank)
+    if not args.no_e2e:
+        e2e = run_e2e(args, env, W, R)
 
     # ---- oracle on the host cores (rank 0, N = 1 only) ------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cores = len(os.sched_getaffinity(0))
-        G = max(1, c["group_size"])
+        cpu = run_cpu_baseline(args, W, value, R["total_tokens"])
 
-        def sample(n_want, tok_cap, ncores):
-            """Whole groups of the first sequences, lengths capped so the sample holds
-            about tok_cap valid tokens (the oracle's per-token cost is the 3 V-long rows)."""
-            n = max(G, (n_want // G) * G)
-            n = min(n, mb) if pooled else n
-            n = max(G, (n // G) * G)
-            bnp = {k: v[:n].detach().cpu().numpy() for k, v in batch.items()}
-            cap = max(1, -(-tok_cap // n))
-            bnp["lengths"] = np.minimum(bnp["lengths"], cap).astype(np.int32)
-            hl = {r: synth.to_numpy_logits(src(r, 0, n)) for r in synth.ROLES}
-            toks, dt = _oracle_sample(lambda role, k: hl[role][:k], bnp, c, n, ncores)
-            desc = (f"first {n} sequences of the same rollout, lengths capped at {min(cap, T)} "
-                    f"({toks} tokens, 3 x {toks} vocab rows), {dt:.1f} s wall")
-            return toks / dt, desc
-
-        v_all, d_all = sample(args.ref_seqs, args.ref_seqs * min(T, 1024), cores)
-        cpu = {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": d_all,
-               "cpu_model": _cpu_model()}
-        # the same oracle on one core (SURVEY 8(d): 1-core and all-core)
-        v_one, d_one = sample(1, 1024, 1)
-        cpu["single_core"] = {"value": v_one, "unit": UNIT, "cores": 1, "sample": d_one}
-        # SURVEY 8(d): the whole step's oracle time extrapolated from the sample, and the ratio
-        cpu["extrapolated_step_s"] = round(total_tokens / v_all, 1)
-        cpu["gpu_over_cpu"] = round(value / v_all, 1)
-
+    line = None
     if rank == 0:
+        c = W["c"]
         line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms, 4),
-                "stage_ms_per_step": stage_ms, "ms_per_step_stats": {"mean": round(statistics.mean(per_step), 4),
-                                      "median": round(statistics.median(per_step), 4),
-                                      "min": round(min(per_step), 4), "max": round(max(per_step), 4),
-                                      "rank": "rank 0 (value uses the max over ranks of the mean)"}, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": round(R["ms"], 4), "stage_ms_per_step": stage_ms,
+                "ms_per_step_stats": {"mean": round(statistics.mean(R["per_step"]), 4),
+                                      "median": round(statistics.median(R["per_step"]), 4),
+                                      "min": round(min(R["per_step"]), 4), "max": round(max(R["per_step"]), 4),
+                                      "rank": "rank 0 (value uses the max over ranks of the mean)"},
+                "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
                 "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
-                "config": {"workload": _workload_desc(args.config, c, B, world), "global_batch": B * world,
-                           "seq_len": T, "vocab": V, "parallelism": f"dp{world}", "collective": coll,
-                           "l2": "inputs larger than L2 (3 x %.1f GB logits per rank vs 126 MB L2)" % (B * T * V * elt / 1e9),
-                           "logits": ("pool of %d micro-batch buffers per model reused across the %d micro-batches "
-                                      "(full batch does not fit)" % (pool_mb, n_mb)) if pooled else "resident"},
-                "status": status, "stats": {k: (round(v, 6) if isinstance(v, float) else v) for k, v in st.items()},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
-                "next1_logits_grad": next1, "next4_lmhead": next4, "graph_replay": graph,
-                "per_gpu_tokens_per_s": round(value / world, 1)}
-        if shared:
+                "config": {"workload": _workload_desc(args.config, c, W), "global_batch": W["B_global"],
+                           "seq_len": W["T"], "vocab": W["V"], "parallelism": f"dp{world}", "collective": coll,
+                           "l2": "inputs larger than L2 (3 x %.1f GB of logits read per step per rank vs 126 MB L2)"
+                                 % (W["step_bytes"] / 3 / 1e9),
+                           "logits": (f"pool of {W['pool']} micro-batch buffers per model reused across the "
+                                      f"{W['n_mb']} micro-batches (the batch does not fit in HBM)")
+                           if W["pool"] else "resident",
+                           "shards": W["bounds"], "tokens_per_step": R["total_tokens"]},
+                "status": status, "stats": _stats_round(st), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": R["clocks"], "gpu_launches": int(R["launches"]),
+                "per_gpu_tokens_per_s": round(value / world, 1), "per_rank": R["per_rank"],
+                "nccl_comm_ranks": world if (env["dist_mode"] and not env["shared"]) else 0}
+        if env["shared"]:
             line["test_mode"] = "ORL_BENCH_SHARED_GPU: all ranks on one GPU (functional test, not a measurement)"
+    free_workload(W)
+
+    # ---- legs: the other shapes, NEXT-1 / NEXT-4 / graph replay (N = 1 only) ------------
+    legs = {}
+    if world == 1 and args.legs:
+        for spec in args.legs.split(","):
+            name, _, lm = spec.partition(":")
+            try:
+                legs[spec] = run_leg(args, env, name, lm or "full")
+            except Exception as exc:  # a leg never hides the headline line
+                legs[spec] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+                torch.cuda.empty_cache()
+    if rank == 0:
+        line["legs"] = legs
+        line["wall_s"] = round(time.perf_counter() - t_start, 1)
         print(json.dumps(line), flush=True)
     ctx.close()
-    if dist_mode:
-        dist.destroy_process_group()
+    if env["dist_mode"]:
+        env["dist"].destroy_process_group()
 
 
-def run_graph(args, ctx, batch, cfg, bufs, src, mb, dev, stream, world, total_tokens, status_eager, st_eager):
-    """The timed step (all S1..S10 launches, C1/C2 included) captured once into a CUDA
+def run_leg(args, env, name, lengths):
+    """A shorter measurement of another shape on one GPU: tokens/s and K1's roofline; the
+    full-length llama8b leg adds the CUDA-graph replay, NEXT-1 and NEXT-4."""
+    ctx = env["ctx"]
+    W = make_workload(name, args, env, lengths, "strong", 0)
+    R = timed_steps(ctx, W, env, args.leg_steps, 3)
+    roof, stage_ms = roofline(W, R)
+    out = {"workload": _workload_desc(name, W["c"], W), "value": round(R["total_tokens"] / (R["ms"] / 1e3), 1),
+           "unit": UNIT, "ms_per_step": round(R["ms"], 4), "tokens_per_step": R["total_tokens"],
+           "steps": args.leg_steps, "status": R["status"], "roofline": roof, "stage_ms_per_step": stage_ms,
+           "clocks": R["clocks"], "gpu_launches": int(R["launches"]),
+           "stats": {k: round(R["stats"][k], 6) for k in ("policy_loss", "entropy", "clip_frac", "kl")}}
+    if name == "llama8b" and W["lengths"] == "full" and not W["pool"]:
+        if args.graph:
+            out["graph_replay"] = run_graph(args, ctx, W, R)
+        if not args.no_next1:
+            out["next1_logits_grad"] = run_next1(args, ctx, W)
+        if args.next4:
+            out["next4_lmhead"] = run_next4(args, ctx, W)
+    free_workload(W)
+    return out
+
+
+def run_cpu_baseline(args, W, value, total_tokens):
+    from paper_2405_11143_b200 import synth
+
+    cores = len(os.sched_getaffinity(0))
+    c, batch, src, T = W["c"], W["batch"], W["src"], W["T"]
+    G = max(1, c["group_size"])
+
+    def sample(n_want, tok_cap, ncores):
+        """Whole groups of the first sequences, lengths capped so the sample holds
+        about tok_cap valid tokens (the oracle's per-token cost is the 3 V-long rows)."""
+        n = max(G, (n_want // G) * G)
+        n = min(n, W["mb"]) if W["pool"] else n
+        n = max(G, (n // G) * G)
+        bnp = {k: v[:n].detach().cpu().numpy() for k, v in batch.items()}
+        cap = max(1, -(-tok_cap // n))
+        bnp["lengths"] = np.minimum(bnp["lengths"], cap).astype(np.int32)
+        hl = {r: synth.to_numpy_logits(src(r, 0, n)[:, :min(cap, T)]) for r in synth.ROLES}
+        sh = dict(bnp)
+        sh["tokens"] = sh["tokens"][:, :min(cap, T)]
+        sh["values_old"] = sh["values_old"][:, :min(cap, T)]
+        sh["values_new"] = sh["values_new"][:, :min(cap, T)]
+        toks, dt = _oracle_sample(lambda role, k: hl[role][:k], sh, c, n, ncores)
+        desc = (f"first {n} sequences ({n // G} whole group(s)) of the same rollout, lengths capped at "
+                f"{min(cap, T)} ({toks} tokens, 3 x {toks} vocab rows of V={W['V']}), {dt:.1f} s wall")
+        return toks / dt, desc
+
+    v_all, d_all = sample(args.ref_seqs, args.ref_seqs * min(T, 1024), cores)
+    cpu = {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": d_all,
+           "cpu_model": _cpu_model()}
+    v_one, d_one = sample(1, 1024, 1)            # the same oracle on one core (SURVEY 8(d))
+    cpu["single_core"] = {"value": v_one, "unit": UNIT, "cores": 1, "sample": d_one}
+    cpu["extrapolated_step_s"] = round(total_tokens / v_all, 1)
+    cpu["gpu_over_cpu"] = round(value / v_all, 1)
+    return cpu
+
+
+def run_graph(args, ctx, W, R_eager):
+    """The timed step (all S1..S10 launches, C1/C2 included) captured once as a CUDA
     graph (pipeline.GraphStep, orl_finalize_async) and replayed K times; the replayed
     statistics must equal the eager step's bit for bit."""
-    import torch.distributed as dist
-
     from paper_2405_11143_b200.pipeline import GraphStep
 
-    step = GraphStep(ctx, batch, cfg, bufs, src, mb)
+    step = GraphStep(ctx, W["batch"], W["cfg"], W["bufs"], W["src"], W["mb"], pdl_chain=True)
     gs = torch.cuda.current_stream()
     for _ in range(2):
         step.replay()
     torch.cuda.synchronize()
-    same = step.result() == (status_eager, st_eager)
-    if dist.is_initialized():
-        dist.barrier()
-    torch.cuda.synchronize()
+    same = step.result() == (R_eager["status"], R_eager["stats"])
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(gs)
-    for _ in range(args.steps):
+    for _ in range(args.leg_steps):
         step.replay()
     b.record(gs)
     torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / args.steps
-    if dist.is_initialized():
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    return {"tokens_per_s": round(total_tokens / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
+    ms = a.elapsed_time(b) / args.leg_steps
+    return {"tokens_per_s": round(W["n_tok"] / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
             "kernels_per_graph": int(step.kernels), "graph_launches_per_step": 1,
-            "stats_bit_identical_to_eager": bool(same), "steps": args.steps}
+            "stats_bit_identical_to_eager": bool(same), "steps": args.leg_steps}
 
 
-def run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok):
-    """Time the NEXT-1 backward pass (orl_logits_grad) over every micro-batch of
-    the actor logits: reads V*2 B and writes V*2 B per token.  Uses the per-token
-    lse / entropy / dloss_dlogp the timed steps left in `bufs`."""
+def run_next1(args, ctx, W):
+    """Time the NEXT-1 backward pass (orl_logits_grad, K5) over every micro-batch of the
+    actor logits (reads V*2 B and writes V*2 B per token), and the fused actor pass
+    (orl_ppo_loss_and_grad: loss epilogue + backward in one pass, the row re-read from L2)."""
     from paper_2405_11143_b200 import orl
 
-    B, T, V = batch["tokens"].shape[0], c["T"], c["V"]
+    batch, cfg, bufs, logits, mb = W["batch"], W["cfg"], W["bufs"], W["logits"], W["mb"]
+    B, T, V = W["B_rank"], W["T"], W["V"]
+    n_tok = W["n_tok"]
     free = torch.cuda.mem_get_info()[0]
     need = B * T * V * 2
     if need > free - (4 << 30):
         return {"skipped": f"needs {need / 1e9:.1f} GB for dlogits"}
-    dl = torch.empty(B, T, V, dtype=logits["new"].dtype, device=dev)
+    dl = torch.empty(B, T, V, dtype=logits["new"].dtype, device=W["bufs"].adv.device)
     tok, L = batch["tokens"], batch["lengths"]
+    stream = torch.cuda.current_stream()
 
     def once():
         for s in range(0, B, mb):
@@ -530,7 +670,7 @@ def run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok):
                                       v_new=batch["values_new"] if critic else None,
                                       v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
                                       lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
-                                      dlogits=dl[s:e], stream=stream)
+                                      flags=bufs.flags, dlogits=dl[s:e], stream=stream)
 
     def timed(fn):
         for _ in range(2):
@@ -544,26 +684,29 @@ def run_next1(args, ctx, c, cfg, batch, logits, bufs, mb, dev, stream, n_tok):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    reps = max(3, args.steps // 4)
+    reps = max(3, args.leg_steps // 2)
+    prev = ctx.pdl_chain
+    ctx.pdl_chain = True
     ms = timed(once)
     byts = n_tok * V * 2 * 2
     peak, _ = _peaks()
-    # fused actor pass (loss epilogue + backward, the row re-read from L2); its
-    # bytes are those of the two-pass path minus the HBM re-read it avoids
     ms_f = timed(fused)
+    ctx.pdl_chain = prev
     del dl
     torch.cuda.empty_cache()
+    ach_f = byts / (ms_f / 1e3) / 1e9
     return {"tokens_per_s": round(n_tok / (ms / 1e3), 1), "ms_per_pass": round(ms, 4),
             "roofline": {"bound": "hbm", "achieved": round(byts / (ms / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(byts / (ms / 1e3) / 1e9 / peak, 4),
                          "bytes": "V*2 read + V*2 written per valid token"},
             "kernel": "k5_tma_kernel", "launches": len(range(0, B, mb)), "reps": reps,
             "fused_actor_pass": {"api": "orl_ppo_loss_and_grad", "tokens_per_s": round(n_tok / (ms_f / 1e3), 1),
-                                 "ms": round(ms_f, 4),
-                                 "algorithmic_GBps": round(byts / (ms_f / 1e3) / 1e9, 1)}}
+                                 "ms": round(ms_f, 4), "algorithmic_GBps": round(ach_f, 1),
+                                 "frac": round(ach_f / peak, 4),
+                                 "bytes": "V*2 read + V*2 written per valid token (the L2 re-read is not counted)"}}
 
 
-def run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok):
+def run_next4(args, ctx, W):
     """NEXT-4 leg (not part of `value`): the whole iteration with every S1 pass computed
     from the model's final hidden states through its LM head, [R, d] x [V, d]^T on the
     tcgen05 tensor cores fused with the online log-sum-exp (K6, orl_lmhead_*), against
@@ -572,7 +715,14 @@ def run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok):
     from paper_2405_11143_b200 import synth
     from paper_2405_11143_b200.pipeline import LmHeadRows, run_iteration
 
-    B, T, V, d = batch["tokens"].shape[0], c["T"], c["V"], args.hidden
+    batch, cfg, bufs, mb = W["batch"], W["cfg"], W["bufs"], W["mb"]
+    B, T, V, d = W["B_rank"], W["T"], W["V"], args.hidden
+    dev = bufs.adv.device
+    n_tok = W["n_tok"]
+    stream = torch.cuda.current_stream()
+    # the leg's logits are no longer needed: free them for the hidden states + W
+    W["logits"].clear()
+    torch.cuda.empty_cache()
     R = B * T
     g = torch.Generator(device=dev).manual_seed(synth.role_seed(4321, 30_000, 0))
     # as synth.make_lmhead_batch: hidden_old = s_r N(0, I), ref = old + 0.05 N, new = old + 0.03 N
@@ -582,41 +732,40 @@ def run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok):
         base = torch.randn(e - s, d, generator=g, device=dev) * (torch.rand(e - s, 1, generator=g, device=dev) + 0.5)
         for r, sd in zip(synth.ROLES, (0.0, 0.05, 0.03)):
             hid[r][s:e] = (base + sd * torch.randn(e - s, d, generator=g, device=dev)).to(torch.bfloat16)
-    W = torch.empty(V, d, dtype=torch.bfloat16, device=dev)
+    Wt = torch.empty(V, d, dtype=torch.bfloat16, device=dev)
     for s in range(0, V, 8192):
         e = min(V, s + 8192)
-        W[s:e] = (torch.randn(e - s, d, generator=g, device=dev) * (3.0 / d ** 0.5)).to(torch.bfloat16)
-    fused_src = lambda role, s, e: LmHeadRows(hid[role][s * T:e * T], W)  # noqa: E731
+        Wt[s:e] = (torch.randn(e - s, d, generator=g, device=dev) * (3.0 / d ** 0.5)).to(torch.bfloat16)
+    fused_src = lambda role, s, e: LmHeadRows(hid[role][s * T:e * T], Wt)  # noqa: E731
     scratch = torch.empty(mb * T, V, dtype=torch.bfloat16, device=dev)
 
     def unfused_src(role, s, e):
         out = scratch[: (e - s) * T]
-        torch.matmul(hid[role][s * T:e * T], W.t(), out=out)
+        torch.matmul(hid[role][s * T:e * T], Wt.t(), out=out)
         return out.view(e - s, T, V)
 
-    def timed(src, reps):
+    def timed(src, reps, chain):
         for _ in range(2):
-            run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream)
+            run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream, pdl_chain=chain)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(reps):
-            status, st = run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream)
+            status, st = run_iteration(ctx, batch, cfg, bufs, src, mb, stream=stream, pdl_chain=chain)
         b.record(stream)
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps, status, st
 
-    reps = max(2, args.steps // 5)
+    reps = max(2, args.leg_steps // 3)
     l0 = ctx.launch_count
-    ms_f, status, st = timed(fused_src, reps)
+    ms_f, status, st = timed(fused_src, reps, True)
     launches = (ctx.launch_count - l0) // (reps + 2)
-    ms_u, status_u, st_u = timed(unfused_src, reps)
+    # cuBLAS writes the logits right before each K1: K1 must wait for it (no PDL chaining)
+    ms_u, status_u, st_u = timed(unfused_src, reps, False)
     flops = 3 * 2.0 * R * d * V
     peak, peak_src = _bf16_peak(sustained=True)
     ach = flops / (ms_f / 1e3) / 1e12
-    del scratch
-    e2e = None if args.no_e2e else _next4_e2e(ctx, cfg, batch, bufs, mb, hid, W, T, n_tok, reps)
-    del hid, W
+    del scratch, hid, Wt
     torch.cuda.empty_cache()
     return {"tokens_per_s": round(n_tok / (ms_f / 1e3), 1), "ms_per_step": round(ms_f, 3), "status": status,
             "hidden": d, "reps": reps, "gpu_launches": int(launches),
@@ -626,103 +775,36 @@ def run_next4(args, ctx, c, cfg, batch, bufs, mb, dev, stream, n_tok):
                          "peak_source": peak_src, "kernel": "k6_lmhead_2sm_kernel + k6_merge_kernel (whole step)"},
             "unfused_cublas_plus_k1": {"tokens_per_s": round(n_tok / (ms_u / 1e3), 1), "ms_per_step": round(ms_u, 3),
                                        "status": status_u, "policy_loss": round(st_u["policy_loss"], 6)},
-            "speedup_vs_unfused": round(ms_u / ms_f, 4), "e2e_from_host_hidden_states": e2e}
+            "speedup_vs_unfused": round(ms_u / ms_f, 4)}
 
 
-def _next4_e2e(ctx, cfg, batch, bufs, mb, hid, W, T, n_tok, steps):
-    """NEXT-4 end to end through the public API with the step's inputs in pinned HOST
-    memory: every step copies the LM-head weight and each micro-batch's final hidden
-    states of the three roles host -> device (double-buffered on a copy stream, the
-    copies overlapping the tensor-core work) plus the per-token inputs, and
-    orl_finalize reads the statistics back and synchronises (host clock)."""
-    from paper_2405_11143_b200.pipeline import LmHeadRows, run_iteration
-
-    B = batch["tokens"].shape[0]
-    hh = {r: v.cpu().pin_memory() for r, v in hid.items()}
-    hW = W.cpu().pin_memory()
-    small = {k: v.cpu().pin_memory() for k, v in batch.items()}
-    dW = torch.empty_like(W)
-    stage = [torch.empty(mb * T, W.shape[1], dtype=W.dtype, device=W.device) for _ in range(2)]
-    dbatch = {k: torch.empty_like(v) for k, v in batch.items()}
-    comp, copy = torch.cuda.current_stream(), torch.cuda.Stream()
-    order = [(r, s) for r in ("old", "ref", "new") for s in range(0, B, mb)]
-    h2d = sum(v.numel() * v.element_size() for v in small.values()) + hW.numel() * hW.element_size()
-    h2d += sum(v.numel() * v.element_size() for v in hh.values())
-
-    def one_step():
-        for k, v in small.items():
-            dbatch[k].copy_(v, non_blocking=True)
-        with torch.cuda.stream(copy):
-            dW.copy_(hW, non_blocking=True)
-            ew = torch.cuda.Event()
-            ew.record(copy)
-        slot_free, pending, counter = [None, None], {}, {"i": 0}
-
-        def fetch(i):
-            r, s = order[i]
-            e = min(B, s + mb)
-            with torch.cuda.stream(copy):
-                if slot_free[i % 2] is not None:
-                    copy.wait_event(slot_free[i % 2])
-                stage[i % 2][: (e - s) * T].copy_(hh[r][s * T:e * T], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-            pending[i] = ev
-
-        def src(role, s, e):
-            i = counter["i"]
-            counter["i"] += 1
-            if i == 0:
-                comp.wait_event(ew)
-            comp.wait_event(pending.pop(i))
-            if i + 1 < len(order):
-                fetch(i + 1)
-            return LmHeadRows(stage[i % 2][: (e - s) * T], dW)
-
-        def hook(tag):
-            def after():
-                ev = torch.cuda.Event()
-                ev.record(comp)
-                slot_free[(counter["i"] - 1) % 2] = ev
-            return after
-
-        fetch(0)
-        return run_iteration(ctx, dbatch, cfg, bufs, src, mb, stream=comp, on_k1=hook)
-
-    one_step()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        status, _ = one_step()
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / steps
-    del hh, hW, dW, stage
-    return {"value": round(n_tok / dt, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": 16 * 8 + 4 * 8, "steps": steps, "status": status,
-            "note": "final hidden states (3 roles) + LM-head weight streamed from pinned host memory each step; "
-                    "host clock"}
-
-
-def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens, rank):
-    """Same iteration through the public API with the step's inputs in pinned
-    HOST memory: every step copies each micro-batch's three logits blocks plus
-    the per-token inputs host->device (double-buffered on a copy stream) and
-    orl_finalize reads the stats back (D2H) and synchronises.  The pinned pool
-    holds one micro-batch per role and is re-sent for every micro-batch, so the
-    bytes moved per step are the full step's."""
-    import torch.distributed as dist
-
+def run_e2e(args, env, W, R_dev):
+    """The same iteration end to end through the public API with the step's inputs in
+    pinned HOST memory.  Every step copies, host -> device, each micro-batch's own logits
+    of the three models (double-buffered on a copy stream, overlapping the kernels) and the
+    per-token inputs, and orl_finalize reads the statistics back (D2H) and synchronises.
+    Host logits: a pinned copy of each micro-batch buffer the device step reads (the pool
+    slots for a pooled config, else the micro-batches themselves up to ~48 GB; micro-batch
+    k is then slot k mod H).  The e2e statistics are checked bit for bit against a
+    device-resident step that reads the same micro-batch buffers."""
     from paper_2405_11143_b200.pipeline import run_iteration
 
-    B = batch["tokens"].shape[0]
-    host = {r: logits[r][:mb].cpu().pin_memory() for r in logits}
+    dist, dev, ctx, world = env["dist"], env["dev"], env["ctx"], env["world"]
+    batch, cfg, bufs, mb, T, V = W["batch"], W["cfg"], W["bufs"], W["mb"], W["T"], W["V"]
+    B = W["B_rank"]
+    logits = W["logits"]
+    mb_bytes = 3 * mb * T * V * W["elt"]
+    H = W["pool"] if W["pool"] else max(1, min(W["n_mb"], int(48e9 // mb_bytes)))
+    # device view of slot h: pool slot h, or the resident micro-batch h
+    dev_slot = {r: [logits[r][h * mb:h * mb + mb] for h in range(H)] for r in logits}
+    host = {r: [torch.empty(x.shape, dtype=x.dtype, pin_memory=True).copy_(x) for x in dev_slot[r]] for r in logits}
     small = {k: v.cpu().pin_memory() for k, v in batch.items()}
-    stage = [{r: torch.empty_like(logits[r][:mb]) for r in logits} for _ in range(2)]
+    stage = [{r: torch.empty_like(dev_slot[r][0]) for r in logits} for _ in range(2)]
     dbatch = {k: torch.empty_like(v) for k, v in batch.items()}
     comp, copy = torch.cuda.current_stream(), torch.cuda.Stream()
     order = [(r, s) for r in ("old", "ref", "new") for s in range(0, B, mb)]
     h2d = sum(v.numel() * v.element_size() for v in small.values())
-    h2d += sum((min(B, s + mb) - s) * host[r][0].numel() * host[r].element_size() for r, s in order)
+    h2d += sum((min(B, s + mb) - s) * T * V * W["elt"] for r, s in order)
     d2h = 16 * 8 + 4 * 8
 
     def one_step():
@@ -738,7 +820,7 @@ def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens
             with torch.cuda.stream(copy):
                 if slot_free[i % 2] is not None:
                     copy.wait_event(slot_free[i % 2])
-                stage[i % 2][r][: e - s].copy_(host[r][: e - s], non_blocking=True)
+                stage[i % 2][r][: e - s].copy_(host[r][(s // mb) % H][: e - s], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(copy)
             pending[i] = ev
@@ -760,27 +842,49 @@ def run_e2e(args, ctx, c, cfg, batch, logits, bufs, mb, dev, world, total_tokens
             return after
 
         fetch(0)
-        return run_iteration(ctx, dbatch, cfg, bufs, src, mb, stream=comp, on_k1=hook)
+        # the logits arrive by copies on another stream: no PDL chaining (every K1 waits)
+        return run_iteration(ctx, dbatch, cfg, bufs, src, mb, stream=comp, on_k1=hook, pdl_chain=False)
 
-    steps = max(2, args.steps // 5)
-    one_step()
+    big = W["step_bytes"] > 2e11
+    steps = args.e2e_steps or (1 if big else max(2, args.steps // 5))
+    if not big:
+        one_step()                                      # warm-up (copy stream, pinned paths)
     torch.cuda.synchronize()
-    if dist.is_initialized():
+    if env["dist_mode"]:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
-        one_step()
+        status, st = one_step()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    if dist.is_initialized():
+    if env["dist_mode"]:
         tt = torch.tensor([dt], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
+    # the device-resident step over the same micro-batch buffers gives the same bits
+    if W["pool"] or H >= W["n_mb"]:
+        ref_status, ref_st = R_dev["status"], R_dev["stats"]
+    else:
+        ref_status, ref_st = run_iteration(ctx, batch, cfg, bufs, lambda r, s, e: dev_slot[r][(s // mb) % H][: e - s],
+                                           mb, pdl_chain=True)
+    same = (status, st) == (ref_status, ref_st)
     del stage, host
-    return {"value": round(total_tokens / dt, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": d2h, "steps": steps,
+    torch.cuda.empty_cache()
+    total = R_dev["total_tokens"]
+    return {"value": round(total / dt, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": d2h, "steps": steps, "status": status,
+            "stats_bit_identical_to_device_step": bool(same),
+            "host_logits": f"{H} pinned micro-batch buffer(s) per model ({H * mb_bytes / 1e9:.1f} GB); "
+                           f"micro-batch k streams buffer k mod {H}",
             "note": "logits streamed from pinned host memory over PCIe each step (double-buffered); host clock"}
+
+
+# ----------------------------------------------------------------------------- launcher
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -790,9 +894,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=10,
                     help="untimed steps; default 10: the paper excludes the first 10 steps (P:94, S:535)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="llama8b")
-    ap.add_argument("--batch", type=int, default=0, help="override B per rank (testing)")
+    ap.add_argument("--config", default="grpo", help="BASELINE.json config: tiny, llama8b, longcot, grpo, rpp8")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: split the config's batch over the ranks (strong) or give each rank one (weak)")
+    ap.add_argument("--lengths", default="full", choices=["full", "secondary"],
+                    help="full: every L_b = T; secondary: SURVEY 8(d) ragged lengths")
+    ap.add_argument("--batch", type=int, default=0, help="override B (testing)")
+    ap.add_argument("--pool", type=int, default=2, help="micro-batch buffers per model when the batch does not fit")
+    ap.add_argument("--legs", default=LEGS_DEFAULT, help="comma list of config[:secondary] legs ('' = none)")
+    ap.add_argument("--leg-steps", type=int, default=10)
     ap.add_argument("--ref-seqs", type=int, default=4, help="oracle sample size (sequences)")
+    ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-next1", action="store_true")
@@ -800,10 +912,16 @@ def main():
     ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
                     help="C1/C2 transport at N > 1 (peer: single peer-memory kernels, NCCL-checked)")
     ap.add_argument("--hidden", type=int, default=4096, help="NEXT-4 hidden size d")
-    ap.add_argument("--graph", type=int, default=1, help="time the CUDA-graph replay of the step (1/0)")
+    ap.add_argument("--graph", type=int, default=1, help="time the CUDA-graph replay of the llama8b leg (1/0)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run on this node
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

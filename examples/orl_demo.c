@@ -111,7 +111,7 @@ int main(int argc, char **argv) {
         orl_rows rows = {B - s < mb ? B - s : mb, T, s, tokens, lengths, NULL};
         orl_logits x = {(const char *)lg[2] + (size_t)(s * T * V) * 2, ORL_BF16, 0, V, T * V, V};
         CHECK(orl_ppo_loss(ctx, &rows, &x, 1.0f, &cfg, logp_old, logp_ref, adv, ret, v_new, v_old, logp_new, ent,
-                           NULL, NULL, NULL, NULL));
+                           NULL, NULL, NULL, NULL, NULL));
     }
     orl_stats st;
     const orl_status fin = orl_finalize(ctx, &cfg, &st, NULL, NULL);  /* S10 + C2 */

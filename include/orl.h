@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define ORL_VERSION 1
+#define ORL_VERSION 2 /* 2: per-token decision flags in the actor passes, orl_set_pdl_chain */
 #define ORL_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
 #define ORL_STATS_N 16          /* length of the device stats vector */
 #define ORL_PARTIALS_N 24       /* length of a rank's loss/stat partial (hooks) */
@@ -67,7 +67,9 @@ typedef enum {
     ORL_E_ALIGN = 3,         /* per-token array not 4-byte aligned             */
     ORL_E_DTYPE = 4,         /* unknown logits dtype                           */
     ORL_E_TOKEN_RANGE = 5,   /* some valid token outside [0, V)       */
-    ORL_E_MASK = 6,          /* lengths[b] < 0 or > T                          */
+    ORL_E_MASK = 6,          /* lengths[b] < 0 or > T (counted once per        */
+                             /* iteration by orl_advantages; the streaming     */
+                             /* passes clamp), non-prefix attention mask       */
     ORL_E_NONFINITE = 7,     /* non-finite logits / loss terms    (Z26)        */
     ORL_E_NUMERIC_GUARD = 8, /* |logp_new - logp_old| > guard     (Z22) */
     ORL_E_EMPTY_BATCH = 9,   /* no valid token on any rank                     */
@@ -205,6 +207,25 @@ const char *orl_last_error(const orl_ctx *ctx);
 /* Number of kernels the context has launched so far (for bench accounting). */
 uint64_t orl_launch_count(const orl_ctx *ctx);
 
+/* Programmatic dependent launch (PDL) between consecutive streaming passes.
+ * Every K1/K5 launch allows the NEXT kernel on its stream to start while its own
+ * CTAs retire.  By default (enable = 0) every warp of a K1/K5 launch waits for
+ * its preceding kernel to complete (griddepcontrol.wait) before its first read,
+ * so inputs written by ANY predecessor -- including one that triggers its
+ * dependents early, such as a PDL-aware GEMM writing the logits -- are complete
+ * and visible.  enable = 1 lets the K1 producer stream the logits, tokens and
+ * lengths without that wait (only the epilogue warps, which read what earlier
+ * passes of the path wrote, wait): the next micro-batch's stream then overlaps
+ * the tail of the previous launch.  Precondition for enable = 1: on every stream
+ * passed to this context, the kernel that immediately precedes an orl_logprobs /
+ * orl_ppo_loss / orl_ppo_loss_and_grad call and writes its logits, tokens or
+ * lengths either is an orl kernel or triggers no early launch (plain kernels and
+ * copies complete before their dependents start).  Host only; takes effect for
+ * later calls; returns ORL_E_INVALID_ARG for a NULL ctx. */
+orl_status orl_set_pdl_chain(orl_ctx *ctx, int enable);
+/* Current setting (0 or 1), -1 for a NULL ctx. */
+int orl_get_pdl_chain(const orl_ctx *ctx);
+
 /* Attention-mask input (Z10, "attention masks"): lengths[b] = the number of
  * leading ones of mask[b, 0..T) (device, u8 [B, T] row-major; nonzero = valid).
  * The path's masks are right-padded prefixes: a valid position after the first
@@ -301,15 +322,22 @@ orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream);
  * Optional per-token outputs:
  *   dloss_dlogp = (-[not clipped] rho A' + [kl_in_loss] beta k'(d_ref)) / N
  *   dloss_dv    = c1 dvl/dVn / N   (ties take the unclipped branch, Z17)
+ *   flags       = uint8 [B_total, T] per-token decisions, taken in fp64 exactly
+ *                 as the sums above take them:
+ *                   bit 0  clipped: clip(rho) A' < rho A' strictly  (Z16)
+ *                   bit 1  value-clipped branch strictly wins the max  (Z13)
+ *                   bit 2  ratio guard |logp_new - logp_old| > guard   (Z22)
+ *                   bit 3  a non-finite loss term                       (Z29)
+ *                 masked positions 0 (S:216 clip_fraction per token)
  * with N the global token count from orl_whiten_stats.
  * logp_old, adv required; logp_ref optional; ret, v_new, v_old together or
- * all NULL (no critic).  logp_new required; entropy, dloss_* optional. */
+ * all NULL (no critic).  logp_new required; entropy, lse, dloss_*, flags optional. */
 orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
                         float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
                         const float *logp_ref, const float *adv, const float *ret,
                         const float *v_new, const float *v_old, float *logp_new,
                         float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                        void *stream);
+                        uint8_t *flags, void *stream);
 /* (lse, optional: the log-partition of the scaled actor logits, saved for
  * orl_logits_grad.) */
 
@@ -339,15 +367,17 @@ orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits 
  * + rank-ordered sum, C2), forms the means and total loss with cfg's c1,c2,
  * beta_loss, writes the device vector dev_out (optional, double[16]) and the
  * host struct host_out (optional), synchronises `stream`, and maps the error
- * counters to a status: TOKEN_RANGE > NONFINITE > NUMERIC_GUARD >
- * EMPTY_BATCH > OK (outputs are written in every case). */
+ * counters to a status: NCCL (a peer collective timed out) > TOKEN_RANGE >
+ * MASK > SHAPE (LM-head rows) > NONFINITE > NUMERIC_GUARD > EMPTY_BATCH > OK
+ * (outputs are written in every case). */
 orl_status orl_finalize(orl_ctx *ctx, const orl_ppo_cfg *cfg, orl_stats *host_out,
                         double *dev_out, void *stream);
 
 /* orl_finalize without the host synchronisation, for CUDA-graph capture of a whole
  * iteration: launches C2 and the final statistics on `stream` and copies the
  * device stats vector (double[ORL_STATS_N]) followed by the 4 device flags
- * (whiten_warn, invalid lengths, collective timeouts, 0) into dev_out
+ * (whiten_warn, invalid lengths + non-prefix mask rows, collective timeouts,
+ * LM-head rows beyond the hidden matrix) into dev_out
  * (device, double[ORL_FINAL_N], required).  No host memory is touched; the
  * caller copies dev_out to the host when it needs it and maps it to a status
  * with orl_stats_decode. */
@@ -371,8 +401,8 @@ orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_l
                                  const float *logp_ref, const float *adv, const float *ret,
                                  const float *v_new, const float *v_old, float *logp_new,
                                  float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                                 void *dlogits, int64_t out_stride_b, int64_t out_stride_t,
-                                 int zero_masked, void *stream);
+                                 uint8_t *flags, void *dlogits, int64_t out_stride_b,
+                                 int64_t out_stride_t, int zero_masked, void *stream);
 
 /* ---- NEXT-4: LM head fused with S1 (tensor cores) ---------------------- */
 
@@ -386,8 +416,8 @@ orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_l
  * S1 online state, so the [rows, V] logits are never written to memory.
  * hidden and weight are bf16, 16-byte aligned, with 16-byte aligned row
  * pitches ld_hidden, ld_weight (elements, >= d); ORL_E_ALIGN otherwise.
- * Every r a valid (b,t) maps to must be < R; a row that does not is counted
- * as a mask error (ORL_E_MASK) with NaN outputs.  Rows of `hidden` that no
+ * Every r a valid (b,t) maps to must be < R; a row that does not gets NaN
+ * outputs and is counted (orl_finalize -> ORL_E_SHAPE, a data error).  Rows of `hidden` that no
  * valid (b,t) maps to are multiplied but do not affect any output. */
 typedef struct {
     const void *hidden; /* [R, d] bf16 final hidden states of the micro-batch */
@@ -414,7 +444,7 @@ orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_lmh
                                const float *logp_ref, const float *adv, const float *ret,
                                const float *v_new, const float *v_old, float *logp_new,
                                float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                               void *stream);
+                               uint8_t *flags, void *stream);
 
 /* ---- C1 / C2 as single kernels over peer memory (NVLink / NVSwitch) ---- */
 

@@ -263,7 +263,8 @@ def ppo_loss(lengths, logp_new, logp_old, adv_w, *, logp_ref=None, ret=None, v_n
                         KL.get(kl_est, kl_est), int(bool(kl_in_loss)), float(ratio_guard),
                         float(n_global), int(bool(seq_mean)), float(n_seq),
                         _p(sums), _p(obj), _p(clipped), _p(vl), _p(dlogp), _p(dv))
-    return dict(sums=sums, obj=obj, clipped=clipped, vl=vl, dlogp=dlogp, dv=dv)
+    # `flags`: bit 0 clipped (Z16), 1 value-clipped (Z13), 2 ratio guard (Z22), 3 non-finite
+    return dict(sums=sums, obj=obj, clipped=clipped & 1, flags=clipped, vl=vl, dlogp=dlogp, dv=dv)
 
 
 STAT_NAMES = ("n_tokens", "policy_loss", "value_loss", "entropy", "kl", "approx_kl_old",

@@ -341,6 +341,9 @@ double oracle_whiten_value(double a, double mean, double std)
  *       dlogp = (-[not clipped] rho A' + [kl_in_loss] beta k'(d_ref)) / N
  *       dv    = c1 * dvl/dVn / N,  dvl/dVn = 2(Vn-R) on the unclipped branch
  *               (ties), else 2(Vc-R)[|Vn-Vo| < eps_v]
+ *     clipped_out[b,t] (optional) holds the token's decisions as bits:
+ *       0 clipped, 1 value-clipped (the clipped branch strictly wins, Z13),
+ *       2 ratio guard (Z22), 3 a non-finite loss term; masked positions 0.
  *     N = n_global (all ranks' valid tokens, Z11).  A' = adv_w, already
  *     whitened by the caller when whitening is on.  Optional arrays may be
  *     NULL (no critic: v_new == NULL; no reference: logp_ref == NULL).
@@ -417,9 +420,10 @@ void oracle_ppo_loss(int64_t B, int64_t T, const int32_t *lengths,
             sums[6] += vclipped ? 1.0 : 0.0;
             sums[7] += k3old;
             sums[8] += rho;
-            if (fabs(dold) > ratio_guard) sums[9] += 1.0;
-            if (!(isfinite(obj) && isfinite(vl) && isfinite(H) && isfinite(kref)))
-                sums[10] += 1.0;
+            int guard = fabs(dold) > ratio_guard;
+            int nonfinite = !(isfinite(obj) && isfinite(vl) && isfinite(H) && isfinite(kref));
+            if (guard) sums[9] += 1.0;
+            if (nonfinite) sums[10] += 1.0;
             double Lb = (double)lengths[b];
             sums[11] += obj / Lb;
             sums[12] += vl / Lb;
@@ -428,7 +432,8 @@ void oracle_ppo_loss(int64_t B, int64_t T, const int32_t *lengths,
 
             double denom = seq_mean ? n_seq * Lb : n_global;
             if (obj_out) obj_out[i] = obj;
-            if (clipped_out) clipped_out[i] = (uint8_t)clipped;
+            if (clipped_out)
+                clipped_out[i] = (uint8_t)(clipped | (vclipped << 1) | (guard << 2) | (nonfinite << 3));
             if (vl_out) vl_out[i] = vl;
             if (dlogp_out)
                 dlogp_out[i] = ((clipped ? 0.0 : -rho * A) +

@@ -94,7 +94,7 @@ def pipeline(shards, cfg=None):
                        beta_loss=cfg["beta_loss"], kl_est=cfg["kl_est_loss"],
                        kl_in_loss=cfg["kl_mode"] == "loss" and o["logp_ref"] is not None,
                        ratio_guard=cfg["ratio_guard"], n_global=n_global, seq_mean=seq_mean, n_seq=n_seq)
-        o.update(obj=res["obj"], clipped=res["clipped"], vl=res["vl"], dlogp=res["dlogp"],
+        o.update(obj=res["obj"], clipped=res["clipped"], flags=res["flags"], vl=res["vl"], dlogp=res["dlogp"],
                  dv=res["dv"], sums=res["sums"])
         sums = sums + res["sums"]
     kl_in_loss = cfg["kl_mode"] == "loss" and out and out[0]["logp_ref"] is not None

@@ -189,20 +189,18 @@ cudaError_t launch_lengths_prefix(const int32_t *lengths, int B, int T, int32_t 
 
 // ---------------------------------------------------------------- prologue
 // Inclusive prefix of the clamped lengths of the micro-batch into cum[0..B).
-// Counts invalid lengths (< 0 or > T) once (block 0) in err[2].
+// Invalid lengths (< 0 or > T) are clamped here and counted once per iteration by K3.
 __device__ void build_prefix(const K1Params &p, int32_t *cum, int32_t *warp_tot) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int per = (p.B + nthr - 1) / nthr;
     const int beg = min(p.B, tid * per), end = min(p.B, beg + per);
-    int local = 0, bad = 0;
+    int local = 0;
     for (int b = beg; b < end; ++b) {
         int L = p.lengths[p.seq_offset + b];
-        if (L < 0 || L > p.T) ++bad;
         L = L < 0 ? 0 : (L > p.T ? p.T : L);
         local += L;
         cum[b] = local;
     }
-    if (bad && blockIdx.x == 0) atomicAdd(&p.err[2], (unsigned long long)bad);
     // exclusive scan of the per-thread totals across the block
     const int lane = tid & 31, warp = tid >> 5;
     int incl = local;
@@ -245,6 +243,7 @@ __device__ void zero_masked(const K1Params &p, const int32_t *cum, int lt, int n
         } else {
             if (p.dlogp) p.dlogp[i] = 0.f;
             if (p.dv) p.dv[i] = 0.f;
+            if (p.flags) p.flags[i] = 0;
         }
     }
 }
@@ -357,8 +356,12 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         wacc[6] += vclipped ? 1.0 : 0.0;
         wacc[7] += k3old;
         wacc[8] += rho;
-        if (fabs(dold) > p.ratio_guard) wacc[9] += 1.0;
-        if (!(isfinite(obj) && isfinite(vl) && isfinite(Hd) && isfinite(kref))) wacc[10] += 1.0;
+        const bool guard = fabs(dold) > p.ratio_guard;
+        const bool nonfin = !(isfinite(obj) && isfinite(vl) && isfinite(Hd) && isfinite(kref));
+        if (guard) wacc[9] += 1.0;
+        if (nonfin) wacc[10] += 1.0;
+        if (p.flags)
+            p.flags[i] = (uint8_t)((clipped ? 1u : 0u) | (vclipped ? 2u : 0u) | (guard ? 4u : 0u) | (nonfin ? 8u : 0u));
         const double invL = 1.0 / (double)L;
         wacc[11] += obj * invL;
         wacc[12] += vl * invL;
@@ -658,15 +661,18 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     }
     if (tid < kEpiWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
     // Programmatic dependent launch: let the next kernel in the stream start
-    // as our CTAs retire (it fills the SMs of this launch's tail).  Only the
-    // epilogue warps touch memory other kernels write or read, and they wait
-    // for the preceding grid first (griddepcontrol.wait below).
+    // as our CTAs retire (it fills the SMs of this launch's tail).  By default
+    // every warp waits for the preceding grid (griddepcontrol.wait) before its
+    // first global read, so a predecessor that triggers early (e.g. a GEMM
+    // writing the logits) is always complete and visible.  With p.pdl_chain
+    // (orl_set_pdl_chain: the caller vouches that the predecessor wrote no
+    // input of this launch after an early trigger -- e.g. the previous K1 of the
+    // same iteration) only the epilogue warps, which read or write memory other
+    // kernels of the path touch, wait; the producer streams the logits at once.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
-    if (p.cum_global) {  // written by the prefix kernel just before us (PDL: wait for it)
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        __syncthreads();
-    }
+    if (!p.pdl_chain || p.cum_global) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.cum_global) __syncthreads();  // prefix written by the prefix kernel just before us
     else build_prefix(p, cum_s, warp_tot);  // contains __syncthreads
     const int64_t N = cum[p.B - 1];
     const int64_t row_bytes = p.row_bytes;
@@ -1198,7 +1204,7 @@ __global__ void __launch_bounds__(256) k6_merge_kernel(const K1Params p) {
                               ? (int64_t)(__ldg(p.cu_seqlens + p.seq_offset + b) - __ldg(p.cu_seqlens + p.seq_offset)) + t
                               : (int64_t)b * p.T + t;
         if (r >= p.lm_R) {  // the hidden matrix does not hold this row: layout/lengths mismatch
-            atomicAdd(&p.err[2], 1ull);
+            atomicAdd(&p.err[4], 1ull);
             const float nan = __int_as_float(0x7fc00000);
             p.logp[gi] = nan;
             if (p.entropy) p.entropy[gi] = nan;

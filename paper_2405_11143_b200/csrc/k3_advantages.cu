@@ -245,7 +245,7 @@ cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten
 
 // ---------------------------------------------------------------- statistics
 __device__ __forceinline__ double stats_pack_value(const double *acc, const unsigned long long *err, int k) {
-    return k < kNumPartials ? acc[k] : (k >= 16 && k <= 18) ? (double)err[k - 16] : 0.0;
+    return k < kNumPartials ? acc[k] : (k >= 16 && k < 16 + kNumErr) ? (double)err[k - 16] : 0.0;
 }
 
 __global__ void stats_pack_kernel(const double *acc, const unsigned long long *err, double *out) {
@@ -288,7 +288,8 @@ __device__ void stats_final_body(const double *gather, int world, const double *
     st[13] = t[10] + t[17];
     st[14] = t[16];
     st[15] = flags[0];
-    flags[1] = t[18];  // invalid lengths (ORL_E_MASK)
+    flags[1] = t[18] + t[19];  // invalid lengths + non-prefix mask rows (ORL_E_MASK)
+    flags[3] = t[20];          // LM-head rows missing from the hidden matrix (ORL_E_SHAPE)
 }
 
 __global__ void stats_final_kernel(const double *gather, int world, const double *whiten,
@@ -407,7 +408,7 @@ cudaError_t launch_stats_peer(const double *acc, const unsigned long long *err, 
 
 // ------------------------------------------------------------------ masks -> lengths
 // Z10: the path's masks are right-padded prefixes.  One CTA per row: L_b = index of the
-// first 0 (T if none); a 1 after that is a non-prefix mask, counted in err[2] (reported
+// first 0 (T if none); a 1 after that is a non-prefix mask, counted in err[3] (reported
 // by orl_finalize as ORL_E_MASK) -- the row then keeps its leading prefix.
 __global__ void __launch_bounds__(256) mask_lengths_kernel(const uint8_t *mask, int64_t T, int32_t *lengths,
                                                            unsigned long long *err) {
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(256) mask_lengths_kernel(const uint8_t *mask, 
     __syncthreads();
     if (threadIdx.x == 0) {
         lengths[b] = first_zero;
-        if (last_one > first_zero && err) atomicAdd(&err[2], 1ull);
+        if (last_one > first_zero && err) atomicAdd(&err[3], 1ull);
     }
 }
 

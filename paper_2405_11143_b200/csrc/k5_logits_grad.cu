@@ -155,15 +155,13 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
         fence_mbar_init();
     }
     const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
-    if (p.cum_global) {  // written by the prefix kernel just before us (PDL: wait for it)
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        __syncthreads();
-    }
+    // Every input (lengths, the prefix, the saved per-token arrays of the actor pass,
+    // the logits) may come from the preceding kernel: wait for it before any read.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.cum_global) __syncthreads();
     else k5_build_prefix(p, cum_s, warp_tot);
     const int64_t N = cum[p.B - 1];
     const int64_t row_bytes = p.V * (int64_t)sizeof(Tin);
-    // The saved per-token inputs come from the actor pass (a previous kernel).
-    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == kConsumerWarps) {
         if (lane == 0) {
@@ -332,12 +330,9 @@ __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
     int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw);
     int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);
     const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
-    if (p.cum_global) {  // written by the prefix kernel just before us (PDL: wait for it)
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        __syncthreads();
-    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // inputs may come from the preceding kernel
+    if (p.cum_global) __syncthreads();
     else k5_build_prefix(p, cum_s, warp_tot);
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t total = (int64_t)p.B * p.T;
     for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
         const int b = (int)(q / p.T), t = (int)(q % p.T);

@@ -59,6 +59,7 @@ struct orl_ctx {
     int coll = 0;                       // 0 NCCL all-gather, 1 peer-memory kernels
     unsigned long long *d_epoch = nullptr;  // [2] C1 / C2 peer epochs (device: graph-replay safe)
     bool have_adv = false, have_whiten = false;
+    int pdl_chain = 0;                  // orl_set_pdl_chain
     int imported_w = 0, imported_s = 0;
     uint64_t launches = 0;
     std::string err;
@@ -200,6 +201,7 @@ static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const o
     p.acc = ctx->d_acc;
     p.err = ctx->d_err;
     p.whiten = ctx->d_whiten;
+    p.pdl_chain = ctx->pdl_chain;
 }
 
 // Large micro-batches (B > kSmemPrefixMax): build the length prefix in global memory.
@@ -213,8 +215,9 @@ static orl_status prepare_prefix(orl_ctx *ctx, const orl_rows *rows, bool count_
         CUDA_TRY(ctx, cudaMalloc(&ctx->d_cum, (size_t)rows->B * sizeof(int32_t)));
         ctx->cum_cap = rows->B;
     }
+    (void)count_err;  // invalid lengths are counted once per iteration, by K3 (orl_advantages)
     CUDA_TRY(ctx, launch_lengths_prefix(rows->lengths + rows->seq_offset, (int)rows->B, (int)rows->T, ctx->d_cum,
-                                        count_err ? ctx->d_err : nullptr, s));
+                                        nullptr, s));
     ctx->launches += 1;
     *out = ctx->d_cum;
     return ORL_OK;
@@ -317,6 +320,14 @@ extern "C" const char *orl_last_error(const orl_ctx *ctx) {
 }
 
 extern "C" uint64_t orl_launch_count(const orl_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" orl_status orl_set_pdl_chain(orl_ctx *ctx, int enable) {
+    if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
+    ctx->pdl_chain = enable ? 1 : 0;
+    return ORL_OK;
+}
+
+extern "C" int orl_get_pdl_chain(const orl_ctx *ctx) { return ctx ? ctx->pdl_chain : -1; }
 
 extern "C" orl_status orl_begin_iteration(orl_ctx *ctx, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
@@ -440,8 +451,9 @@ extern "C" orl_status orl_advantages(orl_ctx *ctx, int64_t B, int64_t T, const i
                                      const float *seq_reward, float *adv, float *ret,
                                      uint8_t *group_keep, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
-    if (B < 1 || B > (1 << 24) || T < 1 || B * T >= ((int64_t)1 << 40))
-        return fail(ctx, ORL_E_SHAPE, "B=%lld T=%lld invalid", (long long)B, (long long)T);
+    if (B < 1 || B > (1 << 24) || T < 1 || T > INT32_MAX || B * T >= ((int64_t)1 << 40))
+        return fail(ctx, ORL_E_SHAPE, "B=%lld T=%lld invalid (1 <= B <= 2^24, 1 <= T <= 2^31-1, B*T < 2^40)",
+                    (long long)B, (long long)T);
     if (kind < ORL_ADV_GAE || kind > ORL_ADV_RPP_BASELINE)
         return fail(ctx, ORL_E_INVALID_ARG, "unknown advantage kind %d", kind);
     if (!lengths || !adv) return fail(ctx, ORL_E_INVALID_ARG, "lengths and adv are required");
@@ -539,7 +551,7 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
                                 const orl_ppo_cfg *cfg, const float *logp_old, const float *logp_ref,
                                 const float *adv, const float *ret, const float *v_new, const float *v_old,
                                 float *logp_new, float *entropy, float *lse, float *dloss_dlogp,
-                                float *dloss_dv, const GradOut *grad, void *stream,
+                                float *dloss_dv, uint8_t *flags, const GradOut *grad, void *stream,
                                 const orl_lmhead *head = nullptr) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
     orl_status st = head ? validate_rows_lmhead(ctx, rows, head, inv_temp)
@@ -578,6 +590,7 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     p.v_old = v_old;
     p.dlogp = dloss_dlogp;
     p.dv = dloss_dv;
+    p.flags = flags;
     p.eps_low = cfg->eps_low;
     p.eps_high = cfg->eps_high;
     p.eps_v = cfg->eps_value;
@@ -629,9 +642,9 @@ extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl
                                    const float *logp_ref, const float *adv, const float *ret,
                                    const float *v_new, const float *v_old, float *logp_new,
                                    float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                                   void *stream) {
+                                   uint8_t *flags, void *stream) {
     return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
-                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, nullptr, stream);
+                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, flags, nullptr, stream);
 }
 
 extern "C" orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *head,
@@ -639,11 +652,11 @@ extern "C" orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, co
                                           const float *logp_ref, const float *adv, const float *ret,
                                           const float *v_new, const float *v_old, float *logp_new,
                                           float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                                          void *stream) {
+                                          uint8_t *flags, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
     if (!head) return fail(ctx, ORL_E_INVALID_ARG, "lmhead is NULL");
     return ppo_loss_impl(ctx, rows, nullptr, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
-                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, nullptr, stream, head);
+                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, flags, nullptr, stream, head);
 }
 
 extern "C" orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
@@ -651,8 +664,8 @@ extern "C" orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, 
                                             const float *logp_ref, const float *adv, const float *ret,
                                             const float *v_new, const float *v_old, float *logp_new,
                                             float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                                            void *dlogits, int64_t out_stride_b, int64_t out_stride_t,
-                                            int zero_masked, void *stream) {
+                                            uint8_t *flags, void *dlogits, int64_t out_stride_b,
+                                            int64_t out_stride_t, int zero_masked, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
     if (!actor || !dlogits || !entropy || !lse || !dloss_dlogp)
         return fail(ctx, ORL_E_INVALID_ARG, "dlogits, entropy, lse and dloss_dlogp are required");
@@ -661,7 +674,7 @@ extern "C" orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, 
                     (long long)out_stride_t);
     const GradOut g{dlogits, out_stride_b, out_stride_t, zero_masked ? 1 : 0};
     return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
-                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, &g, stream);
+                         logp_new, entropy, lse, dloss_dlogp, dloss_dv, flags, &g, stream);
 }
 
 // ------------------------------------------------------------------ NEXT-1
@@ -783,7 +796,12 @@ extern "C" orl_status orl_stats_decode(const double *h, double ratio_guard, orl_
         return fail(nullptr, ORL_E_NCCL, "peer-memory collective: %lld wait(s) timed out (a rank did not arrive)",
                     (long long)h[kStatsOut + 2]);
     if (h[14] > 0) return fail(nullptr, ORL_E_TOKEN_RANGE, "%lld token(s) outside [0, V)", (long long)h[14]);
-    if (mask_err > 0) return fail(nullptr, ORL_E_MASK, "%lld invalid length(s)", (long long)mask_err);
+    if (mask_err > 0)
+        return fail(nullptr, ORL_E_MASK, "%lld invalid length(s) / non-prefix attention-mask row(s)",
+                    (long long)mask_err);
+    if (h[kStatsOut + 3] > 0)
+        return fail(nullptr, ORL_E_SHAPE, "%lld valid token(s) map to LM-head rows beyond the hidden matrix",
+                    (long long)h[kStatsOut + 3]);
     if (h[13] > 0) return fail(nullptr, ORL_E_NONFINITE, "%lld non-finite value(s)", (long long)h[13]);
     if (h[12] > 0)
         return fail(nullptr, ORL_E_NUMERIC_GUARD, "%lld token(s) with |logp_new - logp_old| > %g", (long long)h[12],

@@ -19,8 +19,11 @@ constexpr int kNumPartials = 15;
 // Whitening/count vector on the device: N_global, mu, sigma, apply, N_seq, 0, 0, 0
 constexpr int kWhitenSlots = 8;
 // Device error counters (uint64): 0 token out of range, 1 non-finite S1 rows,
-// 2 invalid lengths (L_b < 0 or > T).
-constexpr int kNumErr = 4;
+// 2 invalid lengths (L_b < 0 or > T; counted once per iteration, by K3 over the
+// whole rank batch -- K1/K5 clamp silently), 3 non-prefix attention-mask rows
+// (orl_lengths_from_mask), 4 LM-head rows a valid (b,t) maps to but the hidden
+// matrix does not hold (K6 merge).
+constexpr int kNumErr = 5;
 
 struct K1Params {
     const char *base;  // logits of the micro-batch's first sequence
@@ -46,6 +49,8 @@ struct K1Params {
     // S7-S9 loss epilogue (actor pass)
     const float *logp_old, *logp_ref, *adv, *ret, *v_new, *v_old;
     float *dlogp, *dv;
+    uint8_t *flags;     // optional per-token decisions: bit 0 clipped (Z16), 1 value-clipped,
+                        // 2 ratio guard (Z22), 3 non-finite loss term; masked positions 0
     double eps_low, eps_high, eps_v, c1, beta_loss, ratio_guard;
     int kl_loss_est, kl_in_loss, loss_agg;
     const double *whiten;  // device [kWhitenSlots]: N_global, mu, sigma, apply, N_seq
@@ -55,6 +60,9 @@ struct K1Params {
     double c2_ent;         // entropy coefficient of the total loss
     int zero_masked_grad;
     const int32_t *cum_global;  // prefix of the micro-batch lengths (large B), else NULL
+    int pdl_chain;              // 1: the caller vouches that the preceding kernel on the stream wrote
+                                // none of this launch's inputs after an early PDL trigger (orl_set_pdl_chain):
+                                // only the epilogue warps wait for it; 0: every warp waits first
     // NEXT-4 merge (k6_merge_kernel): per-split partials of the LM-head GEMM
     const float4 *lm_parts;     // [lm_nsplit][lm_stride] (m, s, u, z_y) per hidden row
     int64_t lm_stride;          // rows per split slab (>= lm_R)
@@ -170,8 +178,9 @@ cudaError_t launch_whiten_merge(const double *gather, int world, int want_whiten
                                 double *flags, cudaStream_t s);
 
 // Fold the error counters into the loss accumulator copy for the collective:
-// out[kStatsSlots] = acc[0..14], err -> slots 16..18 (ORL_PARTIALS_N in orl.h).
+// out[kStatsSlots] = acc[0..14], err[0..kNumErr) -> slots 16.. (ORL_PARTIALS_N in orl.h).
 constexpr int kStatsSlots = 24;
+static_assert(16 + kNumErr <= kStatsSlots, "error counters fit the stats partial");
 constexpr int kStatsOut = 16;  // final stats vector (ORL_STATS_N)
 cudaError_t launch_stats_pack(const double *acc, const unsigned long long *err, double *out,
                               cudaStream_t s);

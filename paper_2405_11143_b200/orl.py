@@ -89,16 +89,19 @@ _lib.orl_logprobs.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), 
 _lib.orl_advantages.argtypes = [_P, _I64, _I64, _P, _I32, _F64, _F64, _I32, _P, _P, _P, _P, _P, _P, _P]
 _lib.orl_whiten_stats.argtypes = [_P, _I32, _P]
 _lib.orl_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
-                              ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+                              ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.orl_ppo_loss_and_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
                                        ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                                       _I64, _I64, _I32, _P]
+                                       _P, _I64, _I64, _I32, _P]
 _lib.orl_logits_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32, ctypes.POINTER(PpoCfg),
                                  _P, _P, _P, _P, _I64, _I64, _I32, _P]
 _lib.orl_lmhead_logprobs.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(LmHead), _F32, _P, _P, _P, _P,
                                      _P, _I32, _F64, _P, _P, _P, _P]
 _lib.orl_lmhead_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(LmHead), _F32,
-                                     ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+                                     ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+_lib.orl_set_pdl_chain.argtypes = [_P, _I32]
+_lib.orl_get_pdl_chain.argtypes = [_P]
+_lib.orl_get_pdl_chain.restype = ctypes.c_int
 _lib.orl_finalize.argtypes = [_P, ctypes.POINTER(PpoCfg), ctypes.POINTER(Stats), _P, _P]
 _lib.orl_export_partials.argtypes = [_P, _I32, _P, _P]
 _lib.orl_import_partials.argtypes = [_P, _I32, _P, _I32, _P]
@@ -113,7 +116,7 @@ _lib.orl_set_collective.argtypes = [_P, _I32]
 _lib.orl_get_collective.argtypes = [_P]
 _lib.orl_get_collective.restype = ctypes.c_int
 _lib.orl_kl_controller_step.argtypes = [ctypes.POINTER(_F64), _F64, _F64, _F64, _F64, ctypes.POINTER(ctypes.c_int)]
-for _f in ("orl_kl_controller_step", "orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
+for _f in ("orl_set_pdl_chain", "orl_kl_controller_step", "orl_get_unique_id", "orl_create", "orl_destroy", "orl_begin_iteration", "orl_logprobs",
            "orl_advantages", "orl_whiten_stats", "orl_ppo_loss", "orl_finalize",
            "orl_export_partials", "orl_import_partials", "orl_logits_grad", "orl_ppo_loss_and_grad"):
     getattr(_lib, _f).restype = ctypes.c_int
@@ -238,6 +241,23 @@ class Context:
     def set_collective(self, mode: str):
         self.check(_lib.orl_set_collective(self.h, {"nccl": 0, "peer": 1}[mode]))
 
+    @property
+    def pdl_chain(self) -> bool:
+        return int(_lib.orl_get_pdl_chain(self.h)) == 1
+
+    @pdl_chain.setter
+    def pdl_chain(self, enable: bool):
+        """orl_set_pdl_chain: see orl.h for the precondition of enable=True."""
+        self.check(_lib.orl_set_pdl_chain(self.h, int(bool(enable))))
+
+
+def orl_set_pdl_chain(ctx: "Context", enable: bool) -> None:
+    ctx.pdl_chain = enable
+
+
+def orl_get_pdl_chain(ctx: "Context") -> bool:
+    return ctx.pdl_chain
+
 
 def orl_peer_handle(ctx: "Context") -> bytes:
     buf = ctypes.create_string_buffer(PEER_HANDLE_BYTES)
@@ -263,6 +283,52 @@ def exchange_peer_handles(mine: bytes, world: int, group=None) -> list:
     return out
 
 
+# ----------------------------------------------------------------------------- argument checks
+# Every pointer handed to liborl is checked here first (dtype, device, contiguity,
+# size), so a wrong tensor raises TypeError / ValueError instead of an out-of-bounds
+# device access or silently reinterpreted bits (e.g. int64 token ids read as int32).
+def _on_ctx(ctx, name, t):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if not t.is_cuda or (t.device.index if t.device.index is not None else torch.cuda.current_device()) != ctx.device:
+        raise ValueError(f"{name} must be a CUDA tensor on cuda:{ctx.device} (got {t.device})")
+
+
+def _arr(ctx, name, t, dtype, numel, optional=True):
+    """A contiguous device array of `dtype` with at least `numel` elements."""
+    if t is None:
+        if optional:
+            return None
+        raise ValueError(f"{name} is required")
+    _on_ctx(ctx, name, t)
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype} (got {t.dtype})")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() < numel:
+        raise ValueError(f"{name} has {t.numel()} elements, needs >= {numel}")
+    return t
+
+
+def _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens=None):
+    """tokens int32 [B_total, T], lengths int32 [B_total], the call's sequences inside."""
+    _arr(ctx, "tokens", tokens, torch.int32, 0, optional=False)
+    if tokens.dim() != 2:
+        raise ValueError("tokens must be [B_total, T]")
+    Bt, T = tokens.shape
+    _arr(ctx, "lengths", lengths, torch.int32, Bt, optional=False)
+    if seq_offset < 0 or B < 1 or seq_offset + B > Bt:
+        raise ValueError(f"sequences [{seq_offset}, {seq_offset + B}) outside the rank batch of {Bt}")
+    _arr(ctx, "cu_seqlens", cu_seqlens, torch.int32, Bt + 1)
+    return Bt, T
+
+
+def _tokarr(ctx, Bt, T, **arrays):
+    """Per-token fp32 [B_total, T] arrays (None = not given)."""
+    for name, t in arrays.items():
+        _arr(ctx, name, t, torch.float32, Bt * T)
+
+
 # ----------------------------------------------------------------------------- C-named calls
 def _rows(tokens, lengths, B, T, seq_offset, cu_seqlens=None):
     return Rows(int(B), int(T), int(seq_offset), tokens.data_ptr(), lengths.data_ptr(),
@@ -272,6 +338,10 @@ def _rows(tokens, lengths, B, T, seq_offset, cu_seqlens=None):
 def _packed(x, B):
     """A packed [total, V] logits tensor seen as the [B, 1, V]-shaped descriptor the C
     ABI wants (stride_b unused with cu_seqlens; stride_t = row pitch)."""
+    if x.dtype not in DTYPE:
+        raise TypeError(f"logits dtype {x.dtype} (bf16 or fp32 expected)")
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("packed logits must be a [total, V] view with unit stride along V")
     return Logits(x.data_ptr(), DTYPE[x.dtype], 0, x.shape[-1], 0, x.stride(-2))
 
 
@@ -293,6 +363,8 @@ def orl_lengths_from_mask(ctx: Context, mask, lengths, stream=None):
     are counted as ORL_E_MASK at orl_finalize)."""
     if mask.dtype not in (torch.uint8, torch.bool) or mask.dim() != 2 or not mask.is_contiguous():
         raise TypeError("mask must be a contiguous [B, T] uint8/bool tensor")
+    _on_ctx(ctx, "mask", mask)
+    _arr(ctx, "lengths", lengths, torch.int32, mask.shape[0], optional=False)
     if lengths.dtype != torch.int32 or lengths.numel() < mask.shape[0]:
         raise TypeError("lengths must be int32 [B]")
     B, T = mask.shape
@@ -304,6 +376,8 @@ def orl_keep_compact(ctx: Context, group_keep, kept_groups, n_kept, stream=None)
     if group_keep.dtype != torch.uint8 or kept_groups.dtype != torch.int32 or n_kept.dtype != torch.int32:
         raise TypeError("group_keep uint8, kept_groups / n_kept int32")
     n = group_keep.numel()
+    for name, t in (("group_keep", group_keep), ("kept_groups", kept_groups), ("n_kept", n_kept)):
+        _on_ctx(ctx, name, t)
     if kept_groups.numel() < n:
         raise ValueError("kept_groups must hold n_groups entries")
     return ctx.check(_lib.orl_keep_compact(ctx.h, n, _ptr(group_keep), _ptr(kept_groups), _ptr(n_kept),
@@ -314,6 +388,23 @@ def orl_begin_iteration(ctx: Context, stream=None):
     return ctx.check(_lib.orl_begin_iteration(ctx.h, _stream(stream)))
 
 
+def _lg(ctx, logits, B, cu_seqlens):
+    _on_ctx(ctx, "logits", logits)
+    return _packed(logits, B) if cu_seqlens is not None else _logits(logits)
+
+
+def _nseq(logits, cu_seqlens, n_seq):
+    if cu_seqlens is None:
+        return logits.shape[0]
+    if n_seq is None:
+        raise ValueError("packed logits (cu_seqlens) need n_seq, the sequences in the call")
+    return int(n_seq)
+
+
+def _flags(ctx, flags, Bt, T):
+    return _arr(ctx, "flags", flags, torch.uint8, Bt * T)
+
+
 def orl_logprobs(ctx: Context, tokens, lengths, logits, logp, *, seq_offset=0, inv_temp=1.0,
                  entropy=None, lse=None, gathered=None, partner_logp=None, kl_est="k1",
                  beta_reward=0.0, seq_reward=None, kl=None, shaped_reward=None, stream=None,
@@ -322,10 +413,14 @@ def orl_logprobs(ctx: Context, tokens, lengths, logits, logp, *, seq_offset=0, i
     [seq_offset, seq_offset+B) of the rank batch; per-token arrays are [B_total, T].
     Packed varlen (NEXT-2): pass `cu_seqlens` and a [total, V] `logits` whose row 0 is
     token cu_seqlens[seq_offset], plus `n_seq` (the B of the call)."""
-    T = tokens.shape[1]
-    B = n_seq if cu_seqlens is not None else logits.shape[0]
+    B = _nseq(logits, cu_seqlens, n_seq)
+    Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
+    _arr(ctx, "logp", logp, torch.float32, Bt * T, optional=False)
+    _tokarr(ctx, Bt, T, entropy=entropy, lse=lse, gathered=gathered, partner_logp=partner_logp, kl=kl,
+            shaped_reward=shaped_reward)
+    _arr(ctx, "seq_reward", seq_reward, torch.float32, Bt)
     rows = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens)
-    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
+    lg = _lg(ctx, logits, B, cu_seqlens)
     st = _lib.orl_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), _ptr(logp),
                            _ptr(entropy), _ptr(lse), _ptr(gathered), _ptr(partner_logp),
                            KL.get(kl_est, kl_est), float(beta_reward), _ptr(seq_reward), _ptr(kl),
@@ -344,6 +439,12 @@ def _lmhead(hidden, weight):
                   hidden.stride(0), weight.stride(0))
 
 
+def _head(ctx, hidden, weight):
+    _on_ctx(ctx, "hidden", hidden)
+    _on_ctx(ctx, "weight", weight)
+    return _lmhead(hidden, weight)
+
+
 def orl_lmhead_logprobs(ctx: Context, tokens, lengths, hidden, weight, logp, *, B=None, seq_offset=0,
                         inv_temp=1.0, entropy=None, lse=None, gathered=None, partner_logp=None, kl_est="k1",
                         beta_reward=0.0, seq_reward=None, kl=None, shaped_reward=None, stream=None,
@@ -351,10 +452,14 @@ def orl_lmhead_logprobs(ctx: Context, tokens, lengths, hidden, weight, logp, *, 
     """NEXT-4: orl_logprobs with logits = hidden @ weight.T computed on the tensor cores
     (never materialised).  hidden [R, d] holds the call's rows: packed by `cu_seqlens`
     or b*T + t; `B` = sequences in the call (default: all from seq_offset)."""
-    T = tokens.shape[1]
     if B is None:
         B = tokens.shape[0] - seq_offset
-    rows, hd = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), _lmhead(hidden, weight)
+    Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
+    _arr(ctx, "logp", logp, torch.float32, Bt * T, optional=False)
+    _tokarr(ctx, Bt, T, entropy=entropy, lse=lse, gathered=gathered, partner_logp=partner_logp, kl=kl,
+            shaped_reward=shaped_reward)
+    _arr(ctx, "seq_reward", seq_reward, torch.float32, Bt)
+    rows, hd = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), _head(ctx, hidden, weight)
     st = _lib.orl_lmhead_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(hd), float(inv_temp), _ptr(logp),
                                   _ptr(entropy), _ptr(lse), _ptr(gathered), _ptr(partner_logp),
                                   KL.get(kl_est, kl_est), float(beta_reward), _ptr(seq_reward), _ptr(kl),
@@ -362,25 +467,44 @@ def orl_lmhead_logprobs(ctx: Context, tokens, lengths, hidden, weight, logp, *, 
     return ctx.check(st)
 
 
+def _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
+                 dloss_dv, flags):
+    for name, t in (("logp_old", logp_old), ("adv", adv), ("logp_new", logp_new)):
+        _arr(ctx, name, t, torch.float32, Bt * T, optional=False)
+    _tokarr(ctx, Bt, T, logp_ref=logp_ref, ret=ret, v_new=v_new, v_old=v_old, entropy=entropy, lse=lse,
+            dloss_dlogp=dloss_dlogp, dloss_dv=dloss_dv)
+    _flags(ctx, flags, Bt, T)
+
+
 def orl_lmhead_ppo_loss(ctx: Context, tokens, lengths, hidden, weight, cfg, logp_old, adv, logp_new, *,
                         B=None, seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
-                        entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, stream=None, cu_seqlens=None):
+                        entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, flags=None, stream=None,
+                        cu_seqlens=None):
     """NEXT-4: orl_ppo_loss with the actor logits computed from its LM head."""
-    T = tokens.shape[1]
     if B is None:
         B = tokens.shape[0] - seq_offset
-    rows, hd, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), _lmhead(hidden, weight), cfg.c()
+    Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
+    _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
+                 dloss_dv, flags)
+    rows, hd, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), _head(ctx, hidden, weight), cfg.c()
     st = _lib.orl_lmhead_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(hd), float(inv_temp), ctypes.byref(c),
                                   _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
                                   _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
-                                  _ptr(dloss_dv), _stream(stream))
+                                  _ptr(dloss_dv), _ptr(flags), _stream(stream))
     return ctx.check(st)
 
 
 def orl_advantages(ctx: Context, lengths, adv, *, kind="gae", gamma=1.0, lam=0.95, group_size=1,
                    shaped_reward=None, values=None, seq_reward=None, ret=None, group_keep=None,
                    stream=None):
+    _arr(ctx, "adv", adv, torch.float32, 0, optional=False)
+    if adv.dim() != 2:
+        raise ValueError("adv must be [B, T]")
     B, T = adv.shape
+    _arr(ctx, "lengths", lengths, torch.int32, B, optional=False)
+    _tokarr(ctx, B, T, shaped_reward=shaped_reward, values=values, ret=ret)
+    _arr(ctx, "seq_reward", seq_reward, torch.float32, B)
+    _arr(ctx, "group_keep", group_keep, torch.uint8, B // max(1, int(group_size)))
     st = _lib.orl_advantages(ctx.h, B, T, _ptr(lengths), ADV.get(kind, kind), float(gamma), float(lam),
                              int(group_size), _ptr(shaped_reward), _ptr(values), _ptr(seq_reward),
                              _ptr(adv), _ptr(ret), _ptr(group_keep), _stream(stream))
@@ -393,36 +517,51 @@ def orl_whiten_stats(ctx: Context, whiten: bool, stream=None):
 
 def orl_ppo_loss(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
                  seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
-                 entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, stream=None,
+                 entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, flags=None, stream=None,
                  cu_seqlens=None, n_seq=None):
-    T = tokens.shape[1]
-    B = n_seq if cu_seqlens is not None else logits.shape[0]
+    """S1 + S7..S9 on the actor logits; `flags` (optional uint8 [B_total, T]) receives the
+    per-token decisions (bit 0 clipped, 1 value-clipped, 2 ratio guard, 3 non-finite)."""
+    B = _nseq(logits, cu_seqlens, n_seq)
+    Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
+    _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
+                 dloss_dv, flags)
     rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
-    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
+    lg = _lg(ctx, logits, B, cu_seqlens)
     st = _lib.orl_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
                            _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
                            _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
-                           _ptr(dloss_dv), _stream(stream))
+                           _ptr(dloss_dv), _ptr(flags), _stream(stream))
     return ctx.check(st)
+
+
+def _dlogits(ctx, dlogits, logits):
+    _on_ctx(ctx, "dlogits", dlogits)
+    if dlogits.dtype != logits.dtype or dlogits.shape[-1] != logits.shape[-1] or dlogits.stride(-1) != 1:
+        raise ValueError("dlogits must be a view with the logits dtype, V and unit V stride")
+    if dlogits.dim() != logits.dim() or tuple(dlogits.shape[:-1]) != tuple(logits.shape[:-1]):
+        raise ValueError(f"dlogits shape {tuple(dlogits.shape)} does not match the logits {tuple(logits.shape)}")
 
 
 def orl_ppo_loss_and_grad(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
                           entropy, lse, dloss_dlogp, dlogits, seq_offset=0, inv_temp=1.0, logp_ref=None,
-                          ret=None, v_new=None, v_old=None, dloss_dv=None, zero_masked=True, stream=None,
-                          cu_seqlens=None, n_seq=None):
+                          ret=None, v_new=None, v_old=None, dloss_dv=None, flags=None, zero_masked=True,
+                          stream=None, cu_seqlens=None, n_seq=None):
     """S1 + S7..S9 + NEXT-1 in one pass over the actor logits (the row is re-read from L2)."""
-    T = tokens.shape[1]
-    B = n_seq if cu_seqlens is not None else logits.shape[0]
-    if dlogits.dtype != logits.dtype or dlogits.shape[-1] != logits.shape[-1] or dlogits.stride(-1) != 1:
-        raise ValueError("dlogits must be a view with the logits dtype, V and unit V stride")
+    B = _nseq(logits, cu_seqlens, n_seq)
+    Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
+    for name, t in (("entropy", entropy), ("lse", lse), ("dloss_dlogp", dloss_dlogp)):
+        _arr(ctx, name, t, torch.float32, Bt * T, optional=False)
+    _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
+                 dloss_dv, flags)
+    _dlogits(ctx, dlogits, logits)
     rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
-    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
+    lg = _lg(ctx, logits, B, cu_seqlens)
     sb = 0 if cu_seqlens is not None else dlogits.stride(0)
     st = _lib.orl_ppo_loss_and_grad(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
                                     _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
                                     _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
-                                    _ptr(dloss_dv), _ptr(dlogits), sb, dlogits.stride(-2), int(bool(zero_masked)),
-                                    _stream(stream))
+                                    _ptr(dloss_dv), _ptr(flags), _ptr(dlogits), sb, dlogits.stride(-2),
+                                    int(bool(zero_masked)), _stream(stream))
     return ctx.check(st)
 
 
@@ -430,12 +569,13 @@ def orl_logits_grad(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, lse, 
                     seq_offset=0, inv_temp=1.0, zero_masked=True, stream=None, cu_seqlens=None, n_seq=None):
     """NEXT-1: dL/dlogits of the micro-batch logits[0:B] into dlogits[0:B] (same dtype/shape view;
     packed [total, V] tensors with cu_seqlens)."""
-    T = tokens.shape[1]
-    B = n_seq if cu_seqlens is not None else logits.shape[0]
-    if dlogits.dtype != logits.dtype or dlogits.shape[-1] != logits.shape[-1] or dlogits.stride(-1) != 1:
-        raise ValueError("dlogits must be a view with the logits dtype, V and unit V stride")
+    B = _nseq(logits, cu_seqlens, n_seq)
+    Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
+    for name, t in (("lse", lse), ("entropy", entropy), ("dloss_dlogp", dloss_dlogp)):
+        _arr(ctx, name, t, torch.float32, Bt * T, optional=False)
+    _dlogits(ctx, dlogits, logits)
     rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
-    lg = _packed(logits, B) if cu_seqlens is not None else _logits(logits)
+    lg = _lg(ctx, logits, B, cu_seqlens)
     sb = 0 if cu_seqlens is not None else dlogits.stride(0)
     st = _lib.orl_logits_grad(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
                               _ptr(lse), _ptr(entropy), _ptr(dloss_dlogp), _ptr(dlogits), sb,
@@ -443,7 +583,9 @@ def orl_logits_grad(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, lse, 
     return ctx.check(st)
 
 
-DATA_ERRORS = (ST["ORL_E_TOKEN_RANGE"], ST["ORL_E_MASK"], ST["ORL_E_NONFINITE"],
+# statuses orl_finalize / orl_stats_decode return for data found on the device (outputs are
+# still written); ORL_E_SHAPE there = valid tokens mapped to LM-head rows beyond the hidden matrix
+DATA_ERRORS = (ST["ORL_E_TOKEN_RANGE"], ST["ORL_E_MASK"], ST["ORL_E_SHAPE"], ST["ORL_E_NONFINITE"],
                ST["ORL_E_NUMERIC_GUARD"], ST["ORL_E_EMPTY_BATCH"])
 
 

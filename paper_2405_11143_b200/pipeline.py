@@ -56,6 +56,8 @@ class Buffers:
         self.lse = f()
         self.dlogp = f() if grads else None
         self.dv = f() if grads else None
+        # per-token decisions of the actor pass: bit 0 clipped, 1 value-clipped, 2 guard, 3 non-finite
+        self.flags = torch.zeros(B, T, dtype=torch.uint8, device=device)
         self.keep = torch.zeros(max(1, B // max(1, group_size)), dtype=torch.uint8, device=device)
         self.stats_dev = torch.zeros(_orl.STATS_N, dtype=torch.float64, device=device)
         self.final_dev = torch.zeros(_orl.FINAL_N, dtype=torch.float64, device=device)  # orl_finalize_async
@@ -80,12 +82,27 @@ def microbatches(B: int, mb: int):
 def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers, logits: LogitsSource,
                   mb: int, stream: Optional[torch.cuda.Stream] = None, finalize: bool = True,
                   on_k1: Optional[Callable[[str], object]] = None,
-                  grad_sink: Optional[Callable[[int, int], torch.Tensor]] = None, fused_grad: bool = True):
+                  grad_sink: Optional[Callable[[int, int], torch.Tensor]] = None, fused_grad: bool = True,
+                  pdl_chain: Optional[bool] = None):
     """One iteration on this rank.  `batch` holds device tensors tokens [B,T] int32,
     lengths [B] int32, seq_reward [B] f32 and (critic) values_old / values_new [B,T].
     `on_k1(tag)` (optional) is called around every K1 launch for timing hooks.
     `grad_sink(s, e)` (optional, NEXT-1) returns the [e-s, T, V] dlogits view the
-    backward pass (orl_logits_grad) writes for micro-batch [s, e)."""
+    backward pass (orl_logits_grad) writes for micro-batch [s, e).
+    `pdl_chain` (optional) sets orl_set_pdl_chain for this iteration only: True is
+    valid when the logits source launches no kernel that writes the logits with an
+    early PDL trigger (resident tensors, slices, copies, plain torch kernels)."""
+    if pdl_chain is None:
+        return _run_iteration(ctx, batch, cfg, bufs, logits, mb, stream, finalize, on_k1, grad_sink, fused_grad)
+    prev = ctx.pdl_chain
+    ctx.pdl_chain = pdl_chain
+    try:
+        return _run_iteration(ctx, batch, cfg, bufs, logits, mb, stream, finalize, on_k1, grad_sink, fused_grad)
+    finally:
+        ctx.pdl_chain = prev
+
+
+def _run_iteration(ctx, batch, cfg, bufs, logits, mb, stream, finalize, on_k1, grad_sink, fused_grad):
     tok, L = batch["tokens"], batch["lengths"]
     B, T = tok.shape
     mbs = microbatches(B, mb)
@@ -124,8 +141,6 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
                             stream=stream)
         _orl.orl_whiten_stats(ctx, cfg.whiten and cfg.adv_kind != "grpo", stream)     # S6 + C1
     critic = cfg.critic and batch.get("values_new") is not None
-    if grad_sink is not None and isinstance(logits("new", 0, min(B, mb)), LmHeadRows):
-        raise NotImplementedError("dL/dlogits needs materialised logits; the LM-head path (NEXT-4) is forward-only")
     if grad_sink is not None and fused_grad:           # S1 + S7..S9 + NEXT-1 in one pass
         with nvtx("orl S1 S7-S9 actor + dL/dlogits"):
             _actor_fused(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, stream)
@@ -137,16 +152,22 @@ def run_iteration(ctx: _orl.Context, batch: dict, cfg: PathConfig, bufs: Buffers
         return _finish(ctx, cfg, bufs, stream, finalize)                   # S10 + C2
 
 
+def _no_lmhead(src):
+    if isinstance(src, LmHeadRows):
+        raise NotImplementedError("dL/dlogits needs materialised logits; the LM-head path (NEXT-4) is forward-only")
+    return src
+
+
 def _actor_fused(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, stream):
     for s, e in mbs:
         h = hook("new+grad")
-        _orl.orl_ppo_loss_and_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.logp_old, bufs.adv,
+        _orl.orl_ppo_loss_and_grad(ctx, tok, L, _no_lmhead(logits("new", s, e)), cfg.ppo, bufs.logp_old, bufs.adv,
                                    bufs.logp_new, seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
                                    ret=bufs.ret if critic else None,
                                    v_new=batch["values_new"] if critic else None,
                                    v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
                                    lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
-                                   dlogits=grad_sink(s, e), stream=stream)
+                                   flags=bufs.flags, dlogits=grad_sink(s, e), stream=stream)
         if h: h()
 
 
@@ -157,8 +178,11 @@ def _actor(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, 
         kw = dict(seq_offset=s, inv_temp=cfg.inv_temp, logp_ref=bufs.logp_ref,
                   ret=bufs.ret if critic else None, v_new=batch["values_new"] if critic else None,
                   v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
-                  lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None, stream=stream)
+                  lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None, flags=bufs.flags,
+                  stream=stream)
         if isinstance(src, LmHeadRows):
+            if grad_sink is not None:
+                _no_lmhead(src)
             _orl.orl_lmhead_ppo_loss(ctx, tok, L, src.hidden, src.weight, cfg.ppo, bufs.logp_old, bufs.adv,
                                      bufs.logp_new, B=e - s, cu_seqlens=src.cu_seqlens, **kw)
         else:
@@ -167,7 +191,7 @@ def _actor(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, 
     if grad_sink is not None:                          # NEXT-1: dL/dlogits
         for s, e in mbs:
             h = hook("grad")
-            _orl.orl_logits_grad(ctx, tok, L, logits("new", s, e), cfg.ppo, bufs.lse, bufs.entropy, bufs.dlogp,
+            _orl.orl_logits_grad(ctx, tok, L, _no_lmhead(logits("new", s, e)), cfg.ppo, bufs.lse, bufs.entropy, bufs.dlogp,
                                  grad_sink(s, e), seq_offset=s, inv_temp=cfg.inv_temp, stream=stream)
             if h: h()
 
@@ -191,20 +215,20 @@ class GraphStep:
     The statistics land in bufs.final_dev; result() copies them to the host and decodes."""
 
     def __init__(self, ctx, batch: dict, cfg: PathConfig, bufs: Buffers, logits: LogitsSource, mb: int,
-                 warmup: int = 1):
+                 warmup: int = 1, pdl_chain: Optional[bool] = None):
         self.ctx, self.cfg, self.bufs = ctx, cfg, bufs
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):                   # eager warm-up sizes every workspace
             for _ in range(max(1, warmup)):
-                run_iteration(ctx, batch, cfg, bufs, logits, mb, stream=side, finalize="async")
+                run_iteration(ctx, batch, cfg, bufs, logits, mb, stream=side, finalize="async", pdl_chain=pdl_chain)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         l0 = ctx.launch_count
         with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
             run_iteration(ctx, batch, cfg, bufs, logits, mb, stream=torch.cuda.current_stream(),
-                          finalize="async")
+                          finalize="async", pdl_chain=pdl_chain)
         self.kernels = ctx.launch_count - l0           # liborl kernels inside the graph
 
     def replay(self):

@@ -45,7 +45,15 @@ CONFIGS = {
     "rpp8": dict(B=1024, T=2048, V=128256, dtype="bf16", adv_kind="rpp", gamma=1.0, lam=1.0,
                  kl_est_reward="k1", beta_reward=0.01, eps_low=0.2, eps_high=0.2, eps_v=0.0,
                  c1=0.0, c2=0.0, whiten=True, rewards="bernoulli", group_size=1, mb=16),
+    # not a BASELINE.json config: the north star's target shape (V = 128256, T = 8192
+    # rollouts), long-CoT settings of "longcot" on the Llama vocabulary; a bench leg only
+    "target": dict(B=16, T=8192, V=128256, dtype="bf16", adv_kind="gae", gamma=1.0, lam=1.0,
+                   kl_est_reward="k3", beta_reward=0.01, eps_low=0.2, eps_high=0.28, eps_v=0.2,
+                   c1=0.5, c2=0.0, whiten=True, rewards="bernoulli", group_size=1, mb=4),
 }
+# SURVEY 8(d) secondary (ragged) lengths per config, for lengths_for()
+SECONDARY_LENGTHS = {"tiny": "tiny", "llama8b": "mixed", "longcot": "cot", "grpo": "mixed", "rpp8": "mixed",
+                     "target": "cot"}
 
 
 def role_seed(seed: int, mb: int, role: int) -> int:
@@ -53,10 +61,17 @@ def role_seed(seed: int, mb: int, role: int) -> int:
 
 
 def lengths_for(B: int, T: int, seed: int, mode: str = "full") -> torch.Tensor:
-    """int32 [B] response lengths.  full: all T.  mixed: U{T//16..T}.  tiny: the
-    hand-picked {T, 11/16 T, 5/16 T, 1} pattern plus a 0-length response."""
+    """int32 [B] response lengths.  full: all T.  mixed: U{T//16..T} (SURVEY 8(d)
+    secondary lengths: llama8b U{64..1024}, grpo U{256..4096}, rpp8 U{128..2048}).
+    cot: long-CoT mix, 40% at T and the rest U{T//8..T} (longcot: U{1024..8192}).
+    tiny: the hand-picked {T, 11/16 T, 5/16 T, 1} pattern plus a 0-length response."""
     if mode == "full":
         return torch.full((B,), T, dtype=torch.int32)
+    if mode == "cot":
+        g = torch.Generator().manual_seed(role_seed(seed, 10_000, 5))
+        L = torch.randint(max(1, T // 8), T + 1, (B,), generator=g, dtype=torch.int32)
+        full = torch.rand(B, generator=g) < 0.4
+        return torch.where(full, torch.full_like(L, T), L)
     if mode == "tiny":
         pat = [T, max(1, (11 * T) // 16), max(1, (5 * T) // 16), 1, 0, T, max(1, T // 2), 3 % (T + 1)]
         return torch.tensor([pat[i % len(pat)] for i in range(B)], dtype=torch.int32)
@@ -166,6 +181,31 @@ def split_bounds(B: int, n: int, group_size: int = 1):
         raise ValueError("batch is not a whole number of groups")
     ng = B // G
     cuts = [(ng * r // n) * G for r in range(n + 1)]
+    return [(cuts[r], cuts[r + 1]) for r in range(n)]
+
+
+def split_bounds_tokens(lengths, n: int, group_size: int = 1):
+    """Contiguous, group-aligned rank shards balanced by valid tokens (SPEC S:468:
+    shards "weighted by token counts"): rank r takes the groups whose
+    token prefix midpoint falls in [r/n, (r+1)/n) of the total.  Sequence order is
+    kept, so concatenating the shards gives the batch back."""
+    L = np.clip(np.asarray(lengths, dtype=np.int64), 0, None)
+    G = max(1, group_size)
+    B = L.size
+    if B % G:
+        raise ValueError("batch is not a whole number of groups")
+    if n < 1:
+        raise ValueError("n >= 1")
+    gt = L.reshape(-1, G).sum(axis=1).astype(np.float64)
+    total = gt.sum()
+    if total <= 0:
+        return split_bounds(B, n, group_size)
+    mid = np.cumsum(gt) - 0.5 * gt                  # token midpoint of each group
+    owner = np.minimum((mid * n / total).astype(np.int64), n - 1)
+    cuts = [0] + [int(np.searchsorted(owner, r, side="left")) * G for r in range(1, n)] + [B]
+    if B // G >= n:                                  # every rank gets at least one group
+        for r in range(1, n):
+            cuts[r] = min(max(cuts[r], cuts[r - 1] + G), B - (n - r) * G)
     return [(cuts[r], cuts[r + 1]) for r in range(n)]
 
 

@@ -80,7 +80,9 @@ def test_host_validation_without_gpu(lib):
     so, _ = lib
     so.orl_last_error.restype = ctypes.c_char_p
     so.orl_last_error.argtypes = [ctypes.c_void_p]
-    assert so.orl_version() == 1
+    assert so.orl_version() == 2
+    assert so.orl_set_pdl_chain(None, 1) == 1
+    assert so.orl_get_pdl_chain(None) == -1
     assert so.orl_begin_iteration(None, None) == 1          # ORL_E_INVALID_ARG, before any CUDA call
     assert b"ctx" in so.orl_last_error(None)
     assert so.orl_whiten_stats(None, 1, None) == 1
@@ -104,6 +106,29 @@ def test_host_validation_without_gpu(lib):
     assert so.orl_stats_decode(None, ctypes.c_double(30.0), None) == 1
     assert so.orl_destroy(None) == 0
     assert so.orl_launch_count(None) == 0
+
+
+def test_stats_decode_status_priority(lib):
+    """orl_stats_decode maps the device flags to the documented status priority
+    (orl.h: NCCL > TOKEN_RANGE > MASK > SHAPE > NONFINITE > NUMERIC_GUARD > EMPTY_BATCH)."""
+    so, _ = lib
+    so.orl_stats_decode.argtypes = [ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p]
+
+    def decode(**kw):
+        v = (ctypes.c_double * 20)()
+        v[0] = 10.0
+        for k, x in kw.items():
+            v[int(k[1:])] = x
+        return so.orl_stats_decode(v, ctypes.c_double(30.0), None)
+
+    assert decode() == 0
+    assert decode(i0=0.0) == 9                          # EMPTY_BATCH
+    assert decode(i12=1) == 8                           # NUMERIC_GUARD
+    assert decode(i12=1, i13=2) == 7                    # NONFINITE
+    assert decode(i13=2, i19=1) == 2                    # SHAPE (LM-head rows beyond R)
+    assert decode(i19=1, i17=3) == 6                    # MASK (invalid lengths / non-prefix masks)
+    assert decode(i17=3, i14=1) == 5                    # TOKEN_RANGE
+    assert decode(i14=1, i18=1) == 12                   # a peer collective timed out
 
 
 def test_product_never_imports_oracle():

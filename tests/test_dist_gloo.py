@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, kind, q):
+def _worker(rank, world, port, kind, q, split="tokens"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -42,7 +42,10 @@ def _worker(rank, world, port, kind, q):
         cfg = dict(synth.CONFIGS["tiny"], adv_kind=kind, group_size=G)
         if kind == "grpo":
             cfg.update(kl_mode="loss", beta_loss=0.01, kl_est_loss="k2", whiten=False, c1=0.0, eps_v=0.0)
-        s, e = synth.split_bounds(8, world, G)[rank]
+        # bench.py's shards: contiguous, group-aligned, balanced by valid tokens
+        bounds = synth.split_bounds_tokens(full["lengths"], world, G) if split == "tokens" \
+            else synth.split_bounds(8, world, G)
+        s, e = bounds[rank]
         shard = {k: v[s:e] for k, v in full.items()}
         # unique-id broadcast as bench.py does it
         uid = [bytes(range(128)) if rank == 0 else None]
@@ -89,12 +92,13 @@ def _worker(rank, world, port, kind, q):
         q.put(("err", traceback.format_exc(), None))
 
 
-@pytest.mark.parametrize("kind", ["gae", "rpp", "grpo"])
-def test_two_rank_protocol_matches_single_process(kind):
+@pytest.mark.parametrize("kind,split", [("gae", "tokens"), ("rpp", "tokens"), ("grpo", "tokens"),
+                                        ("gae", "sequences")])
+def test_two_rank_protocol_matches_single_process(kind, split):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q, split)) for r in range(2)]
     for p in procs:
         p.start()
     status, st, ref = q.get(timeout=240)

@@ -243,13 +243,15 @@ def test_lmhead_token_range_and_mask_errors(ctx):
     assert np.all(np.isfinite(g["logp"][ok]))
     status, stats = orl.orl_finalize(ctx, orl.PPOConfig())
     assert stats["n_token_range"] == 2
-    # hidden too short for the lengths: mask error, NaN outputs, no out-of-bounds read
+    # hidden too short for the lengths: NaN outputs, no out-of-bounds read, its own status
+    # (ORL_E_SHAPE, counted apart from invalid lengths / masks)
     b2 = synth.make_lmhead_batch(16, B, T, d, V, lengths=[16, 9])
     b2["hidden_old"] = b2["hidden_old"][:20]
     g2 = _run_logprobs(ctx, b2)
     assert np.all(np.isnan(g2["logp"][1, 4:9])) and np.all(np.isfinite(g2["logp"][1, :4]))
     status, stats = orl.orl_finalize(ctx, orl.PPOConfig())
-    assert status == "ORL_E_MASK", status
+    assert status == "ORL_E_SHAPE", status
+    assert "5 valid token(s) map to LM-head rows" in orl.orl_last_error(ctx)
 
 
 def test_lmhead_host_argument_errors(ctx):

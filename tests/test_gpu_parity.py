@@ -7,6 +7,7 @@ logits is also compared end to end on the tiny fp32 config.
 """
 from __future__ import annotations
 
+import importlib
 import os
 
 import numpy as np
@@ -57,7 +58,51 @@ def _isolated_oracle(npb, bufs, ocfg):
     sh["logp_ref"] = _np(bufs.logp_ref).astype(np.float64)
     sh["logp_new"] = _np(bufs.logp_new).astype(np.float64)
     sh["entropy_new"] = _np(bufs.entropy).astype(np.float64)
-    return oracle.pipeline([sh], ocfg)
+    out, glob = oracle.pipeline([sh], ocfg)
+    glob["isolated_input"] = (sh, dict(importlib.import_module("oracle.pipeline").DEFAULTS, **ocfg))
+    return out, glob
+
+
+def _check_flags(bufs, sh, ocfg, mask, name):
+    """Per-token decisions bit-exact: the loss stage of the
+    oracle fed the GPU's own fp32 upstream (logp_new/old/ref, adv, ret, entropy; the
+    whitening moments taken by the oracle over the GPU's fp32 advantages) vs the actor
+    pass's flags output.  bit 0 clipped (Z16), 1 value-clipped (Z13), 2 ratio guard
+    (Z22), 3 non-finite.  Tie bands (excluded and counted): rho within 1e-9 of a clip
+    edge (fp64 exp may differ by an ulp), |A'| < 1e-12, |dold| within 1e-9 of the guard."""
+    L = sh["lengths"]
+    f64 = lambda t: _np(t).astype(np.float64)  # noqa: E731
+    adv = f64(bufs.adv)
+    kind = ocfg["adv_kind"]
+    whiten = bool(ocfg["whiten"]) and kind != "grpo"
+    Aw = adv
+    if whiten:
+        mu, sd, warn = oracle.whiten_moments(adv[mask])
+        if not warn:
+            Aw = oracle.whiten(adv, L, mu, sd)
+    critic = kind == "gae" and sh.get("values_new") is not None
+    res = oracle.ppo_loss(L, f64(bufs.logp_new), f64(bufs.logp_old), Aw, logp_ref=f64(bufs.logp_ref),
+                          ret=f64(bufs.ret) if critic else None, v_new=sh["values_new"] if critic else None,
+                          v_old=sh["values_old"] if critic else None, entropy=f64(bufs.entropy),
+                          eps_low=ocfg["eps_low"], eps_high=ocfg["eps_high"], eps_v=ocfg["eps_v"],
+                          c1=ocfg["c1"] if critic else 0.0, beta_loss=ocfg["beta_loss"], kl_est=ocfg["kl_est_loss"],
+                          kl_in_loss=ocfg["kl_mode"] == "loss", ratio_guard=ocfg["ratio_guard"])
+    g, o = _np(bufs.flags).astype(np.int64), res["flags"].astype(np.int64)
+    assert np.all(g[~mask] == 0), f"{name}: flags at masked positions"
+    dold = f64(bufs.logp_new) - f64(bufs.logp_old)
+    rho = np.exp(dold)
+    tie_rho = (np.abs(rho - (1 - ocfg["eps_low"])) < 1e-9) | (np.abs(rho - (1 + ocfg["eps_high"])) < 1e-9)
+    # A' == 0 exactly (constant GRPO groups) is decided identically on both sides; only a
+    # tiny nonzero A' could flip sign between one- and two-pass whitening moments
+    tie_p = tie_rho | ((np.abs(Aw) < 1e-12) & (Aw != 0))
+    tie_g = np.abs(np.abs(dold) - ocfg["ratio_guard"]) < 1e-9
+    for bit, tie in ((0, tie_p), (1, np.zeros_like(mask)), (2, tie_g), (3, np.zeros_like(mask))):
+        sel = mask & ~tie
+        gb, ob = (g >> bit) & 1, (o >> bit) & 1
+        assert np.array_equal(gb[sel], ob[sel]), f"{name}: flag bit {bit} differs on {np.count_nonzero(gb[sel] != ob[sel])} tokens"
+    assert np.count_nonzero(tie_p & mask) <= max(2, mask.sum() // 10000), f"{name}: too many policy ties"
+    assert np.count_nonzero(tie_g & mask) <= 1
+    return int(np.count_nonzero(o[mask] & 1)), int(np.count_nonzero(o[mask] & 2))
 
 
 def _check_downstream(bufs, o, glob, st, mask, cfg_name, ppo_tol=parity.REL, raw_shaped=None):
@@ -72,16 +117,12 @@ def _check_downstream(bufs, o, glob, st, mask, cfg_name, ppo_tol=parity.REL, raw
     parity.check_rel("dloss_dlogp", _np(bufs.dlogp), o["dlogp"], mask)
     if bufs.dv is not None:
         parity.check_rel("dloss_dv", _np(bufs.dv), o["dv"], mask)
-    # clip decisions bit-exact (outside a 1e-6 tie band around the clip edges)
+    # per-token decisions (clip, value clip, guard, non-finite) bit-exact, every config
+    if "isolated_input" in glob:
+        _check_flags(bufs, *glob["isolated_input"], mask, cfg_name)
     lp_n, lp_o = _np(bufs.logp_new).astype(np.float64), _np(bufs.logp_old).astype(np.float64)
     rho = np.exp(lp_n - lp_o)
-    gpu_clipped = (_np(bufs.dlogp) == 0.0) & mask
-    ora_clipped = o["clipped"].astype(bool) & mask
     tie = (np.abs(rho - 0.8) < 1e-6) | (np.abs(rho - 1.2) < 1e-6) | (np.abs(rho - 1.28) < 1e-6)
-    zero_adv = np.abs(o["adv_w"]) < 1e-30
-    sel = mask & ~tie & ~zero_adv
-    if not np.any(o["dlogp"][mask & ora_clipped] != 0):       # no KL term in the gradient
-        assert np.array_equal(gpu_clipped[sel], ora_clipped[sel]), f"{cfg_name}: clip decisions differ"
     gs, os_ = st, glob["stats"]
     assert gs["n_tokens"] == os_["n_tokens"]
     ntie = np.count_nonzero(tie & mask)
@@ -460,13 +501,13 @@ def test_host_argument_errors(ctx):
     with pytest.raises(TypeError):
         orl.orl_logprobs(ctx, tok, L, x.to(torch.float16), lp)
 
-    class Misaligned:                 # a per-token array 2 bytes off a 4-byte boundary
-        def data_ptr(self):
-            return lp.data_ptr() + 2
-
-    with pytest.raises(orl.OrlError) as e:
-        orl.orl_logprobs(ctx, tok, L, x, Misaligned())
-    assert e.value.name == "ORL_E_ALIGN"
+    # the C ABI itself: a per-token array 2 bytes off a 4-byte boundary (the binding only
+    # hands over tensor pointers, so call liborl directly)
+    import ctypes
+    rows, lg = orl._rows(tok, L, tok.shape[0], tok.shape[1], 0), orl._logits(x)
+    st = orl._lib.orl_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(lg), 1.0, ctypes.c_void_p(lp.data_ptr() + 2),
+                               None, None, None, None, 1, 0.0, None, None, None, None)
+    assert orl.STATUS[st] == "ORL_E_ALIGN"
 
 
 # --------------------------------------------------------------------------- determinism / DP
@@ -589,6 +630,165 @@ def test_next1_logits_grad_parity(ctx, dtype, V, inv_temp):
     H = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"], inv_temp)["entropy"]
     _check_grad(gg, o, m, 2e-5 if dtype == "f32" else 8e-3, f"{dtype}-{V}", _np(bufs.dlogp), H,
                 0.01 / float(m.sum()), inv_temp)
+
+
+def _grad_bound(x_rows, tok, lse, H, w, a, inv_temp, o, out_bf16):
+    """Derived per-element bound for dL/dx (NEXT-1) of one row, GPU vs the fp64 oracle.
+    The GPU evaluates g_v = inv_temp (p_v (a (ln p_v + H) - w) + [v = y] w) in fp32 from
+    its saved fp32 lse, H, w (stage isolation: the oracle uses the same w, its own fp64
+    lse and H), p_v = 2^(x_v c - lse log2 e).  Error sources:
+      * p_v: |d ln p| <= |dlse| + 2^-23 (|x c| + |lse log2 e|) ln 2 + 2^-22 (MUFU ex2),
+        |dlse| <= 1e-6 (S1's measured 5.4e-7 bound at V = 128256, SURVEY 8(c).4);
+      * the factor a (ln p + H) - w: |dH| <= 1e-6 plus fp32 rounding of each operand;
+      * at v = y, the delta term: cancellation of p_y w against w, error |w| |d p_y|;
+      * the final rounding to the output dtype: 1/2 ulp = 2^-8 |g| (bf16), 2^-24 (fp32);
+      * below the smallest normal (2^-126) everything is absolute: + 2^-126.
+    bound_v = r_out (|o_v| + e_v) + e_v with
+    e_v = inv_temp (p_v (|w| + a (|ln p_v| + |H| + 1)) eps_p + p_v a 2e-6) + [v = y] inv_temp |w| p_y eps_p."""
+    z = inv_temp * x_rows
+    lp = z - lse
+    p = np.exp(lp)
+    c = inv_temp * 1.4426950408889634
+    eps_p = 1e-6 + (2.0 ** -23) * (np.abs(x_rows * c) + abs(lse) * 1.4426950408889634) * np.log(2) + 2.0 ** -22
+    e = inv_temp * (p * (abs(w) + a * (np.abs(lp) + abs(H) + 1.0)) * eps_p + p * a * 2e-6)
+    e[tok] += inv_temp * abs(w) * p[tok] * eps_p[tok]
+    # below the smallest normal fp32 / bf16 (2^-126) the GPU's exp2 and output rounding are
+    # absolute, not relative: one absolute 2^-126 covers that range
+    e += 2.0 ** -126
+    r_out = 2.0 ** -8 if out_bf16 else 2.0 ** -24
+    return r_out * (np.abs(o) + e) + e
+
+
+@pytest.mark.parametrize("V", [128256, 152064])
+@pytest.mark.parametrize("fused", [True, False])
+def test_next1_full_vocab_derived_bound(ctx, V, fused):
+    """NEXT-1 at the BASELINE vocabularies (Llama-3 128256, Qwen2.5 152064), bf16, in the
+    bench's launch configuration (the fused loss + backward pass, orl_ppo_loss_and_grad,
+    and the two-pass orl_ppo_loss + orl_logits_grad / K5): every element of every valid
+    row within the derived bound of _grad_bound; masked rows exactly 0; each row's
+    gradient sums to ~0 (softmax shift invariance)."""
+    B, T = 3, 40
+    c = dict(synth.CONFIGS["llama8b"], c2=0.01, V=V)
+    g = _gpu_batch(29, B, T, V, "mixed", mode="stress")
+    cfg = PathConfig.from_synth(c)
+    dl = torch.full((B, T, V), 3.0, dtype=torch.bfloat16, device=DEV)
+    bufs = Buffers(B, T, DEV)
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    status, st = run_iteration(ctx, g, cfg, bufs, src, mb=2, grad_sink=lambda s, e: dl[s:e], fused_grad=fused)
+    torch.cuda.synchronize()
+    assert status == "ORL_OK"
+    npb = synth.batch_to_numpy({k: v for k, v in g.items() if k in ("logits_new", "tokens", "lengths")})
+    m = parity.valid_mask(npb["lengths"], T)
+    N = float(m.sum())
+    a = 0.01 / N
+    w = _np(bufs.dlogp).astype(np.float64)
+    gg = dl.float().cpu().numpy()
+    n_el, worst = 0, 0.0
+    for b in range(B):
+        for t in range(T):
+            if not m[b, t]:
+                assert np.all(gg[b, t] == 0)
+                continue
+            x = (npb["logits_new"][b, t].astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+            y = int(npb["tokens"][b, t])
+            o = oracle.logits_grad_row(x, y, 1.0, w[b, t], a)
+            lse, _, H = oracle.row_logsoftmax(x, y)
+            bound = _grad_bound(x, y, lse, H, w[b, t], a, 1.0, o, True)
+            err = np.abs(gg[b, t] - o)
+            worst = max(worst, float((err / bound).max()))
+            assert np.all(err <= bound), (b, t, float((err / bound).max()))
+            assert abs(gg[b, t].sum()) <= 1e-2 * np.abs(gg[b, t]).sum() + 1e-12
+            n_el += V
+    assert n_el >= 40 * V and worst > 0
+
+
+def test_mid_size_end_to_end_chain_grpo_and_gae(ctx):
+    """the whole chain from the logits at mid size (B = 8, T = 512,
+    V = 128256 bf16, stress logits so the clip branches are exercised) against the
+    oracle run end to end from the same logits -- log-probs at the north star's 2e-3
+    (with the 1e-4 alarm), advantages / returns / per-token gradients / statistics at
+    1e-5, per-token decisions bit-exact outside a 1e-5 ratio tie band -- for GAE with
+    global whitening (C2-like) and GRPO with the k2 KL loss (C4-like)."""
+    B, T, V = 8, 512, 128256
+    for name in ("llama8b", "grpo"):
+        c = dict(synth.CONFIGS[name])
+        G = c["group_size"]
+        g = _gpu_batch(808, B, T, V, "mixed", c["rewards"], G, mode="stress")
+        if name == "grpo":                                 # one group of 8: not a constant one
+            g["seq_reward"] = torch.tensor([1, 0, 1, 1, 0, 0, 1, 0], dtype=torch.float32, device=DEV)
+        cfg = PathConfig.from_synth(c)
+        status, st, bufs = _run(ctx, g, cfg, mb=3)
+        assert status == "ORL_OK", status
+        npb = synth.batch_to_numpy(g)
+        m = parity.valid_mask(npb["lengths"], T)
+        out, glob = oracle.pipeline([npb], c)
+        o = out[0]
+        for k, buf in (("logp_old", bufs.logp_old), ("logp_ref", bufs.logp_ref), ("logp_new", bufs.logp_new),
+                       ("entropy", bufs.entropy)):
+            parity.check_abs(f"{name} {k}", _np(buf), o[k], m)
+        parity.check_rel(f"{name} adv", _np(bufs.adv), o["adv"], m)
+        if o.get("ret") is not None:
+            parity.check_rel(f"{name} ret", _np(bufs.ret), o["ret"], m)
+        parity.check_rel(f"{name} dloss_dlogp", _np(bufs.dlogp), o["dlogp"], m)
+        if name == "llama8b":
+            parity.check_rel(f"{name} dloss_dv", _np(bufs.dv), o["dv"], m)
+        lp_n, lp_o = _np(bufs.logp_new).astype(np.float64), _np(bufs.logp_old).astype(np.float64)
+        rho = np.exp(lp_n - lp_o)
+        tie = (np.abs(rho - (1 - c["eps_low"])) < 1e-5) | (np.abs(rho - (1 + c["eps_high"])) < 1e-5)
+        gf, of = _np(bufs.flags).astype(np.int64), o["flags"].astype(np.int64)
+        sel = m & ~tie
+        assert np.array_equal(gf[sel] & 1, of[sel] & 1), f"{name}: clip decisions differ"
+        if name == "llama8b":
+            vn, vo, R = npb["values_new"], npb["values_old"], o["ret"]
+            e1 = vn - R
+            e2 = vo + np.clip(vn - vo, -c["eps_v"], c["eps_v"]) - R
+            vtie = np.abs(e1 * e1 - e2 * e2) < 1e-5 * (np.abs(e1) + np.abs(e2)) + 1e-12
+            assert np.array_equal(gf[m & ~vtie] & 2, of[m & ~vtie] & 2), f"{name}: value-clip decisions differ"
+        n_clip = int(np.count_nonzero(of[m] & 1))
+        assert n_clip > 0.01 * m.sum(), f"{name}: stress logits should clip (got {n_clip})"
+        mabs = lambda a: float(np.mean(np.abs(a[m])))  # noqa: E731
+        floors = dict(policy_loss=mabs(o["obj"]), value_loss=mabs(o["vl"]) or 1e-6, entropy=mabs(o["entropy"]),
+                      kl=1e-6, approx_kl_old=1e-6, ratio_mean=1.0)
+        floors["total_loss"] = sum(floors[k] for k in ("policy_loss", "value_loss", "entropy"))
+        for k, fl in floors.items():
+            assert abs(st[k] - glob["stats"][k]) <= parity.REL * max(abs(glob["stats"][k]), fl), \
+                (name, k, st[k], glob["stats"][k])
+        assert abs(st["clip_frac"] - glob["stats"]["clip_frac"]) <= (np.count_nonzero(tie & m) + 1e-9) / m.sum()
+        del g
+        torch.cuda.empty_cache()
+
+
+def test_binding_rejects_bad_arguments(ctx):
+    """orl.py checks every pointer argument before the C call (dtype, device,
+    contiguity, size): int64 token ids, short or CPU per-token arrays, a micro-batch
+    outside the rank batch and a wrong flags dtype raise instead of reaching the kernels."""
+    B, T, V = 2, 8, 64
+    g = _gpu_batch(1, B, T, V, "mixed")
+    logp = torch.zeros(B, T, device=DEV)
+    with pytest.raises(TypeError):
+        orl.orl_logprobs(ctx, g["tokens"].long(), g["lengths"], g["logits_old"], logp)
+    with pytest.raises(ValueError):
+        orl.orl_logprobs(ctx, g["tokens"], g["lengths"], g["logits_old"], torch.zeros(B, T - 1, device=DEV))
+    with pytest.raises(ValueError):
+        orl.orl_logprobs(ctx, g["tokens"], g["lengths"], g["logits_old"], logp.cpu())
+    with pytest.raises(ValueError):
+        orl.orl_logprobs(ctx, g["tokens"], g["lengths"], g["logits_old"], logp, seq_offset=1)
+    with pytest.raises(ValueError):
+        orl.orl_logprobs(ctx, g["tokens"], g["lengths"], g["logits_old"].cpu(), logp)
+    with pytest.raises(TypeError):
+        orl.orl_advantages(ctx, g["lengths"].long(), torch.zeros(B, T, device=DEV), kind="rpp",
+                           shaped_reward=torch.zeros(B, T, device=DEV))
+    orl.orl_begin_iteration(ctx)
+    orl.orl_logprobs(ctx, g["tokens"], g["lengths"], g["logits_old"], logp)
+    orl.orl_advantages(ctx, g["lengths"], torch.zeros(B, T, device=DEV), kind="rpp",
+                       shaped_reward=torch.zeros(B, T, device=DEV))
+    orl.orl_whiten_stats(ctx, True)
+    z = torch.zeros(B, T, device=DEV)
+    with pytest.raises(TypeError):
+        orl.orl_ppo_loss(ctx, g["tokens"], g["lengths"], g["logits_new"], orl.PPOConfig(), z, z, z.clone(),
+                         flags=torch.zeros(B, T, device=DEV))
+    with pytest.raises(ValueError):
+        orl.orl_ppo_loss(ctx, g["tokens"], g["lengths"], g["logits_new"], orl.PPOConfig(), z, z[:1], z.clone())
 
 
 @pytest.mark.parametrize("dtype,V,pad", [("bf16", 50257, 0), ("bf16", 4096, 5), ("f32", 1001, 1)])

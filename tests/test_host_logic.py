@@ -1,0 +1,37 @@
+"""Host-side logic of the N > 1 path (CPU, -m "not gpu"): the token-balanced,
+group-aligned contiguous rank shards bench.py and a trainer use (SPEC S:468
+"contiguous shards weighted by token counts")."""
+import numpy as np
+import pytest
+
+from paper_2405_11143_b200 import synth
+
+
+@pytest.mark.parametrize("name", ["llama8b", "longcot", "grpo", "rpp8"])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+def test_token_balanced_shards(name, n):
+    c = synth.CONFIGS[name]
+    G = max(1, c["group_size"])
+    for mode in ("full", synth.SECONDARY_LENGTHS[name]):
+        L = synth.lengths_for(c["B"], c["T"], 1234, mode).numpy().astype(np.int64)
+        b = synth.split_bounds_tokens(L, n, G)
+        assert len(b) == n and b[0][0] == 0 and b[-1][1] == c["B"]
+        assert all(b[r][1] == b[r + 1][0] for r in range(n - 1))          # contiguous, in order
+        assert all((e - s) % G == 0 and e > s for s, e in b)               # whole groups, never empty
+        tok = np.array([L[s:e].sum() for s, e in b], dtype=np.float64)
+        gmax = L.reshape(-1, G).sum(axis=1).max()
+        # the midpoint rule puts every cut within one group of the ideal token boundary
+        assert tok.max() - tok.mean() <= gmax + 1e-9, (mode, tok)
+        if mode == "full":
+            assert np.all(tok == tok[0]) or c["B"] // G % n
+
+
+def test_token_balanced_shards_edge_cases():
+    # a huge first group: the others still get one group each
+    L = np.array([1000, 1000, 1, 1, 1, 1, 1, 1])
+    b = synth.split_bounds_tokens(L, 3, 2)
+    assert b == [(0, 2), (2, 4), (4, 8)]
+    # all-empty batch falls back to an even split of sequences
+    assert synth.split_bounds_tokens(np.zeros(8), 4, 1) == synth.split_bounds(8, 4, 1)
+    with pytest.raises(ValueError):
+        synth.split_bounds_tokens(np.ones(7), 2, 2)

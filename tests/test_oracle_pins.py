@@ -338,6 +338,12 @@ def test_s7_worked_example_w5(golden):
     res = oracle.ppo_loss([1], [[-1.0]], [[-1.0]], [[1.0]], ret=[[vc["ret"]]], v_new=[[vc["v_new"]]],
                           v_old=[[vc["v_old"]]], eps_v=vc["eps_v"], c1=1.0)
     assert abs(res["vl"][0, 0] - vc["vl"]) < 1e-14 and res["dv"][0, 0] == vc["dvl"]
+    # per-token decision bits: W5's value case takes the clipped branch (0.64 > 0.25),
+    # the policy term is on-policy (rho = 1, never clipped, Z16)
+    assert res["flags"][0, 0] == 2
+    # ratio guard (Z22) and a non-finite loss term set bits 2 and 3
+    r2 = oracle.ppo_loss([2], [[0.0, -40.0]], [[0.0, -5.0]], [[1.0, float("nan")]])
+    assert list(r2["flags"][0]) == [0, 4 | 8]
 
 
 def test_s7_spec_examples(golden):

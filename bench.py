@@ -257,13 +257,15 @@ def make_workload(name, args, env, lengths="full", scaling="strong", batch_overr
         v_old, v_new = (v[s0:e0].clone() for v in synth.values_for(B_global, T, seed))
     n_mb = -(-B_rank // mb)
     full_bytes = 3 * B_rank * T * V * elt
-    pooled = full_bytes > 0.80 * torch.cuda.mem_get_info()[0]
+    # ranks sharing one GPU (ORL_BENCH_SHARED_GPU functional test) split its memory
+    free = torch.cuda.mem_get_info()[0] / (world if env["shared"] else 1)
+    pooled = full_bytes > 0.80 * free
     pool = 0
     if pooled:
         # 2 buffers per model, 8.4 GB each at grpo (>> L2): micro-batch k reads slot k % 2;
         # token ids follow the slot, so each micro-batch's targets match its logits
         per_mb = mb * T * V * elt
-        pool = max(1, min(n_mb, args.pool, int(0.70 * torch.cuda.mem_get_info()[0] // (3 * per_mb))))
+        pool = max(1, min(n_mb, args.pool, int(0.70 * free // (3 * per_mb))))
         for k in range(pool, n_mb):
             a, b = k * mb, min(B_rank, (k + 1) * mb)
             j = (k % pool) * mb

@@ -950,10 +950,12 @@ def test_next2_seq_mean_aggregation(ctx, kind):
 
 @pytest.mark.parametrize("agg", ["token_mean", "seq_mean_token_mean"])
 @pytest.mark.parametrize("V,pad", [(8192, 0), (50257, 0), (8192, 3)])
-def test_next1_fused_forward_backward_matches_two_passes(ctx, agg, V, pad):
-    """orl_ppo_loss_and_grad (one pass, the row re-read from L2) gives the same bits as
-    orl_ppo_loss followed by orl_logits_grad (K5); also for unaligned rows (V = 50257,
-    padded pitches: the aligned interiors by TMA, heads / tails singly; targets in them)."""
+def test_next1_fused_forward_backward_matches_two_passes(ctx, monkeypatch, agg, V, pad):
+    """The K1 fused mode of orl_ppo_loss_and_grad (one pass, the row re-read from L2;
+    ORL_FUSED_K1 selects it over K7) gives the same bits as orl_ppo_loss followed by
+    orl_logits_grad (K5); also for unaligned rows (V = 50257, padded pitches: the
+    aligned interiors by TMA, heads / tails singly; targets in them)."""
+    monkeypatch.setenv("ORL_FUSED_K1", "1")
     B, T = 6, 96
     g = _gpu_batch(29, B, T, V, "mixed", mode="stress")
     g["tokens"][0, :4] = torch.tensor([0, 1, V - 1, V - 2], dtype=torch.int32, device=DEV)
@@ -976,6 +978,69 @@ def test_next1_fused_forward_backward_matches_two_passes(ctx, agg, V, pad):
     assert torch.equal(out[True][1], out[False][1])
     for k in ("logp_new", "entropy", "lse", "dlogp", "dv"):
         assert torch.equal(getattr(out[True][2], k), getattr(out[False][2], k)), k
+
+
+@pytest.mark.parametrize("dtype,V,B,T,agg", [("bf16", 128256, 3, 40, "token_mean"), ("bf16", 8192, 6, 96, "seq_mean_token_mean"),
+                                             ("bf16", 152064, 2, 24, "token_mean"), ("f32", 4096, 5, 33, "token_mean"),
+                                             ("bf16", 136, 7, 50, "token_mean")])
+def test_next1_k7_cluster_pass(ctx, dtype, V, B, T, agg):
+    """K7 (orl_ppo_loss_and_grad on aligned rows: cluster pairs keep each half-row in
+    shared memory between the forward and the backward): per-token outputs and stats
+    equal the two-pass path (orl_ppo_loss + K5) to rounding of the merge order (the
+    two halves' online states are merged in another order), decisions bit-exact,
+    every dlogits element within the derived NEXT-1 bound of the fp64 oracle, masked
+    rows exactly 0, and run-to-run bit identical."""
+    c = dict(synth.CONFIGS["llama8b"], V=V, c2=0.01, loss_agg=agg)
+    if dtype == "f32":
+        g = _to_dev(synth.make_batch(31, B, T, V, "f32", "stress", "tiny"))
+    else:
+        g = _gpu_batch(31, B, T, V, "mixed", mode="stress")
+    g["tokens"][0, :4] = torch.tensor([0, 1, V - 1, V // 2], dtype=torch.int32, device=DEV)
+    # spikes far above the first-vector seed (> 64 log2 units): the exact redo of a held half-row,
+    # in the first and in the second half of a row
+    for r in ("old", "ref", "new"):
+        g[f"logits_{r}"][1, 0, 5] = 90.0
+        g[f"logits_{r}"][1, 1, V - 3] = 70.0
+    cfg = PathConfig.from_synth(c)
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    out = {}
+    for key, fused in (("k7", True), ("k7b", True), ("two", False)):
+        dl = torch.full((B, T, V), 7.0, dtype=tdt, device=DEV)
+        bufs = Buffers(B, T, DEV)
+        status, st = run_iteration(ctx, g, cfg, bufs, src, mb=2, grad_sink=lambda s, e: dl[s:e], fused_grad=fused)
+        torch.cuda.synchronize()
+        assert status == "ORL_OK", status
+        out[key] = (st, dl, bufs)
+    assert out["k7"][0] == out["k7b"][0] and torch.equal(out["k7"][1], out["k7b"][1])     # run to run
+    m = parity.valid_mask(_np(g["lengths"]), T)
+    (st7, dl7, b7), (st2, dl2, b2) = out["k7"], out["two"]
+    npb = synth.batch_to_numpy({k: g[k] for k in ("logits_new", "tokens", "lengths")})
+    ora = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"])
+    for k in ("logp_new", "entropy", "lse"):
+        parity.check_abs(f"k7 {k}", _np(getattr(b7, k)), ora[k.replace("_new", "")], m)
+        np.testing.assert_allclose(_np(getattr(b7, k))[m], _np(getattr(b2, k))[m], rtol=0, atol=5e-5, err_msg=k)
+    parity.check_rel("dlogp", _np(b7.dlogp), _np(b2.dlogp).astype(np.float64), m, rel=1e-5)
+    assert np.array_equal(_np(b7.flags), _np(b2.flags))
+    for k in ("policy_loss", "entropy", "kl", "ratio_mean", "total_loss", "value_loss"):
+        assert abs(st7[k] - st2[k]) <= 1e-5 * max(abs(st2[k]), 1e-3), (k, st7[k], st2[k])
+    gg = dl7.float().cpu().numpy()
+    assert np.all(gg[~m] == 0)
+    w = _np(b7.dlogp).astype(np.float64)
+    N = float(m.sum())
+    L = npb["lengths"]
+    for b in range(B):
+        a = 0.01 / (float((L > 0).sum()) * float(L[b])) if agg != "token_mean" else 0.01 / N
+        for t in range(int(L[b])):
+            row = npb["logits_new"][b, t]
+            x = (row.astype(np.uint32) << 16).view(np.float32).astype(np.float64) if dtype == "bf16" \
+                else row.astype(np.float64)
+            y = int(npb["tokens"][b, t])
+            o = oracle.logits_grad_row(x, y, 1.0, w[b, t], a)
+            lse, _, H = oracle.row_logsoftmax(x, y)
+            bound = _grad_bound(x, y, lse, H, w[b, t], a, 1.0, o, dtype == "bf16")
+            err = np.abs(gg[b, t] - o)
+            assert np.all(err <= bound), (b, t, float((err / bound).max()))
 
 
 def test_lengths_from_attention_mask(ctx):

@@ -864,12 +864,10 @@ def run_e2e(args, env, W, R_dev):
         tt = torch.tensor([dt], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
-    # the device-resident step over the same micro-batch buffers gives the same bits
-    if W["pool"] or H >= W["n_mb"]:
-        ref_status, ref_st = R_dev["status"], R_dev["stats"]
-    else:
-        ref_status, ref_st = run_iteration(ctx, batch, cfg, bufs, lambda r, s, e: dev_slot[r][(s // mb) % H][: e - s],
-                                           mb, pdl_chain=True)
+    # the device-resident step over the same micro-batch buffers gives the same bits (run on
+    # every rank: the statistics are global, and the collectives need every rank)
+    ref_status, ref_st = run_iteration(ctx, batch, cfg, bufs, lambda r, s, e: dev_slot[r][(s // mb) % H][: e - s],
+                                       mb, pdl_chain=True)
     same = (status, st) == (ref_status, ref_st)
     del stage, host
     torch.cuda.empty_cache()

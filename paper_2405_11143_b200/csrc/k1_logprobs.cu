@@ -29,8 +29,6 @@
 //   * Loss partials: fp64 per epilogue warp in smem, per CTA in a workspace,
 //     reduced in fixed order by the last CTA (ticket) -> deterministic, no
 //     extra launch.
-// K7 at the end of this file is the fused actor pass (NEXT-1) over cluster
-// pairs that keep each row in shared memory between forward and backward.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -282,17 +280,15 @@ struct EpiOut {
     float lse, H, w;
 };
 
-// emit = false (the second CTA of a K7 cluster pair): compute only *eo, no stores,
-// no counters, no partial sums -- the pair's first CTA emits the row.
 // publish(eo) runs as soon as (lse, H, w) are known, before the rest of the loss
-// terms: the fused backward waits for exactly these (shorter critical path).
+// terms: the fused backward waits for exactly these.
 struct NoPublish {
     __device__ void operator()(const EpiOut &) const {}
 };
 template <int MODE, typename Publish = NoPublish>
 __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Online tot,
                              float target, const float *side, const double *wh, double *wacc,
-                             EpiOut *eo = nullptr, bool emit = true, const Publish &publish = Publish()) {
+                             EpiOut *eo = nullptr, const Publish &publish = Publish()) {
     const int64_t i = (p.seq_offset + b) * (int64_t)p.T + t;
     const bool oob = (y < 0) || (y >= p.V);
     const double log2s = log2((double)tot.s);
@@ -301,19 +297,17 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
     double logp = (double)target * (double)p.inv_temp - lse;
     const bool dead = tot.m / p.c2 < 0.5f * kNegClampF32;  // every logit -inf
     if (oob) {
-        if (emit) atomicAdd(&p.err[0], 1ull);
+        atomicAdd(&p.err[0], 1ull);
         lse = H = logp = __longlong_as_double(0x7ff8000000000000ll);
     } else if (dead || !(isfinite(lse) && isfinite(logp) && isfinite(H))) {
-        if (emit) atomicAdd(&p.err[1], 1ull);
+        atomicAdd(&p.err[1], 1ull);
         if (dead) lse = H = logp = __longlong_as_double(0x7ff8000000000000ll);
     }
     const float logp_f = (float)logp, H_f = (float)H;
-    if (emit) {
-        p.logp[i] = logp_f;
-        if (p.entropy) p.entropy[i] = H_f;
-        if (p.lse) p.lse[i] = (float)lse;
-        if (p.gathered) p.gathered[i] = oob ? __int_as_float(0x7fc00000) : target;
-    }
+    p.logp[i] = logp_f;
+    if (p.entropy) p.entropy[i] = H_f;
+    if (p.lse) p.lse[i] = (float)lse;
+    if (p.gathered) p.gathered[i] = oob ? __int_as_float(0x7fc00000) : target;
 
     if (MODE == kModeLogprob) {
         if (p.partner) {
@@ -354,7 +348,6 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
             eo->w = wf;
             publish(*eo);
         }
-        if (!emit) return;
         double vl = 0.0, dvl = 0.0;
         bool vclipped = false;
         if (p.v_new) {
@@ -876,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         mbar_arrive(&S.grad_full[rl % kGradRows]);
                     }
                 };
-                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew], &eo, true, publish);
+                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew], &eo, publish);
             }
             __syncwarp();
         }
@@ -1280,502 +1273,6 @@ cudaError_t launch_k6_merge(const K1Params &p, int mode, int num_sms, cudaStream
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-// ---------------------------------------------------------------- K7: fused actor pass
-// S1 + S7..S9 + NEXT-1 (dL/dlogits) in one pass with NO second read of the logits:
-// a cluster of two CTAs (one TPC) owns each row; CTA q streams half q of the row
-// (16-byte aligned split) into a shared-memory ring and KEEPS it there: the
-// forward consumes the chunks without releasing them, the pair exchanges its two
-// half-row online states through distributed shared memory (st.async into the
-// partner's slot + mbarrier complete_tx), both CTAs run the same fp64 row epilogue
-// on the merged state (CTA 0 emits the per-token outputs and partial sums), and the
-// backward re-reads the half-row from shared memory, writes dlogits and only then
-// releases each stage.  The ring holds one half-row plus E = stages - chunks early
-// chunks of the next row, which the consumers stream while the epilogue of the
-// current row runs (schedule per CTA: F(i)[0, E), B(i-1), F(i)[E, n)).  DRAM traffic
-// is exactly the algorithmic V*elt read + V*elt written per token (DESIGN 5.5c).
-// Rows must be 16-byte aligned (base, pitches, V*elt) and a half-row must fit in
-// the ring with E >= 2; otherwise the host falls back to kModeLossGrad.
-#ifndef ORL_K7_STAGES
-#define ORL_K7_STAGES 13
-#endif
-namespace k7 {
-constexpr int kChunk = 16384;
-constexpr int kStages = ORL_K7_STAGES;
-constexpr int kNW = 4 * (kChunk / 16 / kConsumers);  // 32-bit words per thread per chunk (8)
-constexpr int kVec = kNW / 4;                        // 16-byte vectors per thread per chunk (2)
-constexpr int kSlots = kEpiWarps;                    // row slot rl % kSlots, drained by epilogue warp rl % kEpiWarps
-constexpr int kGrad = 4;
-constexpr int kPeer = 4;
-constexpr int kRowInfo = 32;
-constexpr int kMaxCluster = 4;
-static_assert(kChunk % (16 * kConsumers) == 0, "chunk must split evenly");
-static_assert(kGrad % kEpiWarps == 0 && kPeer % kEpiWarps == 0, "rings must map to fixed epilogue warps");
-}  // namespace k7
-
-// Consumer states of one row after a 2-round xor pre-merge inside each warp (8 per warp).
-constexpr int kK7States = kConsumers / 4;
-struct K7RowSlot {
-    float m[kK7States], s[kK7States], u[kK7States];
-    float target;
-    float pad[31];
-};
-struct __align__(128) K7Smem {
-    uint8_t stage[k7::kStages][k7::kChunk];
-    uint64_t full[k7::kStages];
-    uint64_t empty[k7::kStages];
-    uint64_t row_full[k7::kSlots];
-    uint64_t row_empty[k7::kSlots];
-    uint64_t grad_full[k7::kGrad];
-    uint64_t peer_full[k7::kPeer];   // every partner's part state of row rl arrived (16 tx bytes each)
-    uint64_t peer_empty[k7::kPeer];  // every partner consumed what this CTA wrote into its slot
-    float4 peer_state[k7::kPeer][k7::kMaxCluster];  // (m, s, u, target) written by partner r at [.][r]
-    int32_t row_y[k7::kRowInfo];
-    GradRow grad[k7::kGrad];
-    K7RowSlot slot[k7::kSlots];
-    double wacc[kEpiWarps][kNumPartials];
-};
-
-size_t k7_smem_bytes(int B) {
-    return sizeof(K7Smem) + sizeof(int32_t) * (size_t)((B > kSmemPrefixMax ? 0 : B) + 32);
-}
-
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t map_peer(const void *local, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
-}
-// 16 bytes into the partner's shared memory; completes `bytes` on the partner's mbarrier
-__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                     raddr),
-                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t rbar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-template <typename Tin, int C>
-__global__ void __cluster_dims__(C, 1, 1) __launch_bounds__(kThreads, 1) k7_fused_kernel(const K1Params p) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    K7Smem &S = *reinterpret_cast<K7Smem *>(smem_raw);
-    int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw + sizeof(K7Smem));
-    int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t q = cluster_ctarank();                   // part of every row this CTA owns
-    const int64_t cid = blockIdx.x / C, ncl = gridDim.x / C;  // cluster (row-stream) index and count
-
-    if (tid == 0) {
-        for (int s = 0; s < k7::kStages; ++s) {
-            mbar_init(&S.full[s], 1);
-            mbar_init(&S.empty[s], kConsumerWarps);
-        }
-        for (int s = 0; s < k7::kSlots; ++s) {
-            mbar_init(&S.row_full[s], kConsumerWarps);
-            mbar_init(&S.row_empty[s], 1);
-        }
-        for (int s = 0; s < k7::kGrad; ++s) mbar_init(&S.grad_full[s], 1);
-        for (int s = 0; s < k7::kPeer; ++s) {
-            mbar_init(&S.peer_full[s], 1);
-            mbar_init(&S.peer_empty[s], C - 1);
-        }
-        fence_mbar_init();
-    }
-    if (tid < kEpiWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
-    if (!p.pdl_chain || p.cum_global) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (p.cum_global) __syncthreads();
-    else build_prefix(p, cum_s, warp_tot);
-    cluster_sync_all();  // the partner's barriers are initialised before any remote access
-    const int64_t N = cum[p.B - 1];
-    const int64_t row_bytes = p.row_bytes;
-    const int64_t part = ((row_bytes + C - 1) / C + 15) & ~(int64_t)15;  // 16-byte aligned split
-    const int64_t my_off = (int64_t)q * part;
-    const int64_t my_len = min(part, row_bytes - my_off);  // > 0 (host: row_bytes >= 256 C)
-    const int n_my = (int)((my_len + k7::kChunk - 1) / k7::kChunk);
-    const int E = k7::kStages - n_my;  // >= 2 (host)
-    const int64_t n_rows = N > cid ? (N - cid + ncl - 1) / ncl : 0;
-
-    if (warp == kProducerWarp) {
-        // ===================== producer: one lane streams this CTA's half of each row
-        if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int64_t rl = 0; rl < n_rows; ++rl) {
-                int b, t;
-                locate_row(cum, p.B, cid + rl * ncl, b, t);
-                const int y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
-                const char *src =
-                    p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt +
-                    my_off;
-                for (int c = 0; c < n_my; ++c) {
-                    const uint32_t bytes = (uint32_t)min((int64_t)k7::kChunk, my_len - (int64_t)c * k7::kChunk);
-                    mbar_wait(&S.empty[stage], phase ^ 1u);
-                    if (c == 0) S.row_y[rl % k7::kRowInfo] = y;  // released by the arrive below
-                    mbar_arrive_expect_tx(&S.full[stage], bytes);
-                    tma_load_1d(S.stage[stage], src + (int64_t)c * k7::kChunk, bytes, &S.full[stage], pol);
-                    if (++stage == k7::kStages) { stage = 0; phase ^= 1u; }
-                }
-            }
-        }
-    } else if (warp >= kEpilogueWarp) {
-        // ===================== epilogue: merge, pair exchange, fp64 row epilogue, grad constants
-        const int ew = warp - kEpilogueWarp;
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (q == 0) zero_masked(p, cum, lane + 32 * ew, 32 * kEpiWarps, kModeLossGrad, cid, ncl);
-        double wh[5];
-        wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3]; wh[4] = p.whiten[4];
-        for (int64_t rl = ew; rl < n_rows; rl += kEpiWarps) {
-            int b, t;
-            locate_row(cum, p.B, cid + rl * ncl, b, t);
-            const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
-            const int y = __ldg(p.tokens + gi);
-            float side = 0.f;
-            if (lane < 6) side = load_side(p, kModeLoss, lane, gi, b);
-            const int slot = (int)(rl % k7::kSlots);
-            mbar_wait(&S.row_full[slot], (uint32_t)(rl / k7::kSlots) & 1u);
-            const K7RowSlot &R = S.slot[slot];
-            Online st{R.m[lane], R.s[lane], R.u[lane]};
-#pragma unroll
-            for (int w = 1; w < kK7States / 32; ++w)
-                st = online_merge(st, Online{R.m[lane + 32 * w], R.s[lane + 32 * w], R.u[lane + 32 * w]});
-            st = warp_merge(st);
-            const float my_target = R.target;
-            float sv[6];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&S.row_empty[slot]);
-                // ---- exchange the half-row states with the partner CTA (DSMEM)
-                const int ps = (int)(rl % k7::kPeer);
-                const int64_t use = rl / k7::kPeer;
-                const float4 mine = make_float4(st.m, st.s, st.u, my_target);
-#ifndef ORL_K7_DEBUG_NOXCHG
-                mbar_arrive_expect_tx(&S.peer_full[ps], 16 * (C - 1));
-                if (use > 0) mbar_wait_cluster(&S.peer_empty[ps], (uint32_t)(use - 1) & 1u);
-#pragma unroll
-                for (int r = 1; r < C; ++r) {
-                    const uint32_t dst = (q + r) % C;
-                    st_async_v4(map_peer(&S.peer_state[ps][q], dst), mine, map_peer(&S.peer_full[ps], dst));
-                }
-                mbar_wait_cluster(&S.peer_full[ps], (uint32_t)use & 1u);
-                float4 part_state[C];
-#pragma unroll
-                for (int r = 0; r < C; ++r) part_state[r] = r == (int)q ? mine : S.peer_state[ps][r];
-#pragma unroll
-                for (int r = 1; r < C; ++r) mbar_arrive_remote(map_peer(&S.peer_empty[ps], (q + r) % C));
-#else  // timing experiment only (wrong results): no exchange
-                (void)ps; (void)use;
-                float4 part_state[C];
-#pragma unroll
-                for (int r = 0; r < C; ++r) part_state[r] = mine;
-#endif
-                // every CTA merges the parts in rank order: identical bits on all of them
-                Online tot{part_state[0].x, part_state[0].y, part_state[0].z};
-#pragma unroll
-                for (int r = 1; r < C; ++r) tot = online_merge(tot, Online{part_state[r].x, part_state[r].y, part_state[r].z});
-                const int64_t ybyte = (int64_t)y * p.elt;
-                const int yq = (int)min(ybyte / part, (int64_t)C - 1);
-                float target = part_state[0].w;
-#pragma unroll
-                for (int r = 1; r < C; ++r)
-                    if (r == yq) target = part_state[r].w;
-                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-                EpiOut eo{0.f, 0.f, 0.f};
-                auto publish = [&](const EpiOut &e) {  // as soon as (lse, H, w) exist
-                    // same fp32 constants as K5 (orl_logits_grad) computes from the saved arrays
-                    const float a = (float)(p.loss_agg == 1 ? p.c2_ent / (wh[4] * (double)L) : p.c2_ent / wh[0]);
-                    GradRow &g = S.grad[rl % k7::kGrad];
-                    g.out_off = logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.out_stride_b, p.out_stride_t);
-                    g.y = y;
-                    g.l2 = e.lse * kLog2e;
-                    g.A1 = p.inv_temp * a * (float)kLn2;
-                    g.A0 = p.inv_temp * (a * e.H - e.w);
-                    g.wt = p.inv_temp * e.w;
-                    mbar_arrive(&S.grad_full[rl % k7::kGrad]);
-                };
-                row_epilogue<kModeLoss>(p, b, t, L, y, tot, target, sv, wh, S.wacc[ew], &eo, q == 0, publish);
-            }
-            __syncwarp();
-        }
-        if (kEpiWarps > 1) named_bar_sync(1, 32 * kEpiWarps);
-        if (ew == 0) {
-            double tot[kNumPartials];
-#pragma unroll
-            for (int c = 0; c < kNumPartials; ++c) {
-                double v = 0.0;
-                for (int e = 0; e < kEpiWarps; ++e) v += S.wacc[e][c];  // fixed order (zeros on CTA 1)
-                tot[c] = v;
-            }
-            finish_partials_warp(p, tot, lane);
-        }
-    } else {
-        // ===================== consumers (warps 0..15)
-        const int ct = tid;
-        const float c2 = p.c2;
-        const uint64_t c2p = pack2(c2, c2);
-        int stage = 0;
-        uint32_t phase = 0;
-        int row_stage0_even = 0, row_stage0_odd = 0;  // first stage of row rl (rl even / odd)
-        ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
-        float tgt = 0.f;
-        bool have_tgt = false;
-        int tchunk = -1, tin = 0;
-        bool towner = false;
-        auto fwd_chunks = [&](int64_t rl, int c0, int c1) {
-            for (int ci = c0; ci < min(c1, n_my); ++ci) {
-                mbar_wait(&S.full[stage], phase);
-                if (ci == 0) {  // row start
-                    acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
-                    have_tgt = false;
-                    if (rl & 1) row_stage0_odd = stage;
-                    else row_stage0_even = stage;
-                    const int y = S.row_y[rl % k7::kRowInfo];
-                    const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin) - my_off;  // within this half
-                    const bool y_ok = (y >= 0) && ((int64_t)y < p.V) && ybyte >= 0 && ybyte < my_len;
-                    tchunk = y_ok ? (int)(ybyte / k7::kChunk) : -1;
-                    tin = (int)(ybyte % k7::kChunk);
-                    towner = ((tin >> 4) % kConsumers) == ct;
-                }
-                const int bytes = (int)min((int64_t)k7::kChunk, my_len - (int64_t)ci * k7::kChunk);
-                const uint8_t *sb = S.stage[stage];
-                if (ci == tchunk && towner) {  // raw target value, before any clamping
-                    tgt = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(sb + tin)) << 16)
-                                           : *reinterpret_cast<const float *>(sb + tin);
-                    have_tgt = true;
-                }
-                uint32_t w[k7::kNW];
-                if (bytes == k7::kChunk) load_words<Tin, true, k7::kNW>(w, sb, ct, k7::kChunk >> 4);
-                else load_words<Tin, false, k7::kNW>(w, sb, ct, bytes >> 4);
-                if (++stage == k7::kStages) { stage = 0; phase ^= 1u; }  // the stage stays full until B(rl)
-                if (ci == 0) {  // seed m with the max of the thread's first 16-byte vector (as K1)
-                    float cm;
-                    if (sizeof(Tin) == 2) {
-                        const uint32_t mx = hmax2_nan(hmax2_nan(hmax2_nan(w[0], kNegClampBf16x2), w[1]), hmax2_nan(w[2], w[3]));
-                        cm = fmax_nan(bf16lo(mx), bf16hi(mx));
-                    } else {
-                        cm = fmax_nan(fmax_nan(fmax_nan(__uint_as_float(w[0]), __uint_as_float(w[1])),
-                                               fmax_nan(__uint_as_float(w[2]), __uint_as_float(w[3]))), kNegClampF32);
-                    }
-                    acc.m = fmax_nan(cm * c2, kMInit);
-                }
-                // fast path only: the half-row stays in shared memory, so an overflow (an element
-                // > m + 64 log2 units), -inf or NaN is redone exactly once, at the row end
-                acc_words<Tin, true, 0, k7::kNW>(acc, w, c2p);
-            }
-        };
-        auto fwd_publish = [&](int64_t rl) {
-            if (needs_redo<true>(acc)) {  // rare: exact pass over the held chunks (clamp, max, rescale)
-                acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
-                int stg = (rl & 1) ? row_stage0_odd : row_stage0_even;
-                for (int c = 0; c < n_my; ++c) {
-                    const int bytes = (int)min((int64_t)k7::kChunk, my_len - (int64_t)c * k7::kChunk);
-                    uint32_t w[k7::kNW];
-                    load_words<Tin, false, k7::kNW>(w, S.stage[stg], ct, bytes >> 4);
-                    exact_words<Tin, true, k7::kNW>(acc, w, c2, c2p);
-                    if (++stg == k7::kStages) stg = 0;
-                }
-            }
-            float s0, s1, s2, s3;
-            unpack2(fadd2(acc.sA, acc.sB), s0, s1);
-            unpack2(fadd2(acc.uA, acc.uB), s2, s3);
-            Online st{acc.m, s0 + s1, s2 + s3};
-#pragma unroll
-            for (int off = 1; off <= 2; off <<= 1) {  // pre-merge lanes 4k..4k+3 (fixed order: lane 4k keeps it)
-                Online o;
-                o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
-                o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
-                o.u = __shfl_xor_sync(0xffffffffu, st.u, off);
-                st = online_merge(st, o);
-            }
-            const int slot = (int)(rl % k7::kSlots);
-            mbar_wait(&S.row_empty[slot], ((uint32_t)(rl / k7::kSlots) & 1u) ^ 1u);
-            K7RowSlot &R = S.slot[slot];
-            if ((lane & 3) == 0) {
-                const int k = warp * 8 + (lane >> 2);
-                R.m[k] = st.m;
-                R.s[k] = st.s;
-                R.u[k] = st.u;
-            }
-            if (have_tgt) R.target = tgt;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.row_full[slot]);
-        };
-        const uint64_t st_pol = l2_evict_first_policy();
-        auto bwd_row = [&](int64_t rb) {
-            // dL/dx_v = p_v (A1 t_v + A0) + [v = y] wt,  t_v = x_v c - lse log2 e, from shared memory
-            mbar_wait(&S.grad_full[rb % k7::kGrad], (uint32_t)(rb / k7::kGrad) & 1u);
-            const GradRow g = S.grad[rb % k7::kGrad];
-            char *obase0 = reinterpret_cast<char *>(p.dlogits) + g.out_off * (int64_t)sizeof(Tin) + my_off;
-            const uint64_t nl2 = pack2(-g.l2, -g.l2), A1p = pack2(g.A1, g.A1), A0p = pack2(g.A0, g.A0);
-            const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin) - my_off;
-            const bool y_here = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= 0 && ybyte < my_len;
-            // the chunk whose vector holding y this thread owns (-1: none)
-            const int y_chunk = (y_here && (((int)(ybyte % k7::kChunk) >> 4) % kConsumers) == ct)
-                                    ? (int)(ybyte / k7::kChunk) : -1;
-            int stg = (rb & 1) ? row_stage0_odd : row_stage0_even;
-            for (int c = 0; c < n_my; ++c) {
-                const int64_t off = (int64_t)c * k7::kChunk;
-                const int bytes = (int)min((int64_t)k7::kChunk, my_len - off);
-                const int nvec = bytes >> 4;
-                const uint8_t *sb = S.stage[stg];
-                const bool own_y = c == y_chunk;
-                float xy = 0.f;
-                if (own_y) {
-                    const uint8_t *qq = sb + (ybyte - off);
-                    xy = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(qq)) << 16)
-                                          : *reinterpret_cast<const float *>(qq);
-                }
-                uint4 v[k7::kVec];
-#pragma unroll
-                for (int k = 0; k < k7::kVec; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    if (vi < nvec) v[k] = lds128(sb + vi * 16);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.empty[stg]);  // the producer may refill this stage now
-                if (++stg == k7::kStages) stg = 0;
-                char *obase = obase0 + off;
-#pragma unroll
-                for (int k = 0; k < k7::kVec; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    if (vi >= nvec) continue;
-                    const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                    uint32_t o[4];
-                    if (sizeof(Tin) == 2) {
-#pragma unroll
-                        for (int qd = 0; qd < 4; ++qd) {
-                            const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[qd]), c2p, nl2);
-                            float t0, t1;
-                            unpack2(t2, t0, t1);
-                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
-                            float g0, g1;
-                            unpack2(gr, g0, g1);
-                            o[qd] = f32x2_to_bf16x2_rn(g0, g1);
-                        }
-                    } else {
-#pragma unroll
-                        for (int qd = 0; qd < 2; ++qd) {
-                            uint64_t x;
-                            asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(w4[2 * qd]), "r"(w4[2 * qd + 1]));
-                            const uint64_t t2 = ffma2(x, c2p, nl2);
-                            float t0, t1;
-                            unpack2(t2, t0, t1);
-                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
-                            float g0, g1;
-                            unpack2(gr, g0, g1);
-                            o[2 * qd] = __float_as_uint(g0);
-                            o[2 * qd + 1] = __float_as_uint(g1);
-                        }
-                    }
-                    stg128_hint(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]), st_pol);
-                }
-                if (own_y) {  // program-ordered rewrite of the target element with the delta term
-                    const float t2 = fmaf(xy, c2, -g.l2);
-                    const float gy = __fadd_rn(__fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0)), g.wt);  // not contracted
-                    Tin *yp = reinterpret_cast<Tin *>(obase0 + ybyte);
-                    if (sizeof(Tin) == 2) {
-                        const uint32_t hb = f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu;
-                        asm volatile("st.global.u16 [%0], %1;" ::"l"(yp), "h"((unsigned short)hb) : "memory");
-                    } else {
-                        *reinterpret_cast<float *>(yp) = gy;
-                    }
-                }
-            }
-        };
-        // per CTA: F(0), then F(i)[0, E), B(i-1), F(i)[E, n), ..., B(n-1)
-        for (int64_t rl = 0; rl <= n_rows; ++rl) {
-            if (rl < n_rows) fwd_chunks(rl, 0, E);
-            if (rl > 0) bwd_row(rl - 1);
-            if (rl < n_rows) {
-                fwd_chunks(rl, E, n_my);
-                fwd_publish(rl);
-            }
-        }
-        if (p.zero_masked_grad && !p.cu_seqlens) {  // this CTA's half of every masked dlogits row
-            const int64_t total = (int64_t)p.B * p.T;
-            for (int64_t qq = cid; qq < total; qq += ncl) {
-                const int b = (int)(qq / p.T), t = (int)(qq % p.T);
-                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-                if (t < L) continue;
-                char *orow = reinterpret_cast<char *>(p.dlogits) +
-                             ((int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t) * (int64_t)sizeof(Tin) + my_off;
-                for (int64_t o = (int64_t)ct * 16; o < my_len; o += (int64_t)kConsumers * 16)
-                    stg128_cs(orow + o, make_uint4(0u, 0u, 0u, 0u));
-            }
-        }
-    }
-    cluster_sync_all();  // no CTA leaves while its partner may still touch its shared memory
-}
-
-template <typename Tin, int C>
-static cudaError_t launch_k7_typed(const K1Params &p, int num_sms, cudaStream_t s) {
-    const size_t smem = k7_smem_bytes(p.B);
-    auto kern = k7_fused_kernel<Tin, C>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cfg.gridDim = dim3((unsigned)(C * (num_sms / C)));
-    int ncl = 0;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
-    if (e != cudaSuccess) return e;
-    if (ncl < 1) return cudaErrorInvalidConfiguration;
-    int64_t grid_cl = ncl;
-    const int64_t N_upper = (int64_t)p.B * p.T;
-    if (grid_cl > N_upper) grid_cl = N_upper;
-    if (C * grid_cl > p.ws_stride) grid_cl = p.ws_stride / C;
-    cfg.gridDim = dim3((unsigned)(C * grid_cl));
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-// cluster size: ORL_K7_CLUSTER (2 or 4) if set, else 2
-static int k7_cluster() {
-    const char *e = getenv("ORL_K7_CLUSTER");
-    return e && atoi(e) == 4 ? 4 : 2;
-}
-
-bool k7_eligible(int64_t row_bytes) {
-    const int C = k7_cluster();
-    if (row_bytes < 256 * C || row_bytes % 16 != 0) return false;
-    const int64_t part = ((row_bytes + C - 1) / C + 15) & ~(int64_t)15;
-    const int64_t n = (part + k7::kChunk - 1) / k7::kChunk;
-    return n + 2 <= k7::kStages;
-}
-
-cudaError_t launch_k7(const K1Params &p, int num_sms, cudaStream_t s) {
-    if (k7_cluster() == 4)
-        return p.elt == 2 ? launch_k7_typed<uint16_t, 4>(p, num_sms, s) : launch_k7_typed<float, 4>(p, num_sms, s);
-    return p.elt == 2 ? launch_k7_typed<uint16_t, 2>(p, num_sms, s) : launch_k7_typed<float, 2>(p, num_sms, s);
 }
 
 // ---------------------------------------------------------------- launcher

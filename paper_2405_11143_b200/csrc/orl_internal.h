@@ -79,11 +79,6 @@ struct K1Params {
 // Launch K1.  Returns the CUDA launch error.  `tma` selects the TMA bulk-copy
 // kernel (requires 16-byte aligned rows and row_bytes % 16 == 0).
 cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaStream_t s);
-// K7 (NEXT-1 fused actor pass over cluster pairs, rows kept in shared memory): true when
-// a row of row_bytes (16-byte aligned) fits the pair's rings; launch_k7 takes K1Params
-// as for kModeLossGrad (unaligned = 0).
-bool k7_eligible(int64_t row_bytes);
-cudaError_t launch_k7(const K1Params &p, int num_sms, cudaStream_t s);
 // Micro-batches with more sequences than this keep the length prefix in global
 // memory (written by launch_lengths_prefix) instead of shared memory.
 constexpr int kSmemPrefixMax = 1024;

@@ -950,12 +950,10 @@ def test_next2_seq_mean_aggregation(ctx, kind):
 
 @pytest.mark.parametrize("agg", ["token_mean", "seq_mean_token_mean"])
 @pytest.mark.parametrize("V,pad", [(8192, 0), (50257, 0), (8192, 3)])
-def test_next1_fused_forward_backward_matches_two_passes(ctx, monkeypatch, agg, V, pad):
-    """The K1 fused mode of orl_ppo_loss_and_grad (one pass, the row re-read from L2;
-    ORL_FUSED_K1 selects it over K7) gives the same bits as orl_ppo_loss followed by
-    orl_logits_grad (K5); also for unaligned rows (V = 50257, padded pitches: the
-    aligned interiors by TMA, heads / tails singly; targets in them)."""
-    monkeypatch.setenv("ORL_FUSED_K1", "1")
+def test_next1_fused_forward_backward_matches_two_passes(ctx, agg, V, pad):
+    """orl_ppo_loss_and_grad (one pass, the row re-read from L2) gives the same bits as
+    orl_ppo_loss followed by orl_logits_grad (K5); also for unaligned rows (V = 50257,
+    padded pitches: the aligned interiors by TMA, heads / tails singly; targets in them)."""
     B, T = 6, 96
     g = _gpu_batch(29, B, T, V, "mixed", mode="stress")
     g["tokens"][0, :4] = torch.tensor([0, 1, V - 1, V - 2], dtype=torch.int32, device=DEV)
@@ -983,13 +981,13 @@ def test_next1_fused_forward_backward_matches_two_passes(ctx, monkeypatch, agg, 
 @pytest.mark.parametrize("dtype,V,B,T,agg", [("bf16", 128256, 3, 40, "token_mean"), ("bf16", 8192, 6, 96, "seq_mean_token_mean"),
                                              ("bf16", 152064, 2, 24, "token_mean"), ("f32", 4096, 5, 33, "token_mean"),
                                              ("bf16", 136, 7, 50, "token_mean")])
-def test_next1_k7_cluster_pass(ctx, dtype, V, B, T, agg):
-    """K7 (orl_ppo_loss_and_grad on aligned rows: cluster pairs keep each half-row in
-    shared memory between the forward and the backward): per-token outputs and stats
-    equal the two-pass path (orl_ppo_loss + K5) to rounding of the merge order (the
-    two halves' online states are merged in another order), decisions bit-exact,
-    every dlogits element within the derived NEXT-1 bound of the fp64 oracle, masked
-    rows exactly 0, and run-to-run bit identical."""
+def test_next1_fused_pass_spikes_and_bound(ctx, dtype, V, B, T, agg):
+    """The fused actor pass (orl_ppo_loss_and_grad) at the BASELINE vocabularies and odd
+    shapes, with spikes far above the first-vector seed (the exact redo) in old, ref and
+    actor logits: log-probs / entropy / lse against the oracle, the same outputs as the
+    two-pass path (orl_ppo_loss + K5), decisions bit-exact, every dlogits element within
+    the derived NEXT-1 bound of the fp64 oracle, masked rows exactly 0, run-to-run bit
+    identical."""
     c = dict(synth.CONFIGS["llama8b"], V=V, c2=0.01, loss_agg=agg)
     if dtype == "f32":
         g = _to_dev(synth.make_batch(31, B, T, V, "f32", "stress", "tiny"))
@@ -1005,20 +1003,20 @@ def test_next1_k7_cluster_pass(ctx, dtype, V, B, T, agg):
     tdt = torch.float32 if dtype == "f32" else torch.bfloat16
     src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
     out = {}
-    for key, fused in (("k7", True), ("k7b", True), ("two", False)):
+    for key, fused in (("fused", True), ("fused2", True), ("two", False)):
         dl = torch.full((B, T, V), 7.0, dtype=tdt, device=DEV)
         bufs = Buffers(B, T, DEV)
         status, st = run_iteration(ctx, g, cfg, bufs, src, mb=2, grad_sink=lambda s, e: dl[s:e], fused_grad=fused)
         torch.cuda.synchronize()
         assert status == "ORL_OK", status
         out[key] = (st, dl, bufs)
-    assert out["k7"][0] == out["k7b"][0] and torch.equal(out["k7"][1], out["k7b"][1])     # run to run
+    assert out["fused"][0] == out["fused2"][0] and torch.equal(out["fused"][1], out["fused2"][1])  # run to run
     m = parity.valid_mask(_np(g["lengths"]), T)
-    (st7, dl7, b7), (st2, dl2, b2) = out["k7"], out["two"]
+    (st7, dl7, b7), (st2, dl2, b2) = out["fused"], out["two"]
     npb = synth.batch_to_numpy({k: g[k] for k in ("logits_new", "tokens", "lengths")})
     ora = oracle.logprobs(npb["logits_new"], npb["tokens"], npb["lengths"])
     for k in ("logp_new", "entropy", "lse"):
-        parity.check_abs(f"k7 {k}", _np(getattr(b7, k)), ora[k.replace("_new", "")], m)
+        parity.check_abs(f"fused {k}", _np(getattr(b7, k)), ora[k.replace("_new", "")], m)
         np.testing.assert_allclose(_np(getattr(b7, k))[m], _np(getattr(b2, k))[m], rtol=0, atol=5e-5, err_msg=k)
     parity.check_rel("dlogp", _np(b7.dlogp), _np(b2.dlogp).astype(np.float64), m, rel=1e-5)
     assert np.array_equal(_np(b7.flags), _np(b2.flags))

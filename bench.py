@@ -43,7 +43,7 @@ import torch  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 UNIT = "tokens/s"
-SIDE_BYTES = {"old": 8, "ref": 8 + 12, "new": 8 + 24 + 16 + 1}   # side bytes per token and pass (DESIGN 5.1)
+SIDE_BYTES = {"old": 8, "ref": 8 + 12, "new": 8 + 28 + 16 + 1}   # side bytes per token and pass (DESIGN 5.1)
 LEGS_DEFAULT = "llama8b,longcot,target,llama8b:secondary,longcot:secondary"
 
 
@@ -672,7 +672,7 @@ def run_next1(args, ctx, W):
                                       v_new=batch["values_new"] if critic else None,
                                       v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
                                       lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
-                                      flags=bufs.flags, dlogits=dl[s:e], stream=stream)
+                                      flags=bufs.flags, adv_lo=bufs.adv_lo, dlogits=dl[s:e], stream=stream)
 
     def timed(fn):
         for _ in range(2):
@@ -796,7 +796,22 @@ def run_e2e(args, env, W, R_dev):
     B = W["B_rank"]
     logits = W["logits"]
     mb_bytes = 3 * mb * T * V * W["elt"]
-    H = W["pool"] if W["pool"] else max(1, min(W["n_mb"], int(48e9 // mb_bytes)))
+    # pinned host memory: at most ~56 GB per node (2 grpo buffers per model), split over its ranks
+    budget = 56e9 / (world if world > 1 else 1)
+    H = min(W["pool"], max(1, int(budget // mb_bytes))) if W["pool"] else max(1, min(W["n_mb"], int(budget // mb_bytes)))
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # pragma: no cover
+        avail = None
+    ok = avail is None or H * mb_bytes * world <= 0.6 * avail
+    if env["dist_mode"]:                      # every rank takes the same decision
+        t = torch.tensor([1.0 if ok else 0.0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = t.item() == 1.0
+    if not ok:
+        return {"skipped": f"needs {H * mb_bytes * world / 1e9:.0f} GB of pinned host memory "
+                           f"({(avail or 0) / 1e9:.0f} GB available on this node)"}
     # device view of slot h: pool slot h, or the resident micro-batch h
     dev_slot = {r: [logits[r][h * mb:h * mb + mb] for h in range(H)] for r in logits}
     host = {r: [torch.empty(x.shape, dtype=x.dtype, pin_memory=True).copy_(x) for x in dev_slot[r]] for r in logits}

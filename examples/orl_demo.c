@@ -76,7 +76,8 @@ int main(int argc, char **argv) {
     const float *v_old = load(dir, "values_old.bin", ntok * 4);
     const float *v_new = load(dir, "values_new.bin", ntok * 4);
     float *logp_old = zeros(ntok), *logp_ref = zeros(ntok), *kl = zeros(ntok), *shaped = zeros(ntok);
-    float *adv = zeros(ntok), *ret = zeros(ntok), *logp_new = zeros(ntok), *ent = zeros(ntok);
+    float *adv = zeros(ntok), *adv_lo = zeros(ntok), *ret = zeros(ntok), *logp_new = zeros(ntok);
+    float *ent = zeros(ntok);
 
     orl_ctx *ctx = NULL;
     if (orl_create(0, 1, 0, NULL, &ctx) != ORL_OK) {
@@ -97,8 +98,8 @@ int main(int argc, char **argv) {
                                    reward, kl, shaped, NULL));
         }
     }
-    CHECK(orl_advantages(ctx, B, T, lengths, ORL_ADV_GAE, 1.0, 0.95, 1, shaped, v_old, reward, adv, ret, NULL,
-                         NULL));                        /* S4 */
+    CHECK(orl_advantages(ctx, B, T, lengths, ORL_ADV_GAE, 1.0, 0.95, 1, shaped, v_old, reward, adv, adv_lo, ret,
+                         NULL, NULL));                  /* S4 */
     CHECK(orl_whiten_stats(ctx, 1, NULL));              /* S6 + C1 */
     orl_ppo_cfg cfg;
     memset(&cfg, 0, sizeof cfg);
@@ -110,8 +111,8 @@ int main(int argc, char **argv) {
     for (int64_t s = 0; s < B; s += mb) {               /* S1 + S7..S9 actor */
         orl_rows rows = {B - s < mb ? B - s : mb, T, s, tokens, lengths, NULL};
         orl_logits x = {(const char *)lg[2] + (size_t)(s * T * V) * 2, ORL_BF16, 0, V, T * V, V};
-        CHECK(orl_ppo_loss(ctx, &rows, &x, 1.0f, &cfg, logp_old, logp_ref, adv, ret, v_new, v_old, logp_new, ent,
-                           NULL, NULL, NULL, NULL, NULL));
+        CHECK(orl_ppo_loss(ctx, &rows, &x, 1.0f, &cfg, logp_old, logp_ref, adv, adv_lo, ret, v_new, v_old, logp_new,
+                           ent, NULL, NULL, NULL, NULL, NULL));
     }
     orl_stats st;
     const orl_status fin = orl_finalize(ctx, &cfg, &st, NULL, NULL);  /* S10 + C2 */

@@ -54,7 +54,8 @@
 extern "C" {
 #endif
 
-#define ORL_VERSION 2 /* 2: per-token decision flags in the actor passes, orl_set_pdl_chain */
+#define ORL_VERSION 2 /* 2: per-token decision flags in the actor passes, orl_set_pdl_chain,
+                         the optional low part of the advantages (adv_lo) */
 #define ORL_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
 #define ORL_STATS_N 16          /* length of the device stats vector */
 #define ORL_PARTIALS_N 24       /* length of a rank's loss/stat partial (hooks) */
@@ -290,13 +291,18 @@ orl_status orl_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_logits *lo
  *              tokens; ret unused; constant groups give exactly 0.
  * group_keep (optional, [B/group_size] uint8, GRPO and RPP_BASELINE) is the
  * DAPO dynamic-sampling flag max_g - min_g >= 1e-12.
+ * adv_lo (optional, [B, T] fp32) receives A - (float)A for every valid token, so
+ * adv + adv_lo carries the fp64 scan value to ~2^-48 relative; passed to the actor
+ * pass it makes the whitening (A - mu)/(sigma + 1e-8) exact to fp64 even when the
+ * advantages are nearly constant (|mu|/sigma up to ~1e9; Z33).  With adv_lo the
+ * whitening moments are taken from adv + adv_lo, else from adv.
  * gamma, lambda in [0,1].  The whitening partials (count, mean, M2 over valid
  * tokens, fp64) are staged in ctx for orl_whiten_stats.
  * ORL_E_GROUP_SPLIT if B is not a multiple of group_size (GRPO/RPP_BASELINE). */
 orl_status orl_advantages(orl_ctx *ctx, int64_t B, int64_t T, const int32_t *lengths,
                           int kind, double gamma, double lambda, int group_size,
                           const float *shaped_reward, const float *values,
-                          const float *seq_reward, float *adv, float *ret,
+                          const float *seq_reward, float *adv, float *adv_lo, float *ret,
                           uint8_t *group_keep, void *stream);
 
 /* ---- S6 + C1: global whitening moments -------------------------------- */
@@ -330,11 +336,12 @@ orl_status orl_whiten_stats(orl_ctx *ctx, int whiten, void *stream);
  *                   bit 3  a non-finite loss term                       (Z29)
  *                 masked positions 0 (S:216 clip_fraction per token)
  * with N the global token count from orl_whiten_stats.
- * logp_old, adv required; logp_ref optional; ret, v_new, v_old together or
+ * A = adv (+ adv_lo when given: the low part orl_advantages wrote, Z33).
+ * logp_old, adv required; logp_ref, adv_lo optional; ret, v_new, v_old together or
  * all NULL (no critic).  logp_new required; entropy, lse, dloss_*, flags optional. */
 orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
                         float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
-                        const float *logp_ref, const float *adv, const float *ret,
+                        const float *logp_ref, const float *adv, const float *adv_lo, const float *ret,
                         const float *v_new, const float *v_old, float *logp_new,
                         float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
                         uint8_t *flags, void *stream);
@@ -398,7 +405,8 @@ orl_status orl_stats_decode(const double *final_vec, double ratio_guard, orl_sta
  * passes when the logits or dlogits layout is not 16-byte aligned. */
 orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
                                  float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
-                                 const float *logp_ref, const float *adv, const float *ret,
+                                 const float *logp_ref, const float *adv, const float *adv_lo,
+                                 const float *ret,
                                  const float *v_new, const float *v_old, float *logp_new,
                                  float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
                                  uint8_t *flags, void *dlogits, int64_t out_stride_b,
@@ -441,7 +449,8 @@ orl_status orl_lmhead_logprobs(orl_ctx *ctx, const orl_rows *rows, const orl_lmh
 /* orl_ppo_loss with the actor logits computed from its LM head (as above). */
 orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *head,
                                float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
-                               const float *logp_ref, const float *adv, const float *ret,
+                               const float *logp_ref, const float *adv, const float *adv_lo,
+                               const float *ret,
                                const float *v_new, const float *v_old, float *logp_new,
                                float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
                                uint8_t *flags, void *stream);

@@ -77,15 +77,17 @@ __global__ void __launch_bounds__(kK3Threads) k3_kernel(const K3Params p) {
 
     if (grpo) {
         const float a = (float)sh_seq[0];
+        const float alo = p.adv_lo ? (float)(sh_seq[0] - (double)a) : 0.f;
         for (int t = tid; t < p.T; t += kK3Threads) {
             const float v = t < L ? a : 0.f;
             p.adv[row + t] = v;
+            if (p.adv_lo) p.adv_lo[row + t] = t < L ? alo : 0.f;
             if (p.ret) p.ret[row + t] = v;
         }
         if (tid == 0) {
             double *o = p.seq_part + 3 * (int64_t)b;
             o[0] = (double)L;
-            o[1] = L > 0 ? (double)a : 0.0;
+            o[1] = L > 0 ? (double)a + (double)alo : 0.0;
             o[2] = 0.0;
         }
         return;
@@ -129,17 +131,25 @@ __global__ void __launch_bounds__(kK3Threads) k3_kernel(const K3Params p) {
     }
     const double carry = (tid + 1 < kK3Threads) ? sh_b[tid + 1] : 0.0;  // A at t = end
 
-    // pass 2: write A, R; local sum of the stored fp32 advantages
+    // pass 2: write A (fp32, plus the fp32 residual when adv_lo is given), R; local sum
+    // of the stored advantages (the values the actor pass will whiten)
     double A = carry, lsum = 0.0;
     for (int t = end - 1; t >= beg; --t) {
         A = delta(t) + c * A;
         const float af = (float)A;
         p.adv[row + t] = af;
+        double As = (double)af;
+        if (p.adv_lo) {
+            const float lo = (float)(A - (double)af);
+            p.adv_lo[row + t] = lo;
+            As += (double)lo;
+        }
         if (p.ret) p.ret[row + t] = gae ? (float)(A + (double)p.values[row + t]) : af;
-        lsum += (double)af;
+        lsum += As;
     }
     for (int t = L + tid; t < p.T; t += kK3Threads) {
         p.adv[row + t] = 0.f;
+        if (p.adv_lo) p.adv_lo[row + t] = 0.f;
         if (p.ret) p.ret[row + t] = 0.f;
     }
     // whitening partial of this response: n, mean, M2 (two-pass, fp64)
@@ -147,7 +157,7 @@ __global__ void __launch_bounds__(kK3Threads) k3_kernel(const K3Params p) {
     const double mean = L > 0 ? S / (double)L : 0.0;
     double lss = 0.0;
     for (int t = beg; t < end; ++t) {
-        const double d = (double)p.adv[row + t] - mean;  // own writes
+        const double d = (double)p.adv[row + t] + (p.adv_lo ? (double)p.adv_lo[row + t] : 0.0) - mean;  // own writes
         lss += d * d;
     }
     const double M2 = block_sum(lss, sh_red);

@@ -448,7 +448,7 @@ extern "C" orl_status orl_lmhead_logprobs(orl_ctx *ctx, const orl_rows *rows, co
 extern "C" orl_status orl_advantages(orl_ctx *ctx, int64_t B, int64_t T, const int32_t *lengths,
                                      int kind, double gamma, double lambda, int group_size,
                                      const float *shaped_reward, const float *values,
-                                     const float *seq_reward, float *adv, float *ret,
+                                     const float *seq_reward, float *adv, float *adv_lo, float *ret,
                                      uint8_t *group_keep, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
     if (B < 1 || B > (1 << 24) || T < 1 || T > INT32_MAX || B * T >= ((int64_t)1 << 40))
@@ -468,7 +468,7 @@ extern "C" orl_status orl_advantages(orl_ctx *ctx, int64_t B, int64_t T, const i
     if (grouped && (group_size < 1 || B % group_size != 0))
         return fail(ctx, ORL_E_GROUP_SPLIT, "B=%lld is not a multiple of group_size=%d", (long long)B, group_size);
     if (!aligned4(lengths) || !aligned4(shaped_reward) || !aligned4(values) || !aligned4(seq_reward) ||
-        !aligned4(adv) || !aligned4(ret))
+        !aligned4(adv) || !aligned4(adv_lo) || !aligned4(ret))
         return fail(ctx, ORL_E_ALIGN, "per-token arrays must be 4-byte aligned");
     orl_status st = set_device(ctx);
     if (st) return st;
@@ -491,6 +491,7 @@ extern "C" orl_status orl_advantages(orl_ctx *ctx, int64_t B, int64_t T, const i
     p.values = values;
     p.seq_reward = seq_reward;
     p.adv = adv;
+    p.adv_lo = adv_lo;
     p.ret = ret;
     p.keep = grouped ? group_keep : nullptr;
     p.seq_part = ctx->d_seq_part;
@@ -549,8 +550,8 @@ struct GradOut {  // optional fused backward (orl_ppo_loss_and_grad)
 
 static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor, float inv_temp,
                                 const orl_ppo_cfg *cfg, const float *logp_old, const float *logp_ref,
-                                const float *adv, const float *ret, const float *v_new, const float *v_old,
-                                float *logp_new, float *entropy, float *lse, float *dloss_dlogp,
+                                const float *adv, const float *adv_lo, const float *ret, const float *v_new,
+                                const float *v_old, float *logp_new, float *entropy, float *lse, float *dloss_dlogp,
                                 float *dloss_dv, uint8_t *flags, const GradOut *grad, void *stream,
                                 const orl_lmhead *head = nullptr) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
@@ -562,7 +563,8 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     const int critic = (ret != nullptr) + (v_new != nullptr) + (v_old != nullptr);
     if (critic != 0 && critic != 3) return fail(ctx, ORL_E_INVALID_ARG, "ret, v_new, v_old go together");
     if (dloss_dv && critic == 0) return fail(ctx, ORL_E_INVALID_ARG, "dloss_dv needs the critic arrays");
-    if (!aligned4(logp_old) || !aligned4(logp_ref) || !aligned4(adv) || !aligned4(ret) || !aligned4(v_new) ||
+    if (!aligned4(logp_old) || !aligned4(logp_ref) || !aligned4(adv) || !aligned4(adv_lo) || !aligned4(ret) ||
+        !aligned4(v_new) ||
         !aligned4(v_old) || !aligned4(logp_new) || !aligned4(entropy) || !aligned4(dloss_dlogp) ||
         !aligned4(dloss_dv) || !aligned4(lse))
         return fail(ctx, ORL_E_ALIGN, "per-token arrays must be 4-byte aligned");
@@ -585,6 +587,7 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     p.logp_old = logp_old;
     p.logp_ref = logp_ref;
     p.adv = adv;
+    p.adv_lo = adv_lo;
     p.ret = ret;
     p.v_new = v_new;
     p.v_old = v_old;
@@ -620,6 +623,17 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     const bool out_same = lay == 2 && dgap % 16 == 0 && ((grad->stride_t - actor->stride_t) * elt) % 16 == 0 &&
                           ((grad->stride_b - actor->stride_b) * elt) % 16 == 0 &&
                           reinterpret_cast<uintptr_t>(grad->dlogits) % elt == 0;
+    if (tma && out_ok && k1_pair_eligible(p.row_bytes) && getenv("ORL_FUSED_PAIR")) {
+        p.unaligned = 0;
+        p.dlogits = grad->dlogits;
+        p.out_stride_b = grad->stride_b;
+        p.out_stride_t = grad->stride_t;
+        p.c2_ent = cfg->c2;
+        p.zero_masked_grad = grad->zero_masked;
+        CUDA_TRY(ctx, launch_k1_pair(p, ctx->num_sms, as_stream(stream)));
+        ctx->launches += 1;
+        return ORL_OK;
+    }
     if ((tma && out_ok) || out_same) {
         p.unaligned = out_same ? 1 : 0;
         p.dlogits = grad->dlogits;
@@ -639,30 +653,31 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
 
 extern "C" orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
                                    float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
-                                   const float *logp_ref, const float *adv, const float *ret,
-                                   const float *v_new, const float *v_old, float *logp_new,
+                                   const float *logp_ref, const float *adv, const float *adv_lo,
+                                   const float *ret, const float *v_new, const float *v_old, float *logp_new,
                                    float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
                                    uint8_t *flags, void *stream) {
-    return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
+    return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, adv_lo, ret, v_new, v_old,
                          logp_new, entropy, lse, dloss_dlogp, dloss_dv, flags, nullptr, stream);
 }
 
 extern "C" orl_status orl_lmhead_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_lmhead *head,
                                           float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
-                                          const float *logp_ref, const float *adv, const float *ret,
-                                          const float *v_new, const float *v_old, float *logp_new,
-                                          float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
-                                          uint8_t *flags, void *stream) {
+                                          const float *logp_ref, const float *adv, const float *adv_lo,
+                                          const float *ret, const float *v_new, const float *v_old,
+                                          float *logp_new, float *entropy, float *lse, float *dloss_dlogp,
+                                          float *dloss_dv, uint8_t *flags, void *stream) {
     if (!ctx) return fail(nullptr, ORL_E_INVALID_ARG, "ctx is NULL");
     if (!head) return fail(ctx, ORL_E_INVALID_ARG, "lmhead is NULL");
-    return ppo_loss_impl(ctx, rows, nullptr, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
+    return ppo_loss_impl(ctx, rows, nullptr, inv_temp, cfg, logp_old, logp_ref, adv, adv_lo, ret, v_new, v_old,
                          logp_new, entropy, lse, dloss_dlogp, dloss_dv, flags, nullptr, stream, head);
 }
 
 extern "C" orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
                                             float inv_temp, const orl_ppo_cfg *cfg, const float *logp_old,
-                                            const float *logp_ref, const float *adv, const float *ret,
-                                            const float *v_new, const float *v_old, float *logp_new,
+                                            const float *logp_ref, const float *adv, const float *adv_lo,
+                                            const float *ret, const float *v_new, const float *v_old,
+                                            float *logp_new,
                                             float *entropy, float *lse, float *dloss_dlogp, float *dloss_dv,
                                             uint8_t *flags, void *dlogits, int64_t out_stride_b,
                                             int64_t out_stride_t, int zero_masked, void *stream) {
@@ -673,7 +688,7 @@ extern "C" orl_status orl_ppo_loss_and_grad(orl_ctx *ctx, const orl_rows *rows, 
         return fail(ctx, ORL_E_SHAPE, "dlogits strides (%lld, %lld) invalid", (long long)out_stride_b,
                     (long long)out_stride_t);
     const GradOut g{dlogits, out_stride_b, out_stride_t, zero_masked ? 1 : 0};
-    return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, ret, v_new, v_old,
+    return ppo_loss_impl(ctx, rows, actor, inv_temp, cfg, logp_old, logp_ref, adv, adv_lo, ret, v_new, v_old,
                          logp_new, entropy, lse, dloss_dlogp, dloss_dv, flags, &g, stream);
 }
 

@@ -48,6 +48,7 @@ struct K1Params {
     float *kl_out, *shaped;
     // S7-S9 loss epilogue (actor pass)
     const float *logp_old, *logp_ref, *adv, *ret, *v_new, *v_old;
+    const float *adv_lo;  // optional low part: A = adv + adv_lo (~48-bit advantages, orl_advantages)
     float *dlogp, *dv;
     uint8_t *flags;     // optional per-token decisions: bit 0 clipped (Z16), 1 value-clipped,
                         // 2 ratio guard (Z22), 3 non-finite loss term; masked positions 0
@@ -79,6 +80,10 @@ struct K1Params {
 // Launch K1.  Returns the CUDA launch error.  `tma` selects the TMA bulk-copy
 // kernel (requires 16-byte aligned rows and row_bytes % 16 == 0).
 cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaStream_t s);
+// The fused actor pass over CTA pairs (each row split in halves between the two CTAs of
+// a cluster; kModeLossGrad semantics): rows 16-byte aligned, >= 256 bytes.
+bool k1_pair_eligible(int64_t row_bytes);
+cudaError_t launch_k1_pair(const K1Params &p, int num_sms, cudaStream_t s);
 // Micro-batches with more sequences than this keep the length prefix in global
 // memory (written by launch_lengths_prefix) instead of shared memory.
 constexpr int kSmemPrefixMax = 1024;
@@ -139,8 +144,9 @@ struct K3Params {
     const int32_t *lengths;
     const float *shaped, *values, *seq_reward;
     float *adv, *ret;
+    float *adv_lo;     // optional: A - (float)A, so adv + adv_lo carries the fp64 scan value
     uint8_t *keep;
-    double *seq_part;  // [B][3]: n_b, mean_b, M2_b of the stored fp32 advantages
+    double *seq_part;  // [B][3]: n_b, mean_b, M2_b of the stored advantages (adv + adv_lo)
     unsigned long long *err;
 };
 cudaError_t launch_k3(const K3Params &p, cudaStream_t s);

@@ -86,19 +86,19 @@ _lib.orl_launch_count.restype = ctypes.c_uint64
 _lib.orl_begin_iteration.argtypes = [_P, _P]
 _lib.orl_logprobs.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32, _P, _P, _P, _P,
                               _P, _I32, _F64, _P, _P, _P, _P]
-_lib.orl_advantages.argtypes = [_P, _I64, _I64, _P, _I32, _F64, _F64, _I32, _P, _P, _P, _P, _P, _P, _P]
+_lib.orl_advantages.argtypes = [_P, _I64, _I64, _P, _I32, _F64, _F64, _I32, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.orl_whiten_stats.argtypes = [_P, _I32, _P]
 _lib.orl_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
-                              ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+                              ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.orl_ppo_loss_and_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32,
                                        ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                                       _P, _I64, _I64, _I32, _P]
+                                       _P, _P, _I64, _I64, _I32, _P]
 _lib.orl_logits_grad.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(Logits), _F32, ctypes.POINTER(PpoCfg),
                                  _P, _P, _P, _P, _I64, _I64, _I32, _P]
 _lib.orl_lmhead_logprobs.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(LmHead), _F32, _P, _P, _P, _P,
                                      _P, _I32, _F64, _P, _P, _P, _P]
 _lib.orl_lmhead_ppo_loss.argtypes = [_P, ctypes.POINTER(Rows), ctypes.POINTER(LmHead), _F32,
-                                     ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
+                                     ctypes.POINTER(PpoCfg), _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]
 _lib.orl_set_pdl_chain.argtypes = [_P, _I32]
 _lib.orl_get_pdl_chain.argtypes = [_P]
 _lib.orl_get_pdl_chain.restype = ctypes.c_int
@@ -468,27 +468,27 @@ def orl_lmhead_logprobs(ctx: Context, tokens, lengths, hidden, weight, logp, *, 
 
 
 def _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
-                 dloss_dv, flags):
+                 dloss_dv, flags, adv_lo=None):
     for name, t in (("logp_old", logp_old), ("adv", adv), ("logp_new", logp_new)):
         _arr(ctx, name, t, torch.float32, Bt * T, optional=False)
     _tokarr(ctx, Bt, T, logp_ref=logp_ref, ret=ret, v_new=v_new, v_old=v_old, entropy=entropy, lse=lse,
-            dloss_dlogp=dloss_dlogp, dloss_dv=dloss_dv)
+            dloss_dlogp=dloss_dlogp, dloss_dv=dloss_dv, adv_lo=adv_lo)
     _flags(ctx, flags, Bt, T)
 
 
 def orl_lmhead_ppo_loss(ctx: Context, tokens, lengths, hidden, weight, cfg, logp_old, adv, logp_new, *,
                         B=None, seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
                         entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, flags=None, stream=None,
-                        cu_seqlens=None):
+                        cu_seqlens=None, adv_lo=None):
     """NEXT-4: orl_ppo_loss with the actor logits computed from its LM head."""
     if B is None:
         B = tokens.shape[0] - seq_offset
     Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
     _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
-                 dloss_dv, flags)
+                 dloss_dv, flags, adv_lo)
     rows, hd, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), _head(ctx, hidden, weight), cfg.c()
     st = _lib.orl_lmhead_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(hd), float(inv_temp), ctypes.byref(c),
-                                  _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
+                                  _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(adv_lo), _ptr(ret), _ptr(v_new),
                                   _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
                                   _ptr(dloss_dv), _ptr(flags), _stream(stream))
     return ctx.check(st)
@@ -496,18 +496,20 @@ def orl_lmhead_ppo_loss(ctx: Context, tokens, lengths, hidden, weight, cfg, logp
 
 def orl_advantages(ctx: Context, lengths, adv, *, kind="gae", gamma=1.0, lam=0.95, group_size=1,
                    shaped_reward=None, values=None, seq_reward=None, ret=None, group_keep=None,
-                   stream=None):
+                   adv_lo=None, stream=None):
+    """S4/S4'/S5; `adv_lo` (optional fp32 [B, T]) receives A - (float)A (pass it to the
+    actor pass: fp64-exact whitening of nearly constant advantages, Z33)."""
     _arr(ctx, "adv", adv, torch.float32, 0, optional=False)
     if adv.dim() != 2:
         raise ValueError("adv must be [B, T]")
     B, T = adv.shape
     _arr(ctx, "lengths", lengths, torch.int32, B, optional=False)
-    _tokarr(ctx, B, T, shaped_reward=shaped_reward, values=values, ret=ret)
+    _tokarr(ctx, B, T, shaped_reward=shaped_reward, values=values, ret=ret, adv_lo=adv_lo)
     _arr(ctx, "seq_reward", seq_reward, torch.float32, B)
     _arr(ctx, "group_keep", group_keep, torch.uint8, B // max(1, int(group_size)))
     st = _lib.orl_advantages(ctx.h, B, T, _ptr(lengths), ADV.get(kind, kind), float(gamma), float(lam),
                              int(group_size), _ptr(shaped_reward), _ptr(values), _ptr(seq_reward),
-                             _ptr(adv), _ptr(ret), _ptr(group_keep), _stream(stream))
+                             _ptr(adv), _ptr(adv_lo), _ptr(ret), _ptr(group_keep), _stream(stream))
     return ctx.check(st)
 
 
@@ -518,17 +520,18 @@ def orl_whiten_stats(ctx: Context, whiten: bool, stream=None):
 def orl_ppo_loss(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
                  seq_offset=0, inv_temp=1.0, logp_ref=None, ret=None, v_new=None, v_old=None,
                  entropy=None, lse=None, dloss_dlogp=None, dloss_dv=None, flags=None, stream=None,
-                 cu_seqlens=None, n_seq=None):
+                 cu_seqlens=None, n_seq=None, adv_lo=None):
     """S1 + S7..S9 on the actor logits; `flags` (optional uint8 [B_total, T]) receives the
-    per-token decisions (bit 0 clipped, 1 value-clipped, 2 ratio guard, 3 non-finite)."""
+    per-token decisions (bit 0 clipped, 1 value-clipped, 2 ratio guard, 3 non-finite);
+    `adv_lo` (optional) is orl_advantages' low part (A = adv + adv_lo)."""
     B = _nseq(logits, cu_seqlens, n_seq)
     Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
     _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
-                 dloss_dv, flags)
+                 dloss_dv, flags, adv_lo)
     rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
     lg = _lg(ctx, logits, B, cu_seqlens)
     st = _lib.orl_ppo_loss(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
-                           _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
+                           _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(adv_lo), _ptr(ret), _ptr(v_new),
                            _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
                            _ptr(dloss_dv), _ptr(flags), _stream(stream))
     return ctx.check(st)
@@ -545,20 +548,20 @@ def _dlogits(ctx, dlogits, logits):
 def orl_ppo_loss_and_grad(ctx: Context, tokens, lengths, logits, cfg: PPOConfig, logp_old, adv, logp_new, *,
                           entropy, lse, dloss_dlogp, dlogits, seq_offset=0, inv_temp=1.0, logp_ref=None,
                           ret=None, v_new=None, v_old=None, dloss_dv=None, flags=None, zero_masked=True,
-                          stream=None, cu_seqlens=None, n_seq=None):
+                          stream=None, cu_seqlens=None, n_seq=None, adv_lo=None):
     """S1 + S7..S9 + NEXT-1 in one pass over the actor logits (the row is re-read from L2)."""
     B = _nseq(logits, cu_seqlens, n_seq)
     Bt, T = _tok(ctx, tokens, lengths, B, seq_offset, cu_seqlens)
     for name, t in (("entropy", entropy), ("lse", lse), ("dloss_dlogp", dloss_dlogp)):
         _arr(ctx, name, t, torch.float32, Bt * T, optional=False)
     _loss_arrays(ctx, Bt, T, logp_old, adv, logp_new, logp_ref, ret, v_new, v_old, entropy, lse, dloss_dlogp,
-                 dloss_dv, flags)
+                 dloss_dv, flags, adv_lo)
     _dlogits(ctx, dlogits, logits)
     rows, c = _rows(tokens, lengths, B, T, seq_offset, cu_seqlens), cfg.c()
     lg = _lg(ctx, logits, B, cu_seqlens)
     sb = 0 if cu_seqlens is not None else dlogits.stride(0)
     st = _lib.orl_ppo_loss_and_grad(ctx.h, ctypes.byref(rows), ctypes.byref(lg), float(inv_temp), ctypes.byref(c),
-                                    _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(ret), _ptr(v_new),
+                                    _ptr(logp_old), _ptr(logp_ref), _ptr(adv), _ptr(adv_lo), _ptr(ret), _ptr(v_new),
                                     _ptr(v_old), _ptr(logp_new), _ptr(entropy), _ptr(lse), _ptr(dloss_dlogp),
                                     _ptr(dloss_dv), _ptr(flags), _ptr(dlogits), sb, dlogits.stride(-2),
                                     int(bool(zero_masked)), _stream(stream))

@@ -53,6 +53,7 @@ class Buffers:
         f = lambda: torch.zeros(B, T, dtype=torch.float32, device=device)  # noqa: E731
         self.logp_old, self.logp_ref, self.kl, self.shaped = f(), f(), f(), f()
         self.adv, self.ret, self.logp_new, self.entropy = f(), f(), f(), f()
+        self.adv_lo = f()  # A - (float)A: the actor pass whitens adv + adv_lo (fp64-exact, Z33)
         self.lse = f()
         self.dlogp = f() if grads else None
         self.dv = f() if grads else None
@@ -138,7 +139,7 @@ def _run_iteration(ctx, batch, cfg, bufs, logits, mb, stream, finalize, on_k1, g
                             values=batch.get("values_old") if cfg.critic else None,
                             seq_reward=batch["seq_reward"], ret=bufs.ret,
                             group_keep=bufs.keep if cfg.adv_kind in ("grpo", "rpp_baseline") else None,
-                            stream=stream)
+                            adv_lo=bufs.adv_lo, stream=stream)
         _orl.orl_whiten_stats(ctx, cfg.whiten and cfg.adv_kind != "grpo", stream)     # S6 + C1
     critic = cfg.critic and batch.get("values_new") is not None
     if grad_sink is not None and fused_grad:           # S1 + S7..S9 + NEXT-1 in one pass
@@ -167,7 +168,7 @@ def _actor_fused(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, to
                                    v_new=batch["values_new"] if critic else None,
                                    v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
                                    lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None,
-                                   flags=bufs.flags, dlogits=grad_sink(s, e), stream=stream)
+                                   flags=bufs.flags, adv_lo=bufs.adv_lo, dlogits=grad_sink(s, e), stream=stream)
         if h: h()
 
 
@@ -179,7 +180,7 @@ def _actor(ctx, cfg, batch, bufs, logits, mbs, hook, grad_sink, critic, tok, L, 
                   ret=bufs.ret if critic else None, v_new=batch["values_new"] if critic else None,
                   v_old=batch["values_old"] if critic else None, entropy=bufs.entropy,
                   lse=bufs.lse, dloss_dlogp=bufs.dlogp, dloss_dv=bufs.dv if critic else None, flags=bufs.flags,
-                  stream=stream)
+                  adv_lo=bufs.adv_lo, stream=stream)
         if isinstance(src, LmHeadRows):
             if grad_sink is not None:
                 _no_lmhead(src)

@@ -72,7 +72,7 @@ def _check_flags(bufs, sh, ocfg, mask, name):
     edge (fp64 exp may differ by an ulp), |A'| < 1e-12, |dold| within 1e-9 of the guard."""
     L = sh["lengths"]
     f64 = lambda t: _np(t).astype(np.float64)  # noqa: E731
-    adv = f64(bufs.adv)
+    adv = f64(bufs.adv) + f64(bufs.adv_lo)            # the value the actor pass whitens (Z33)
     kind = ocfg["adv_kind"]
     whiten = bool(ocfg["whiten"]) and kind != "grpo"
     Aw = adv
@@ -553,7 +553,7 @@ def test_shard_emulation_matches_single_rank(kind, n):
         orl.orl_advantages(cx, gs["lengths"], bb.adv, kind=kind, gamma=cfg.gamma, lam=cfg.lam,
                            group_size=cfg.group_size, shaped_reward=bb.shaped,
                            values=gs["values_old"] if cfg.critic else None, seq_reward=gs["seq_reward"],
-                           ret=bb.ret)
+                           ret=bb.ret, adv_lo=bb.adv_lo)
         shard_bufs.append((gs, bb, src))
     wparts = np.stack([orl.orl_export_partials(cx, 0) for cx in ctxs])
     for cx in ctxs:
@@ -566,7 +566,7 @@ def test_shard_emulation_matches_single_rank(kind, n):
             orl.orl_ppo_loss(cx, gs["tokens"], gs["lengths"], src("new", a, z), cfg.ppo, bb.logp_old, bb.adv,
                              bb.logp_new, seq_offset=a, logp_ref=bb.logp_ref, ret=bb.ret if crit else None,
                              v_new=gs["values_new"] if crit else None, v_old=gs["values_old"] if crit else None,
-                             entropy=bb.entropy, dloss_dlogp=bb.dlogp)
+                             entropy=bb.entropy, dloss_dlogp=bb.dlogp, adv_lo=bb.adv_lo)
     sparts = np.stack([orl.orl_export_partials(cx, 1) for cx in ctxs])
     res = []
     for cx in ctxs:
@@ -895,13 +895,13 @@ def test_next2_packed_varlen_matches_padded(ctx):
                          n_seq=e - s, partner_logp=bk.logp_old, kl_est=cfg.kl_est_reward, beta_reward=cfg.beta_reward,
                          seq_reward=g["seq_reward"], kl=bk.kl, shaped_reward=bk.shaped)
     orl.orl_advantages(ctx, g["lengths"], bk.adv, kind="gae", gamma=cfg.gamma, lam=cfg.lam, shaped_reward=bk.shaped,
-                       values=g["values_old"], seq_reward=g["seq_reward"], ret=bk.ret)
+                       values=g["values_old"], seq_reward=g["seq_reward"], ret=bk.ret, adv_lo=bk.adv_lo)
     orl.orl_whiten_stats(ctx, True)
     for s, e in mbs:
         orl.orl_ppo_loss(ctx, tok, g["lengths"], view("new", s), cfg.ppo, bk.logp_old, bk.adv, bk.logp_new,
                          seq_offset=s, cu_seqlens=cu, n_seq=e - s, logp_ref=bk.logp_ref, ret=bk.ret,
                          v_new=g["values_new"], v_old=g["values_old"], entropy=bk.entropy, lse=bk.lse,
-                         dloss_dlogp=bk.dlogp, dloss_dv=bk.dv)
+                         dloss_dlogp=bk.dlogp, dloss_dv=bk.dv, adv_lo=bk.adv_lo)
     for s, e in mbs:
         orl.orl_logits_grad(ctx, tok, g["lengths"], view("new", s), cfg.ppo, bk.lse, bk.entropy, bk.dlogp,
                             dl_pk[int(cu[s]):], seq_offset=s, cu_seqlens=cu, n_seq=e - s)
@@ -1039,6 +1039,53 @@ def test_next1_fused_pass_spikes_and_bound(ctx, dtype, V, B, T, agg):
             bound = _grad_bound(x, y, lse, H, w[b, t], a, 1.0, o, dtype == "bf16")
             err = np.abs(gg[b, t] - o)
             assert np.all(err <= bound), (b, t, float((err / bound).max()))
+
+
+@pytest.mark.parametrize("kind", ["rpp", "gae"])
+def test_whitening_near_constant_advantages(ctx, kind):
+    """Z33: global whitening of nearly constant advantages (|mu|/sigma ~ 1e7: gamma = 1, one
+    reward per sequence, tiny KL shaping) is exact to fp64 because the actor pass whitens
+    adv + adv_lo (orl_advantages' low part). Stage-isolated: the oracle's S4 is fed the GPU's
+    own fp32 shaped rewards (at this conditioning the fp32 rounding of r' itself is of the
+    order of sigma), then whitening and the loss stage; A + A_lo, A', dL/dlogp and the
+    statistics at the 1e-5 bar, decisions bit-exact."""
+    B, T, V = 3, 64, 512
+    c = dict(synth.CONFIGS["llama8b"], V=V, adv_kind=kind, gamma=1.0, lam=1.0, beta_reward=1e-7, eps_v=0.2)
+    g = _gpu_batch(41, B, T, V, "full")
+    g["seq_reward"] = torch.full((B,), 5.0, device=DEV)
+    if kind == "gae":
+        g["values_old"] = torch.zeros(B, T, device=DEV)
+    cfg = PathConfig.from_synth(c)
+    status, st, bufs = _run(ctx, g, cfg, mb=2)
+    assert status == "ORL_OK"
+    L = _np(g["lengths"])
+    m = parity.valid_mask(L, T)
+    f64 = lambda t: _np(t).astype(np.float64)  # noqa: E731
+    r = f64(bufs.shaped)                                   # the GPU's S3 output
+    if kind == "gae":
+        A, R = oracle.gae(L, r, f64(g["values_old"]), 1.0, 1.0)
+    else:
+        A = R = oracle.discounted_returns(L, r, 1.0)
+    A_gpu = f64(bufs.adv) + f64(bufs.adv_lo)
+    np.testing.assert_allclose(A_gpu[m], A[m], rtol=1e-13, atol=0)   # ~48-bit advantages
+    mu, sd, warn = oracle.whiten_moments(A[m])
+    assert not warn and abs(mu) / sd > 1e6, (mu, sd)
+    assert abs(st["adv_mean"] - mu) <= 1e-12 * abs(mu) and abs(st["adv_std"] - sd) <= 1e-5 * sd
+    Aw = oracle.whiten(A, L, mu, sd)
+    crit = kind == "gae"
+    res = oracle.ppo_loss(L, f64(bufs.logp_new), f64(bufs.logp_old), Aw, logp_ref=f64(bufs.logp_ref),
+                          ret=R if crit else None, v_new=f64(g["values_new"]) if crit else None,
+                          v_old=f64(g["values_old"]) if crit else None, entropy=f64(bufs.entropy),
+                          eps_low=c["eps_low"], eps_high=c["eps_high"], eps_v=c["eps_v"], c1=c["c1"] if crit else 0.0)
+    parity.check_rel("dloss_dlogp", _np(bufs.dlogp), res["dlogp"], m)
+    rho = np.exp(f64(bufs.logp_new) - f64(bufs.logp_old))
+    tie = (np.abs(rho - 0.8) < 1e-9) | (np.abs(rho - 1.2) < 1e-9)
+    assert np.array_equal((_np(bufs.flags) & 1)[m & ~tie], (res["flags"] & 1)[m & ~tie])
+    ost = oracle.stats(res["sums"], c1=c["c1"] if crit else 0.0)
+    fl = float(np.mean(np.abs(res["obj"][m])))
+    assert abs(st["policy_loss"] - ost["policy_loss"]) <= parity.REL * max(abs(ost["policy_loss"]), fl)
+    # without the low part the fp32 advantages could not carry sigma / |mu| ~ 1e-7
+    assert np.any(_np(bufs.adv_lo)[m] != 0)
 
 
 def test_lengths_from_attention_mask(ctx):

@@ -86,13 +86,8 @@ def test_random_shapes_end_to_end(i):
     ocfg = dict(c, kl_mode=c.get("kl_mode", "reward"))
     ocfg["inv_temp"] = cs["inv_temp"]
     out_i, glob_i = _isolated_oracle(npb, bufs, ocfg)
-    mu, sd = glob_i.get("adv_mean", 0.0), glob_i.get("adv_std", 0.0)
-    if c["whiten"] and kind != "grpo" and sd > 0 and abs(mu) / sd > 1e4:
-        # whitening of (near-)constant advantages is ill-conditioned (fp64 one-pass
-        # and two-pass moments agree only while |mu|/sigma < ~1e4; the fp32 advantage outputs,
-        # Z25, cannot carry sigma/|mu| < 6e-8): only the count is comparable here
-        assert st["n_tokens"] == glob_i["stats"]["n_tokens"]
-        return
+    # near-constant advantages (|mu|/sigma > 1e4) are compared like the rest: the actor pass
+    # whitens adv + adv_lo, the fp64 scan value (Z33)
     raw = None
     if kind == "rpp_baseline":
         raw = oracle.shape_rewards(npb["lengths"], _np(bufs.logp_old), _np(bufs.logp_ref), c["kl_est_reward"],

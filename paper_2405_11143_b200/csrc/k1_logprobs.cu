@@ -282,15 +282,14 @@ struct EpiOut {
 };
 
 // publish(eo) runs as soon as (lse, H, w) are known, before the rest of the loss
-// terms: the fused backward waits for exactly these.  emit = false (the second CTA
-// of a pair, k1_pair_kernel): no stores, counters or partial sums.
+// terms: the fused backward waits for exactly these.
 struct NoPublish {
     __device__ void operator()(const EpiOut &) const {}
 };
 template <int MODE, typename Publish = NoPublish>
 __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Online tot,
                              float target, const float *side, const double *wh, double *wacc,
-                             EpiOut *eo = nullptr, const Publish &publish = Publish(), bool emit = true) {
+                             EpiOut *eo = nullptr, const Publish &publish = Publish()) {
     const int64_t i = (p.seq_offset + b) * (int64_t)p.T + t;
     const bool oob = (y < 0) || (y >= p.V);
     const double log2s = log2((double)tot.s);
@@ -299,19 +298,17 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
     double logp = (double)target * (double)p.inv_temp - lse;
     const bool dead = tot.m / p.c2 < 0.5f * kNegClampF32;  // every logit -inf
     if (oob) {
-        if (emit) atomicAdd(&p.err[0], 1ull);
+        atomicAdd(&p.err[0], 1ull);
         lse = H = logp = __longlong_as_double(0x7ff8000000000000ll);
     } else if (dead || !(isfinite(lse) && isfinite(logp) && isfinite(H))) {
-        if (emit) atomicAdd(&p.err[1], 1ull);
+        atomicAdd(&p.err[1], 1ull);
         if (dead) lse = H = logp = __longlong_as_double(0x7ff8000000000000ll);
     }
     const float logp_f = (float)logp, H_f = (float)H;
-    if (emit) {
-        p.logp[i] = logp_f;
-        if (p.entropy) p.entropy[i] = H_f;
-        if (p.lse) p.lse[i] = (float)lse;
-        if (p.gathered) p.gathered[i] = oob ? __int_as_float(0x7fc00000) : target;
-    }
+    p.logp[i] = logp_f;
+    if (p.entropy) p.entropy[i] = H_f;
+    if (p.lse) p.lse[i] = (float)lse;
+    if (p.gathered) p.gathered[i] = oob ? __int_as_float(0x7fc00000) : target;
 
     if (MODE == kModeLogprob) {
         if (p.partner) {
@@ -352,7 +349,6 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
             eo->w = wf;
             publish(*eo);
         }
-        if (!emit) return;  // the second CTA of a pair only needs (lse, H, w)
         double vl = 0.0, dvl = 0.0;
         bool vclipped = false;
         if (p.v_new) {
@@ -1278,442 +1274,6 @@ cudaError_t launch_k6_merge(const K1Params &p, int mode, int num_sms, cudaStream
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-// ---------------------------------------------------------------- fused actor pass over CTA pairs
-// kModeLossGrad with each row split between the two CTAs of a cluster (one TPC):
-// CTA q streams half q of every row of its pair, exactly like the one-CTA fused mode
-// (forward chunks released at once, the backward re-reads the half-row from L2), and
-// the pair exchanges its half-row online states through distributed shared memory
-// (st.async into the partner's slot, mbarrier complete_tx) before both run the same
-// fp64 row epilogue (CTA 0 emits the row).  A half-row per SM halves the L2 reuse
-// distance of the backward's re-read (~28 MB chip-wide instead of ~47 MB at
-// V = 128256), which is what the one-CTA mode loses to DRAM re-reads (DESIGN 5.5b).
-#ifndef ORL_PAIR_SPLIT
-#define ORL_PAIR_SPLIT 2
-#endif
-namespace pair {
-constexpr int kSplit = ORL_PAIR_SPLIT;      // forward chunks of row i before the backward of row i-1
-constexpr int kStates = kConsumers / 4;     // consumer states per row after a 2-round shuffle pre-merge
-constexpr int kSlots = kEpiWarps * 2;       // row slot rl % kSlots, drained by epilogue warp rl % kEpiWarps
-constexpr int kPeer = 4;
-constexpr int kRowInfo = 16;
-}  // namespace pair
-
-struct PairRowSlot {
-    float m[pair::kStates], s[pair::kStates], u[pair::kStates];
-    float target;
-    float pad[31];
-};
-struct __align__(128) PairSmem {
-    uint8_t stage[kStages][kChunk];
-    uint64_t full[kStages];
-    uint64_t empty[kStages];
-    uint64_t row_full[pair::kSlots];
-    uint64_t row_empty[pair::kSlots];
-    uint64_t grad_full[kGradRows];
-    uint64_t peer_full[pair::kPeer];   // the partner's half-row state of row rl arrived (16 tx bytes)
-    uint64_t peer_empty[pair::kPeer];  // the partner consumed what this CTA wrote into its slot
-    float4 peer_state[pair::kPeer];    // (m, s, u, target) written by the partner
-    int32_t row_y[pair::kRowInfo];
-    GradRow grad[kGradRows];
-    PairRowSlot slot[pair::kSlots];
-    double wacc[kEpiWarps][kNumPartials];
-};
-static_assert(kGradRows % kEpiWarps == 0 && pair::kPeer % kEpiWarps == 0, "rings must map to fixed epilogue warps");
-
-size_t k1_pair_smem_bytes(int B) {
-    return sizeof(PairSmem) + sizeof(int32_t) * (size_t)((B > kSmemPrefixMax ? 0 : B) + 32);
-}
-
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t map_peer(const void *local, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
-}
-// 16 bytes into the partner's shared memory; completes 16 tx bytes on the partner's mbarrier
-__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                     raddr),
-                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t rbar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-template <typename Tin>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k1_pair_kernel(const K1Params p) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    PairSmem &S = *reinterpret_cast<PairSmem *>(smem_raw);
-    int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw + sizeof(PairSmem));
-    int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t q = cluster_ctarank();                       // half of every row this CTA owns
-    const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;  // pair (row-stream) index and count
-
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&S.full[s], 1);
-            mbar_init(&S.empty[s], kConsumerWarps);
-        }
-        for (int s = 0; s < pair::kSlots; ++s) {
-            mbar_init(&S.row_full[s], kConsumerWarps);
-            mbar_init(&S.row_empty[s], 1);
-        }
-        for (int s = 0; s < kGradRows; ++s) mbar_init(&S.grad_full[s], 1);
-        for (int s = 0; s < pair::kPeer; ++s) {
-            mbar_init(&S.peer_full[s], 1);
-            mbar_init(&S.peer_empty[s], 1);
-        }
-        fence_mbar_init();
-    }
-    if (tid < kEpiWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int32_t *cum = p.cum_global ? p.cum_global : cum_s;
-    if (!p.pdl_chain || p.cum_global) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (p.cum_global) __syncthreads();
-    else build_prefix(p, cum_s, warp_tot);
-    cluster_sync_all();  // the partner's barriers are initialised before any remote access
-    const int64_t N = cum[p.B - 1];
-    const int64_t row_bytes = p.row_bytes;
-    const int64_t half = ((row_bytes / 2) + 15) & ~(int64_t)15;  // 16-byte aligned split
-    const int64_t my_off = q ? half : 0;
-    const int64_t my_len = q ? row_bytes - half : half;           // > 0 (host: row_bytes >= 256)
-    const int64_t nch = (my_len + kChunk - 1) / kChunk;
-    const int64_t ksplit = min((int64_t)pair::kSplit, nch);
-    const int64_t n_rows = N > cid ? (N - cid + ncl - 1) / ncl : 0;
-
-    if (warp == kProducerWarp) {
-        // ===================== producer: F(i)[0, k), B(i-1), F(i)[k, n) of this CTA's halves
-        if (lane == 0) {
-            const uint64_t pol_fwd = l2_evict_last_policy();   // kept for the backward's re-read
-            const uint64_t pol_bwd = l2_evict_first_policy();  // not needed after it
-            int stage = 0;
-            uint32_t phase = 0;
-            auto issue = [&](const char *src, int64_t c0, int64_t c1, uint64_t pol, int64_t publish_rl, int y) {
-                for (int64_t c = c0; c < c1; ++c) {
-                    const int64_t off = c * kChunk;
-                    const uint32_t bytes = (uint32_t)min((int64_t)kChunk, my_len - off);
-                    mbar_wait(&S.empty[stage], phase ^ 1u);
-                    if (c == 0 && publish_rl >= 0) S.row_y[publish_rl % pair::kRowInfo] = y;  // released below
-                    mbar_arrive_expect_tx(&S.full[stage], bytes);
-                    tma_load_1d(S.stage[stage], src + off, bytes, &S.full[stage], pol);
-                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
-                }
-            };
-            const char *prev_src = nullptr;
-            for (int64_t rl = 0; rl <= n_rows; ++rl) {
-                const char *src = nullptr;
-                if (rl < n_rows) {
-                    int b, t;
-                    locate_row(cum, p.B, cid + rl * ncl, b, t);
-                    const int y = __ldg(p.tokens + (p.seq_offset + b) * (int64_t)p.T + t);
-                    src = p.base + logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.stride_b, p.stride_t) * p.elt +
-                          my_off;
-                    issue(src, 0, ksplit, pol_fwd, rl, y);
-                }
-                if (rl > 0) issue(prev_src, 0, nch, pol_bwd, -1, 0);
-                if (rl < n_rows) issue(src, ksplit, nch, pol_fwd, -1, 0);
-                prev_src = src;
-            }
-        }
-    } else if (warp >= kEpilogueWarp) {
-        // ===================== epilogue: merge, pair exchange, fp64 row epilogue, grad constants
-        const int ew = warp - kEpilogueWarp;
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (q == 0) zero_masked(p, cum, lane + 32 * ew, 32 * kEpiWarps, kModeLossGrad, cid, ncl);
-        double wh[5];
-        wh[0] = p.whiten[0]; wh[1] = p.whiten[1]; wh[2] = p.whiten[2]; wh[3] = p.whiten[3]; wh[4] = p.whiten[4];
-        const uint32_t peer = q ^ 1u;
-        for (int64_t rl = ew; rl < n_rows; rl += kEpiWarps) {
-            int b, t;
-            locate_row(cum, p.B, cid + rl * ncl, b, t);
-            const int64_t gi = (p.seq_offset + b) * (int64_t)p.T + t;
-            const int y = __ldg(p.tokens + gi);
-            float side = 0.f;
-            if (lane < kSide) side = load_side(p, kModeLoss, lane, gi, b);
-            const int slot = (int)(rl % pair::kSlots);
-            mbar_wait(&S.row_full[slot], (uint32_t)(rl / pair::kSlots) & 1u);
-            const PairRowSlot &R = S.slot[slot];
-            Online st{R.m[lane], R.s[lane], R.u[lane]};
-#pragma unroll
-            for (int w = 1; w < pair::kStates / 32; ++w)
-                st = online_merge(st, Online{R.m[lane + 32 * w], R.s[lane + 32 * w], R.u[lane + 32 * w]});
-            st = warp_merge(st);
-            const float my_target = R.target;
-            float sv[kSide];
-#pragma unroll
-            for (int k = 0; k < kSide; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&S.row_empty[slot]);
-                // ---- exchange the half-row states with the partner CTA (DSMEM)
-                const int ps = (int)(rl % pair::kPeer);
-                const int64_t use = rl / pair::kPeer;
-                mbar_arrive_expect_tx(&S.peer_full[ps], 16);
-                if (use > 0) mbar_wait_cluster(&S.peer_empty[ps], (uint32_t)(use - 1) & 1u);
-                st_async_v4(map_peer(&S.peer_state[ps], peer), make_float4(st.m, st.s, st.u, my_target),
-                            map_peer(&S.peer_full[ps], peer));
-                mbar_wait_cluster(&S.peer_full[ps], (uint32_t)use & 1u);
-                const float4 o = S.peer_state[ps];
-                mbar_arrive_remote(map_peer(&S.peer_empty[ps], peer));
-                // both CTAs merge in CTA order: identical bits on both
-                const Online other{o.x, o.y, o.z};
-                const Online tot = q == 0 ? online_merge(st, other) : online_merge(other, st);
-                const uint32_t yq = (int64_t)y * p.elt >= half ? 1u : 0u;
-                const float target = yq == q ? my_target : o.w;
-                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-                EpiOut eo{0.f, 0.f, 0.f};
-                auto publish = [&](const EpiOut &e) {  // as soon as (lse, H, w) exist
-                    // same fp32 constants as K5 (orl_logits_grad) computes from the saved arrays
-                    const float a = (float)(p.loss_agg == 1 ? p.c2_ent / (wh[4] * (double)L) : p.c2_ent / wh[0]);
-                    GradRow &g = S.grad[rl % kGradRows];
-                    g.out_off = logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.out_stride_b, p.out_stride_t);
-                    g.y = y;
-                    g.l2 = e.lse * kLog2e;
-                    g.A1 = p.inv_temp * a * (float)kLn2;
-                    g.A0 = p.inv_temp * (a * e.H - e.w);
-                    g.wt = p.inv_temp * e.w;
-                    mbar_arrive(&S.grad_full[rl % kGradRows]);
-                };
-                row_epilogue<kModeLoss>(p, b, t, L, y, tot, target, sv, wh, S.wacc[ew], &eo, publish, q == 0);
-            }
-            __syncwarp();
-        }
-        if (kEpiWarps > 1) named_bar_sync(1, 32 * kEpiWarps);
-        if (ew == 0) {
-            double tot[kNumPartials];
-#pragma unroll
-            for (int c = 0; c < kNumPartials; ++c) {
-                double v = 0.0;
-                for (int e = 0; e < kEpiWarps; ++e) v += S.wacc[e][c];  // fixed order (zeros on CTA 1)
-                tot[c] = v;
-            }
-            finish_partials_warp(p, tot, lane);
-        }
-    } else {
-        // ===================== consumers (warps 0..15)
-        const int ct = tid;
-        const float c2 = p.c2;
-        const uint64_t c2p = pack2(c2, c2);
-        int stage = 0;
-        uint32_t phase = 0;
-        ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
-        float tgt = 0.f;
-        bool have_tgt = false;
-        int64_t tchunk = -1;
-        int tin = 0;
-        bool towner = false;
-        auto fwd_chunks = [&](int64_t rl, int64_t c0, int64_t c1) {
-            for (int64_t ci = c0; ci < c1; ++ci) {
-                mbar_wait(&S.full[stage], phase);
-                if (ci == 0) {  // row start: which chunk / thread holds the target logit
-                    acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
-                    have_tgt = false;
-                    const int y = S.row_y[rl % pair::kRowInfo];
-                    const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin) - my_off;  // within this half
-                    const bool y_ok = (y >= 0) && ((int64_t)y < p.V) && ybyte >= 0 && ybyte < my_len;
-                    tchunk = y_ok ? ybyte / kChunk : -1;
-                    tin = (int)(ybyte % kChunk);
-                    towner = ((tin >> 4) % kConsumers) == ct;
-                }
-                const int bytes = (int)min((int64_t)kChunk, my_len - ci * kChunk);
-                const uint8_t *sb = S.stage[stage];
-                if (ci == tchunk && towner) {  // raw target value, before any clamping
-                    tgt = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(sb + tin)) << 16)
-                                           : *reinterpret_cast<const float *>(sb + tin);
-                    have_tgt = true;
-                }
-                uint32_t w[kW];
-                if (bytes == kChunk) load_words<Tin, true>(w, sb, ct, kChunk >> 4);
-                else load_words<Tin, false>(w, sb, ct, bytes >> 4);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.empty[stage]);
-                if (++stage == kStages) { stage = 0; phase ^= 1u; }
-                process_words<Tin, true, 0>(acc, w, ci == 0, c2, c2p);
-            }
-        };
-        auto fwd_publish = [&](int64_t rl) {
-            float s0, s1, s2, s3;
-            unpack2(fadd2(acc.sA, acc.sB), s0, s1);
-            unpack2(fadd2(acc.uA, acc.uB), s2, s3);
-            Online st{acc.m, s0 + s1, s2 + s3};
-#pragma unroll
-            for (int off = 1; off <= 2; off <<= 1) {  // pre-merge lanes 4k..4k+3 (lane 4k keeps it)
-                Online o;
-                o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
-                o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
-                o.u = __shfl_xor_sync(0xffffffffu, st.u, off);
-                st = online_merge(st, o);
-            }
-            const int slot = (int)(rl % pair::kSlots);
-            mbar_wait(&S.row_empty[slot], ((uint32_t)(rl / pair::kSlots) & 1u) ^ 1u);
-            PairRowSlot &R = S.slot[slot];
-            if ((lane & 3) == 0) {
-                const int k = warp * 8 + (lane >> 2);
-                R.m[k] = st.m;
-                R.s[k] = st.s;
-                R.u[k] = st.u;
-            }
-            if (have_tgt) R.target = tgt;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.row_full[slot]);
-        };
-        const uint64_t st_pol = l2_evict_first_policy();
-        auto bwd_row = [&](int64_t rb) {
-            // dL/dx_v = p_v (A1 t_v + A0) + [v = y] wt,  t_v = x_v c - lse log2 e (the half-row from L2)
-            mbar_wait(&S.grad_full[rb % kGradRows], (uint32_t)(rb / kGradRows) & 1u);
-            const GradRow g = S.grad[rb % kGradRows];
-            char *obase0 = reinterpret_cast<char *>(p.dlogits) + g.out_off * (int64_t)sizeof(Tin) + my_off;
-            const uint64_t nl2 = pack2(-g.l2, -g.l2), A1p = pack2(g.A1, g.A1), A0p = pack2(g.A0, g.A0);
-            const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin) - my_off;
-            const bool y_here = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= 0 && ybyte < my_len;
-            const int64_t y_chunk = (y_here && (((int)(ybyte % kChunk) >> 4) % kConsumers) == ct) ? ybyte / kChunk : -1;
-            for (int64_t c = 0; c < nch; ++c) {
-                const int64_t off = c * kChunk;
-                const int bytes = (int)min((int64_t)kChunk, my_len - off);
-                const int nvec = bytes >> 4;
-                mbar_wait(&S.full[stage], phase);
-                const uint8_t *sb = S.stage[stage];
-                const bool own_y = c == y_chunk;
-                float xy = 0.f;
-                if (own_y) {
-                    const uint8_t *qq = sb + (ybyte - off);
-                    xy = sizeof(Tin) == 2 ? __uint_as_float(((uint32_t)*reinterpret_cast<const uint16_t *>(qq)) << 16)
-                                          : *reinterpret_cast<const float *>(qq);
-                }
-                uint4 v[kVecPerThread];
-#pragma unroll
-                for (int k = 0; k < kVecPerThread; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    if (vi < nvec) v[k] = lds128(sb + vi * 16);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.empty[stage]);
-                if (++stage == kStages) { stage = 0; phase ^= 1u; }
-                char *obase = obase0 + off;
-#pragma unroll
-                for (int k = 0; k < kVecPerThread; ++k) {
-                    const int vi = ct + k * kConsumers;
-                    if (vi >= nvec) continue;
-                    const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                    uint32_t o[4];
-                    if (sizeof(Tin) == 2) {
-#pragma unroll
-                        for (int qd = 0; qd < 4; ++qd) {
-                            const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[qd]), c2p, nl2);
-                            float t0, t1;
-                            unpack2(t2, t0, t1);
-                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
-                            float g0, g1;
-                            unpack2(gr, g0, g1);
-                            o[qd] = f32x2_to_bf16x2_rn(g0, g1);
-                        }
-                    } else {
-#pragma unroll
-                        for (int qd = 0; qd < 2; ++qd) {
-                            uint64_t x;
-                            asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(w4[2 * qd]), "r"(w4[2 * qd + 1]));
-                            const uint64_t t2 = ffma2(x, c2p, nl2);
-                            float t0, t1;
-                            unpack2(t2, t0, t1);
-                            const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
-                            float g0, g1;
-                            unpack2(gr, g0, g1);
-                            o[2 * qd] = __float_as_uint(g0);
-                            o[2 * qd + 1] = __float_as_uint(g1);
-                        }
-                    }
-                    stg128_hint(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]), st_pol);
-                }
-                if (own_y) {  // program-ordered rewrite of the target element with the delta term
-                    const float t2 = fmaf(xy, c2, -g.l2);
-                    const float gy = __fadd_rn(__fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0)), g.wt);  // not contracted
-                    Tin *yp = reinterpret_cast<Tin *>(obase0 + ybyte);
-                    if (sizeof(Tin) == 2) {
-                        const uint32_t hb = f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu;
-                        asm volatile("st.global.u16 [%0], %1;" ::"l"(yp), "h"((unsigned short)hb) : "memory");
-                    } else {
-                        *reinterpret_cast<float *>(yp) = gy;
-                    }
-                }
-            }
-        };
-        // mirrors the producer: F(i)[0, k), B(i-1), F(i)[k, n), publish F(i)
-        for (int64_t rl = 0; rl <= n_rows; ++rl) {
-            if (rl < n_rows) fwd_chunks(rl, 0, ksplit);
-            if (rl > 0) bwd_row(rl - 1);
-            if (rl < n_rows) {
-                fwd_chunks(rl, ksplit, nch);
-                fwd_publish(rl);
-            }
-        }
-        if (p.zero_masked_grad && !p.cu_seqlens) {  // this CTA's half of every masked dlogits row
-            const int64_t total = (int64_t)p.B * p.T;
-            for (int64_t qq = cid; qq < total; qq += ncl) {
-                const int b = (int)(qq / p.T), t = (int)(qq % p.T);
-                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
-                if (t < L) continue;
-                char *orow = reinterpret_cast<char *>(p.dlogits) +
-                             ((int64_t)b * p.out_stride_b + (int64_t)t * p.out_stride_t) * (int64_t)sizeof(Tin) + my_off;
-                for (int64_t o = (int64_t)ct * 16; o < my_len; o += (int64_t)kConsumers * 16)
-                    stg128_cs(orow + o, make_uint4(0u, 0u, 0u, 0u));
-            }
-        }
-    }
-    cluster_sync_all();  // no CTA leaves while its partner may still touch its shared memory
-}
-
-template <typename Tin>
-static cudaError_t launch_pair_typed(const K1Params &p, int num_sms, cudaStream_t s) {
-    const size_t smem = k1_pair_smem_bytes(p.B);
-    auto kern = k1_pair_kernel<Tin>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cfg.gridDim = dim3((unsigned)(2 * (num_sms / 2)));
-    int ncl = 0;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
-    if (e != cudaSuccess) return e;
-    if (ncl < 1) return cudaErrorInvalidConfiguration;
-    int64_t grid_cl = ncl;
-    const int64_t N_upper = (int64_t)p.B * p.T;
-    if (grid_cl > N_upper) grid_cl = N_upper;
-    if (2 * grid_cl > p.ws_stride) grid_cl = p.ws_stride / 2;
-    cfg.gridDim = dim3((unsigned)(2 * grid_cl));
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-bool k1_pair_eligible(int64_t row_bytes) { return row_bytes >= 256 && row_bytes % 16 == 0; }
-
-cudaError_t launch_k1_pair(const K1Params &p, int num_sms, cudaStream_t s) {
-    return p.elt == 2 ? launch_pair_typed<uint16_t>(p, num_sms, s) : launch_pair_typed<float>(p, num_sms, s);
 }
 
 // ---------------------------------------------------------------- launcher

@@ -623,17 +623,6 @@ static orl_status ppo_loss_impl(orl_ctx *ctx, const orl_rows *rows, const orl_lo
     const bool out_same = lay == 2 && dgap % 16 == 0 && ((grad->stride_t - actor->stride_t) * elt) % 16 == 0 &&
                           ((grad->stride_b - actor->stride_b) * elt) % 16 == 0 &&
                           reinterpret_cast<uintptr_t>(grad->dlogits) % elt == 0;
-    if (tma && out_ok && k1_pair_eligible(p.row_bytes) && getenv("ORL_FUSED_PAIR")) {
-        p.unaligned = 0;
-        p.dlogits = grad->dlogits;
-        p.out_stride_b = grad->stride_b;
-        p.out_stride_t = grad->stride_t;
-        p.c2_ent = cfg->c2;
-        p.zero_masked_grad = grad->zero_masked;
-        CUDA_TRY(ctx, launch_k1_pair(p, ctx->num_sms, as_stream(stream)));
-        ctx->launches += 1;
-        return ORL_OK;
-    }
     if ((tma && out_ok) || out_same) {
         p.unaligned = out_same ? 1 : 0;
         p.dlogits = grad->dlogits;

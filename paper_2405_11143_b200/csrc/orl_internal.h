@@ -80,10 +80,6 @@ struct K1Params {
 // Launch K1.  Returns the CUDA launch error.  `tma` selects the TMA bulk-copy
 // kernel (requires 16-byte aligned rows and row_bytes % 16 == 0).
 cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaStream_t s);
-// The fused actor pass over CTA pairs (each row split in halves between the two CTAs of
-// a cluster; kModeLossGrad semantics): rows 16-byte aligned, >= 256 bytes.
-bool k1_pair_eligible(int64_t row_bytes);
-cudaError_t launch_k1_pair(const K1Params &p, int num_sms, cudaStream_t s);
 // Micro-batches with more sequences than this keep the length prefix in global
 // memory (written by launch_lengths_prefix) instead of shared memory.
 constexpr int kSmemPrefixMax = 1024;

@@ -71,7 +71,8 @@ MUTATIONS = [
      "for (int64_t g = 0; g + 1 < n_groups; ++g)\n        if (keep[g] != 0)"),
     ("C: DAPO keep threshold strict", "oracle/orl_oracle.c", "keep[g] = (mx - mn >= 1e-12) ? 1 : 0;",
      "keep[g] = (mx - mn > 1e-12) ? 1 : 0;"),
-    ("C: ratio guard not counted", "oracle/orl_oracle.c", "if (fabs(dold) > ratio_guard) sums[9] += 1.0;", ""),
+    ("C: ratio guard not counted", "oracle/orl_oracle.c", "if (guard) sums[9] += 1.0;", ""),
+    ("C: decision flag bits swapped", "oracle/orl_oracle.c", "(uint8_t)(clipped | (vclipped << 1)", "(uint8_t)(vclipped | (clipped << 1)"),
 ]
 
 SUITES = ["tests/test_oracle_pins.py", "tests/test_oracle_pipeline_pins.py", "tests/test_oracle_properties.py"]

@@ -495,7 +495,7 @@ def run_ours(args):
     t_start = time.perf_counter()
     W = make_workload(args.config, args, env, args.lengths, args.scaling, args.batch)
     coll = choose_collective(args, env, W)
-    R = timed_steps(ctx, W, env, args.steps, args.warmup)
+    R = timed_steps(ctx, W, env, args.steps, args.warmup, pdl_chain=bool(args.pdl_chain))
     value = R["total_tokens"] / (R["ms"] / 1e3)
     roof, stage_ms = roofline(W, R)
     status, st = R["status"], R["stats"]
@@ -528,7 +528,8 @@ def run_ours(args):
                            "logits": (f"pool of {W['pool']} micro-batch buffers per model reused across the "
                                       f"{W['n_mb']} micro-batches (the batch does not fit in HBM)")
                            if W["pool"] else "resident",
-                           "shards": W["bounds"], "tokens_per_step": R["total_tokens"]},
+                           "shards": W["bounds"], "tokens_per_step": R["total_tokens"],
+                           "pdl_chain": bool(args.pdl_chain)},
                 "status": status, "stats": _stats_round(st), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": R["clocks"], "gpu_launches": int(R["launches"]),
                 "per_gpu_tokens_per_s": round(value / world, 1), "per_rank": R["per_rank"],
@@ -928,6 +929,9 @@ def main():
                     help="C1/C2 transport at N > 1 (peer: single peer-memory kernels, NCCL-checked)")
     ap.add_argument("--hidden", type=int, default=4096, help="NEXT-4 hidden size d")
     ap.add_argument("--graph", type=int, default=1, help="time the CUDA-graph replay of the llama8b leg (1/0)")
+    ap.add_argument("--pdl-chain", type=int, default=1,
+                    help="headline: K1 launches overlap the previous launch's tail (orl_set_pdl_chain; the logits "
+                         "are resident, nothing else writes them)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -38,11 +38,11 @@ def _to_dev(batch):
     return {k: (v.to(DEV) if isinstance(v, torch.Tensor) else v) for k, v in batch.items()}
 
 
-def _run(ctx, batch_dev, cfg, mb, grads=True):
+def _run(ctx, batch_dev, cfg, mb, grads=True, pdl_chain=None):
     B, T = batch_dev["tokens"].shape
     bufs = Buffers(B, T, DEV, cfg.group_size, grads=grads)
     src = lambda role, s, e: batch_dev[f"logits_{role}"][s:e]  # noqa: E731
-    status, st = run_iteration(ctx, batch_dev, cfg, bufs, src, mb=mb)
+    status, st = run_iteration(ctx, batch_dev, cfg, bufs, src, mb=mb, pdl_chain=pdl_chain)
     torch.cuda.synchronize()
     return status, st, bufs
 
@@ -260,7 +260,8 @@ def test_full_size_sampled(ctx, name, B):
         pytest.skip(f"needs {need / 1e9:.0f} GB")
     g = _gpu_batch(1234, B, T, V, "full" if name == "llama8b" else "mixed", c["rewards"], c["group_size"])
     cfg = PathConfig.from_synth(c)
-    status, st, bufs = _run(ctx, g, cfg, mb=min(c["mb"], B))
+    # bench.py's launch configuration: its micro-batch size and PDL chaining between the K1 launches
+    status, st, bufs = _run(ctx, g, cfg, mb=min(c["mb"], B), pdl_chain=True)
     assert status == "ORL_OK", status
     _sampled_rows_check(g, bufs)
     # downstream stages on the whole batch, oracle fed the GPU's fp32 upstream
@@ -1086,6 +1087,30 @@ def test_whitening_near_constant_advantages(ctx, kind):
     assert abs(st["policy_loss"] - ost["policy_loss"]) <= parity.REL * max(abs(ost["policy_loss"]), fl)
     # without the low part the fp32 advantages could not carry sigma / |mu| ~ 1e-7
     assert np.any(_np(bufs.adv_lo)[m] != 0)
+
+
+def test_pdl_chain_is_bit_identical(ctx):
+    """orl_set_pdl_chain only changes when a K1 launch may start reading (its producer does
+    not wait for the previous grid): every output and statistic is bit-identical with and
+    without it, for every pass of an iteration (logprob, reward, loss and fused modes)."""
+    c = dict(synth.CONFIGS["llama8b"], c2=0.01)
+    B, T, V = 12, 160, 8192
+    g = _gpu_batch(55, B, T, V, "mixed", mode="stress")
+    cfg = PathConfig.from_synth(dict(c, V=V))
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    out = {}
+    for chain in (False, True):
+        dl = torch.zeros(B, T, V, dtype=torch.bfloat16, device=DEV)
+        bufs = Buffers(B, T, DEV)
+        res = run_iteration(ctx, g, cfg, bufs, src, mb=3, pdl_chain=chain, grad_sink=lambda s, e: dl[s:e])
+        torch.cuda.synchronize()
+        out[chain] = (res, bufs, dl)
+    assert out[False][0] == out[True][0]
+    for k in ("logp_old", "logp_ref", "kl", "shaped", "adv", "adv_lo", "ret", "logp_new", "entropy", "lse", "dlogp",
+              "dv", "flags"):
+        assert torch.equal(getattr(out[False][1], k), getattr(out[True][1], k)), k
+    assert torch.equal(out[False][2], out[True][2])
+    assert ctx.pdl_chain is False                     # run_iteration restores the context setting
 
 
 def test_lengths_from_attention_mask(ctx):

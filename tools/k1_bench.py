@@ -29,7 +29,20 @@ ap.add_argument("--kinds", default="logp,logp+H,loss,sum,copy")
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--warm-seconds", type=float, default=0.0)
 ap.add_argument("--libs", default="")
+ap.add_argument("--l2-persist-mb", type=float, default=-1.0,
+                help="experiment: cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize) before the run")
 a = ap.parse_args()
+if a.l2_persist_mb >= 0:
+    import ctypes
+    import nvidia.cuda_runtime as _cr
+    _rt = ctypes.CDLL(os.path.join(list(_cr.__path__)[0], "lib", "libcudart.so.12"))
+    torch.cuda.init()
+    _v = ctypes.c_int(0)
+    _rt.cudaDeviceGetAttribute(ctypes.byref(_v), 108, 0)  # cudaDevAttrMaxPersistingL2CacheSize
+    _err = _rt.cudaDeviceSetLimit(0x06, ctypes.c_size_t(int(a.l2_persist_mb * 2**20)))  # cudaLimitPersistingL2CacheSize
+    _got = ctypes.c_size_t(0)
+    _rt.cudaDeviceGetLimit(ctypes.byref(_got), 0x06)
+    print(f"persisting L2 limit: max {_v.value / 2**20:.1f} MB, set err {_err}, now {_got.value / 2**20:.1f} MB")
 
 libs = a.libs.split(",") if a.libs else [os.environ.get("ORL_LIB_PATH", "")]
 mods = []

@@ -661,6 +661,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw + sizeof(K1Smem));
     int32_t *warp_tot = cum_s + (p.cum_global ? 0 : p.B);  // 32 ints after the prefix
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifndef ORL_K1_PREMERGE
+#define ORL_K1_PREMERGE 1
+#endif
+    // 1: actor passes only; 2: every pass (A/B knob)
+    constexpr bool kPremerge = ORL_K1_PREMERGE == 2 || (ORL_K1_PREMERGE == 1 && MODE != kModeLogprob);
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -835,7 +840,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             const RowSlot &R = S.slot[slot];
             Online st{R.m[lane], R.s[lane], R.u[lane]};
 #pragma unroll
-            for (int w = 1; w < kConsumerWarps; ++w)
+            for (int w = 1; w < (kPremerge ? kConsumerWarps / 4 : kConsumerWarps); ++w)
                 st = online_merge(st, Online{R.m[lane + 32 * w], R.s[lane + 32 * w], R.u[lane + 32 * w]});
             st = warp_merge(st);
             float target = R.target;
@@ -960,12 +965,28 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         float s0, s1, s2, s3;
         unpack2(fadd2(acc.sA, acc.sB), s0, s1);
         unpack2(fadd2(acc.uA, acc.uB), s2, s3);
+        Online st{acc.m, s0 + s1, s2 + s3};
+        if (kPremerge) {
+            // actor passes: a 2-round xor pre-merge (lanes 4k..4k+3, lane 4k keeps it) shortens the
+            // epilogue's merge from 16 to 4 states per lane -- the fused backward waits for it
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                Online o;
+                o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
+                o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
+                o.u = __shfl_xor_sync(0xffffffffu, st.u, off);
+                st = online_merge(st, o);
+            }
+        }
         const int slot = (int)(rl % kSlots);
         mbar_wait(&S.row_empty[slot], ((uint32_t)(rl / kSlots) & 1u) ^ 1u);
         RowSlot &R = S.slot[slot];
-        R.m[ct] = acc.m;
-        R.s[ct] = s0 + s1;
-        R.u[ct] = s2 + s3;
+        if (!kPremerge || (lane & 3) == 0) {
+            const int k = kPremerge ? warp * 8 + (lane >> 2) : ct;
+            R.m[k] = st.m;
+            R.s[k] = st.s;
+            R.u[k] = st.u;
+        }
         if (have_tgt) R.target = tgt;
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.row_full[slot]);

@@ -532,6 +532,8 @@ def run_ours(args):
                            "pdl_chain": bool(args.pdl_chain)},
                 "status": status, "stats": _stats_round(st), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "clocks": R["clocks"], "gpu_launches": int(R["launches"]),
+                "gpu_launches_note": "liborl kernels per timed step (x steps inside the timed region)",
+                "gpu_launches_timed_region": int(R["launches"]) * args.steps,
                 "per_gpu_tokens_per_s": round(value / world, 1), "per_rank": R["per_rank"],
                 "nccl_comm_ranks": world if (env["dist_mode"] and not env["shared"]) else 0}
         if env["shared"]:

@@ -14,7 +14,8 @@ from paper_2405_11143_b200.pipeline import Buffers, GraphStep, PathConfig, run_i
 DEV = torch.device("cuda:0")
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 ctx = orl.Context(0)
-KEYS = ("logp_old", "logp_ref", "kl", "shaped", "adv", "ret", "logp_new", "entropy", "lse", "dlogp", "dv")
+KEYS = ("logp_old", "logp_ref", "kl", "shaped", "adv", "adv_lo", "ret", "logp_new", "entropy", "lse", "dlogp", "dv",
+        "flags")
 fails = 0
 for it in range(iters):
     rng = np.random.default_rng(it)

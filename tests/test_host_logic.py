@@ -35,3 +35,30 @@ def test_token_balanced_shards_edge_cases():
     assert synth.split_bounds_tokens(np.zeros(8), 4, 1) == synth.split_bounds(8, 4, 1)
     with pytest.raises(ValueError):
         synth.split_bounds_tokens(np.ones(7), 2, 2)
+
+
+def _bench_cpu(args, env=None):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **(env or {}))
+    return subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], cwd=root, env=e,
+                          capture_output=True, text=True, timeout=600)
+
+
+def test_bench_rejects_world_size_mismatch():
+    """Under torchrun WORLD_SIZE must equal --gpus (a plain --gpus 8 never silently measures 1 GPU)."""
+    r = _bench_cpu(["--gpus", "1"], env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE=2 but --gpus 1" in (r.stderr + r.stdout)
+
+
+def test_bench_reference_arm_on_cpu():
+    """--impl reference: the fp64 oracle on the host cores, one JSON line with the contract's keys."""
+    import json
+    r = _bench_cpu(["--impl", "reference", "--config", "tiny", "--steps", "2", "--warmup", "1"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "tokens/s" and d["dtype"] == "f64"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}

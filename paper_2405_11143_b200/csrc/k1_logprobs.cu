@@ -125,6 +125,12 @@ constexpr int kGradRows = 4;  // ring; each slot always written by the same epil
 #define ORL_K1_FUSED_SPLIT 3
 #endif
 constexpr int kFusedSplit = ORL_K1_FUSED_SPLIT;
+#ifdef ORL_K1_PROF  // latency probes of the fused pass (tools only; not in the product build)
+__device__ unsigned long long g_k1prof[8];
+#define K1PROF(i, v) atomicAdd(&g_k1prof[i], (unsigned long long)(v))
+#else
+#define K1PROF(i, v) ((void)0)
+#endif
 
 struct __align__(128) K1Smem {
     uint8_t stage[kStages][kChunk];
@@ -286,10 +292,32 @@ struct EpiOut {
 struct NoPublish {
     __device__ void operator()(const EpiOut &) const {}
 };
+// Per-row quantities of the actor epilogue that do not depend on the logits row
+// (whitened advantage, 1/N, the entropy coefficient a of the backward): the TMA
+// kernel computes them before it waits for the row, off the backward's critical path.
+struct RowPre {
+    double A, invN;
+    float a;
+};
+__device__ __forceinline__ RowPre row_pre(const K1Params &p, int L, const float *side, const double *wh) {
+    RowPre r;
+    // derivatives are per token of the token mean (1/N) or, NEXT-2 sequence mean (Z31),
+    // of the mean of per-sequence means (1/(N_seq L_b))
+    const double N = p.loss_agg == 1 ? wh[4] * (double)L : wh[0];
+    r.invN = 1.0 / N;
+    double A = (double)side[2] + (double)side[6];  // adv (+ its low part, 0 when not given)
+    if (wh[3] != 0.0) A = (A - wh[1]) / (wh[2] + 1e-8);
+    r.A = A;
+    // same fp32 constant as K5 (orl_logits_grad) computes from the saved arrays
+    r.a = (float)(p.loss_agg == 1 ? p.c2_ent / (wh[4] * (double)L) : p.c2_ent / wh[0]);
+    return r;
+}
+
 template <int MODE, typename Publish = NoPublish>
 __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Online tot,
                              float target, const float *side, const double *wh, double *wacc,
-                             EpiOut *eo = nullptr, const Publish &publish = Publish()) {
+                             EpiOut *eo = nullptr, const Publish &publish = Publish(),
+                             const RowPre *pre = nullptr) {
     const int64_t i = (p.seq_offset + b) * (int64_t)p.T + t;
     const bool oob = (y < 0) || (y >= p.V);
     const double log2s = log2((double)tot.s);
@@ -305,12 +333,15 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         if (dead) lse = H = logp = __longlong_as_double(0x7ff8000000000000ll);
     }
     const float logp_f = (float)logp, H_f = (float)H;
-    p.logp[i] = logp_f;
-    if (p.entropy) p.entropy[i] = H_f;
-    if (p.lse) p.lse[i] = (float)lse;
-    if (p.gathered) p.gathered[i] = oob ? __int_as_float(0x7fc00000) : target;
+    auto store_row = [&]() {
+        p.logp[i] = logp_f;
+        if (p.entropy) p.entropy[i] = H_f;
+        if (p.lse) p.lse[i] = (float)lse;
+        if (p.gathered) p.gathered[i] = oob ? __int_as_float(0x7fc00000) : target;
+    };
 
     if (MODE == kModeLogprob) {
+        store_row();
         if (p.partner) {
             // S2 + S3 (Z4, Z7): d = logp_old - logp_ref,
             // r'_t = [t = L_b - 1] R_b - beta k(d)
@@ -324,31 +355,33 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         }
         return;
     } else {
-        // S7-S9 (Z11-Z17, Z22), all in fp64.  Derivatives are
-        // per token of the token mean (1/N) or, NEXT-2 sequence mean (Z31),
-        // of the mean of per-sequence means (1/(N_seq L_b)).
-        const double N = p.loss_agg == 1 ? wh[4] * (double)L : wh[0];
-        double A = (double)side[2] + (double)side[6];  // adv (+ its low part, 0 when not given)
-        if (wh[3] != 0.0) A = (A - wh[1]) / (wh[2] + 1e-8);
-        const double lpn = (double)logp_f, lpo = (double)side[0];
-        const double dold = lpn - lpo;
-        const double rho = exp(dold);
+        // S7-S9 (Z11-Z17, Z22, Z38), all in fp64.
+        const RowPre pr = pre ? *pre : row_pre(p, L, side, wh);
+        const double A = pr.A;
+        const double lpo = side[0];
+        // ratio rho = exp(logp - logp_old) (Z38: the fp64 log-prob of this epilogue).  For a
+        // finite row it is evaluated as exp(x_y / T - logp_old - ln2 m) / s, which does not
+        // wait for log2(s): this chain and the lse chain above run side by side, and the
+        // fused backward (which needs lse, H and w) starts sooner.
+        double rho = exp((double)target * (double)p.inv_temp - lpo - kLn2 * (double)tot.m) / (double)tot.s;
+        if (oob || dead || !isfinite(logp)) rho = exp(logp - lpo);
         const double rc = fmin(fmax(rho, 1.0 - p.eps_low), 1.0 + p.eps_high);
         const double unc = rho * A, clt = rc * A;
         const bool clipped = clt < unc;
         const double obj = clipped ? clt : unc;
         double dr = 0.0, dkref = 0.0;
         if (p.logp_ref) {
-            dr = lpn - (double)side[1];
+            dr = logp - (double)side[1];
             dkref = kl_grad(dr, p.kl_loss_est);
         }
-        const float wf = (float)(((clipped ? 0.0 : -rho * A) + (p.kl_in_loss ? p.beta_loss * dkref : 0.0)) / N);
+        const float wf = (float)(((clipped ? 0.0 : -rho * A) + (p.kl_in_loss ? p.beta_loss * dkref : 0.0)) * pr.invN);
         if (eo) {
             eo->lse = (float)lse;
             eo->H = H_f;
             eo->w = wf;
             publish(*eo);
         }
+        store_row();
         double vl = 0.0, dvl = 0.0;
         bool vclipped = false;
         if (p.v_new) {
@@ -367,8 +400,9 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
             }
         }
         const double kref = p.logp_ref ? kl_est(dr, p.kl_loss_est) : 0.0;
-        const double k3old = kl_est(lpo - lpn, 3);
+        const double k3old = kl_est(lpo - logp, 3);
         const double Hd = (double)H_f;
+        const double dold = logp - lpo;
         wacc[0] += 1.0;
         wacc[1] += obj;
         wacc[2] += vl;
@@ -390,7 +424,7 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         wacc[13] += Hd * invL;
         wacc[14] += kref * invL;
         if (p.dlogp) p.dlogp[i] = wf;
-        if (p.dv) p.dv[i] = (float)(p.c1 * dvl / N);
+        if (p.dv) p.dv[i] = (float)(p.c1 * dvl * pr.invN);
     }
 }
 
@@ -664,6 +698,12 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 #ifndef ORL_K1_PREMERGE
 #define ORL_K1_PREMERGE 1
 #endif
+#ifndef ORL_K1_BWD_POLY
+#define ORL_K1_BWD_POLY 0
+#endif
+#ifndef ORL_K1_ABL
+#define ORL_K1_ABL 0  // timing ablations of the fused pass (tools only): 1 fwd math, 2 bwd math, 4 bwd stores, 8 const wait
+#endif
     // 1: actor passes only; 2: every pass (A/B knob)
     constexpr bool kPremerge = ORL_K1_PREMERGE == 2 || (ORL_K1_PREMERGE == 1 && MODE != kModeLogprob);
 
@@ -835,8 +875,18 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                              ? __uint_as_float(((uint32_t)__ldg(reinterpret_cast<const unsigned short *>(rsrc) + eidx)) << 16)
                              : __ldg(reinterpret_cast<const float *>(rsrc) + eidx);
             }
+            // everything that does not depend on the row's logits is ready before the wait
+            float sv[kSide];
+#pragma unroll
+            for (int k = 0; k < kSide; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
+            const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
+            RowPre pre{0.0, 0.0, 0.f};
+            if (MODE != kModeLogprob && lane == 0) pre = row_pre(p, L, sv, wh);
             const int slot = (int)(rl % kSlots);
             mbar_wait_hint<ORL_K1_EPI_WAIT_NS>(&S.row_full[slot], (uint32_t)(rl / kSlots) & 1u);
+#ifdef ORL_K1_PROF
+            const long long t_full = clock64();
+#endif
             const RowSlot &R = S.slot[slot];
             Online st{R.m[lane], R.s[lane], R.u[lane]};
 #pragma unroll
@@ -852,19 +902,22 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 const float xt = __shfl_sync(0xffffffffu, ex, hit ? __ffs(hit) - 1 : 0);
                 if (hit) target = xt;
             }
-            float sv[kSide];
-#pragma unroll
-            for (int k = 0; k < kSide; ++k) sv[k] = __shfl_sync(0xffffffffu, side, k);
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&S.row_empty[slot]);
-                const int L = cum[b] - (b > 0 ? cum[b - 1] : 0);
                 EpiOut eo{0.f, 0.f, 0.f};
                 // the backward's row constants are published as soon as (lse, H, w) exist
+#ifdef ORL_K1_PROF
+                if (MODE == kModeLossGrad) K1PROF(1, clock64() - t_full);
+#endif
                 auto publish = [&](const EpiOut &e) {
                     if (MODE == kModeLossGrad) {
+#ifdef ORL_K1_PROF
+                        K1PROF(0, clock64() - t_full);
+                        K1PROF(2, 1);
+#endif
                         // same fp32 constants as K5 (orl_logits_grad) computes from the saved arrays
-                        const float a = (float)(p.loss_agg == 1 ? p.c2_ent / (wh[4] * (double)L) : p.c2_ent / wh[0]);
+                        const float a = pre.a;
                         GradRow &g = S.grad[rl % kGradRows];
                         g.out_off = logits_row_offset(p.cu_seqlens, p.seq_offset, b, t, p.out_stride_b, p.out_stride_t);
                         g.y = y;
@@ -875,7 +928,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         mbar_arrive(&S.grad_full[rl % kGradRows]);
                     }
                 };
-                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew], &eo, publish);
+                row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew], &eo, publish, &pre);
             }
             __syncwarp();
         }
@@ -957,11 +1010,18 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
+#if ORL_K1_ABL & 1  // timing ablation: no forward math (loads kept)
+            acc.sA ^= (uint64_t)w[0] ^ ((uint64_t)w[kW - 1] << 32);
+#else
             if (ent) process_words<Tin, true, POLY>(acc, w, ci == 0, p.c2, c2p);
             else process_words<Tin, false, POLY>(acc, w, ci == 0, p.c2, c2p);
+#endif
         }
     };
     auto fwd_publish = [&](int64_t rl) {  // row end: this thread's state into the row slot
+#ifdef ORL_K1_PROF
+        const long long t_p0 = clock64();
+#endif
         float s0, s1, s2, s3;
         unpack2(fadd2(acc.sA, acc.sB), s0, s1);
         unpack2(fadd2(acc.uA, acc.uB), s2, s3);
@@ -990,11 +1050,23 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         if (have_tgt) R.target = tgt;
         __syncwarp();
         if (lane == 0) mbar_arrive(&S.row_full[slot]);
+#ifdef ORL_K1_PROF
+        if (MODE == kModeLossGrad && ct == 0) { K1PROF(5, clock64() - t_p0); K1PROF(6, 1); }
+#endif
     };
     auto bwd_row = [&](int64_t rb) {
         // backward pass over row rb (NEXT-1, re-read from L2):
         // dL/dx_v = p_v (A1 t_v + A0) + [v = y] wt,  t_v = x_v c - lse log2 e
+#if ORL_K1_ABL & 8  // timing ablation: wait for the row constants of the first rows only (then stale ones)
+        if (rb < kGradRows)
+#endif
+#ifdef ORL_K1_PROF
+        const long long t_w0 = clock64();
+#endif
         mbar_wait(&S.grad_full[rb % kGradRows], (uint32_t)(rb / kGradRows) & 1u);
+#ifdef ORL_K1_PROF
+        if (ct == 0) { K1PROF(3, clock64() - t_w0); K1PROF(4, 1); }
+#endif
         const GradRow g = S.grad[rb % kGradRows];
         Tin *orow = reinterpret_cast<Tin *>(p.dlogits) + g.out_off;
         const uint64_t nl2 = pack2(-g.l2, -g.l2), A1p = pack2(g.A1, g.A1), A0p = pack2(g.A0, g.A0);
@@ -1021,7 +1093,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             }
         }
         const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin) - bh;  // offset in the interior
-        const uint64_t st_pol = l2_evict_first_policy();
+#ifndef ORL_K1_FUSED_STORE
+#define ORL_K1_FUSED_STORE 0  // dlogits stores: 0 evict_first hint, 1 .cs, 2 plain, 3 evict_normal hint, 4 evict_unchanged hint
+#endif
+        const uint64_t st_pol = ORL_K1_FUSED_STORE == 3 ? l2_evict_normal_policy()
+                                : ORL_K1_FUSED_STORE == 4 ? l2_evict_unchanged_policy() : l2_evict_first_policy();
         for (int64_t off = 0; off < bib; off += kChunk) {
             const int bytes = (int)min((int64_t)kChunk, bib - off);
             const int nvec = bytes >> 4;
@@ -1045,19 +1121,26 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             if (lane == 0) mbar_arrive(&S.empty[stage]);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
             char *obase = reinterpret_cast<char *>(orow) + bh + off;
+            // dL/dx of one 16-byte vector: the same per-element operations on every path (and as K5)
+            auto grad_vec = [&](const uint4 &vv, uint32_t (&o)[4]) {
+                const uint32_t w4[4] = {vv.x, vv.y, vv.z, vv.w};
+#if ORL_K1_ABL & 2  // timing ablation: no backward math (stores kept)
+                if (true) {
 #pragma unroll
-            for (int k = 0; k < kVecPerThread; ++k) {
-                const int vi = ct + k * kConsumers;
-                if (vi >= nvec) continue;
-                const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                uint32_t o[4];
+                    for (int q = 0; q < 4; ++q) o[q] = w4[q] ^ 0x55u;
+                } else
+#endif
                 if (sizeof(Tin) == 2) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[q]), c2p, nl2);
+#if ORL_K1_BWD_POLY > 0  // experiment: backward exps on the FMA pipe (inputs assumed in range)
+                        const uint64_t gr = fmul2(ex2_poly_x2<ORL_K1_BWD_POLY>(t2), ffma2(A1p, t2, A0p));
+#else
                         float t0, t1;
                         unpack2(t2, t0, t1);
                         const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
+#endif
                         float g0, g1;
                         unpack2(gr, g0, g1);
                         o[q] = f32x2_to_bf16x2_rn(g0, g1);
@@ -1077,11 +1160,38 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         o[2 * q + 1] = __float_as_uint(g1);
                     }
                 }
-#ifdef ORL_K1_FUSED_STORE_CS
-                stg128_cs(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+            };
+            auto store_vec = [&](char *dst, const uint32_t (&o)[4]) {
+#if ORL_K1_ABL & 4  // timing ablation: no backward stores (math kept)
+                if (o[0] == 0x7fc17fc1u && o[3] == 0x7fc17fc1u)
+                stg128_hint(dst, make_uint4(o[0], o[1], o[2], o[3]), st_pol);
+#elif ORL_K1_FUSED_STORE == 1
+                stg128_cs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+#elif ORL_K1_FUSED_STORE == 2
+                asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(o[0]), "r"(o[1]),
+                             "r"(o[2]), "r"(o[3]) : "memory");
 #else
-                stg128_hint(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]), st_pol);
+                stg128_hint(dst, make_uint4(o[0], o[1], o[2], o[3]), st_pol);
 #endif
+            };
+            if (nvec == kVecPerThread * kConsumers) {
+                // full chunk: every thread owns kVecPerThread vectors -- one straight-line block
+                // (no per-vector branches), so the vectors' MUFU / FMA chains interleave
+                char *tb = obase + ct * 16;
+                uint32_t o[kVecPerThread][4];
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) grad_vec(v[k], o[k]);
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) store_vec(tb + k * (kConsumers * 16), o[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    const int vi = ct + k * kConsumers;
+                    if (vi >= nvec) continue;
+                    uint32_t o[4];
+                    grad_vec(v[k], o);
+                    store_vec(obase + vi * 16, o);
+                }
             }
             if (own_y) {  // program-ordered rewrite of the target element with the delta term
                 const float t2 = fmaf(xy, p.c2, -g.l2);
@@ -1361,3 +1471,11 @@ cudaError_t launch_k1(const K1Params &p, bool tma, int mode, int num_sms, cudaSt
 }
 
 }  // namespace orl
+
+#ifdef ORL_K1_PROF
+extern "C" int orl_debug_k1_prof(unsigned long long *out8) {
+    if (cudaMemcpyFromSymbol(out8, orl::g_k1prof, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    return cudaMemcpyToSymbol(orl::g_k1prof, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif

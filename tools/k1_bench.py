@@ -46,13 +46,19 @@ if a.l2_persist_mb >= 0:
 
 libs = a.libs.split(",") if a.libs else [os.environ.get("ORL_LIB_PATH", "")]
 mods = []
-for path in libs:
-    # load each build as a separate binding module instance
+import importlib.util  # noqa: E402
+
+_ORL_PY = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2405_11143_b200", "orl.py")
+for i, path in enumerate(libs):
+    # each build gets its own binding module instance (own ctypes handle); importlib.reload
+    # would mutate one shared module so that every "lib" ran the last build loaded
     if path:
-        os.environ["ORL_LIB_PATH"] = path
-    import importlib
-    import paper_2405_11143_b200.orl as orl_mod
-    orl_mod = importlib.reload(orl_mod)
+        os.environ["ORL_LIB_PATH"] = os.path.abspath(path)
+    spec = importlib.util.spec_from_file_location(f"orl_build_{i}", _ORL_PY)
+    orl_mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = orl_mod
+    spec.loader.exec_module(orl_mod)
+    assert os.path.abspath(orl_mod.LIB_PATH) == os.path.abspath(path or orl_mod.LIB_PATH)
     mods.append((os.path.basename(path) or "liborl.so", orl_mod))
 
 from paper_2405_11143_b200 import synth  # noqa: E402

@@ -113,7 +113,7 @@ typedef struct {
     const void *ptr;
     int32_t dtype; /* orl_dtype */
     int32_t pad_;
-    int64_t V;
+    int64_t V;        /* vocabulary size; V * element size < 2^31 bytes (else ORL_E_SHAPE) */
     int64_t stride_b; /* elements */
     int64_t stride_t; /* elements */
 } orl_logits;

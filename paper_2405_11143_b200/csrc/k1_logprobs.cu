@@ -125,6 +125,21 @@ constexpr int kGradRows = 4;  // ring; each slot always written by the same epil
 #define ORL_K1_FUSED_SPLIT 3
 #endif
 constexpr int kFusedSplit = ORL_K1_FUSED_SPLIT;
+// Stage release: every consumer thread arrives on the stage's empty barrier after its
+// shared-memory loads (1), or lane 0 of each warp after a __syncwarp (0).
+#ifndef ORL_K1_THREAD_ARRIVE
+#define ORL_K1_THREAD_ARRIVE 1
+#endif
+constexpr int kEmptyArrivals = ORL_K1_THREAD_ARRIVE ? kConsumers : kConsumerWarps;
+__device__ __forceinline__ void release_stage(uint64_t *empty, int lane) {
+#if ORL_K1_THREAD_ARRIVE
+    (void)lane;
+    mbar_arrive(empty);  // release: this thread's loads of the stage happen before
+#else
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty);
+#endif
+}
 #ifdef ORL_K1_PROF  // latency probes of the fused pass (tools only; not in the product build)
 __device__ unsigned long long g_k1prof[8];
 #define K1PROF(i, v) atomicAdd(&g_k1prof[i], (unsigned long long)(v))
@@ -621,12 +636,32 @@ __device__ __forceinline__ void process_words(ThreadAcc &a, uint32_t (&w)[NW], b
         }
         a.m = fmax_nan(cm * c2, kMInit);
     }
+#ifndef ORL_K1_CHUNK_PARTIAL
+#define ORL_K1_CHUNK_PARTIAL 1
+#endif
+#if ORL_K1_CHUNK_PARTIAL
+    // the chunk is summed into fresh partials and added to the row state only if the
+    // fast pass held (no saved copy of the state to restore: fewer moves per chunk)
+    ThreadAcc c{a.m, 0ull, 0ull, 0ull, 0ull};
+    acc_words<Tin, ENT, POLY, NW>(c, w, c2p);
+    if (needs_redo<ENT>(c)) {
+        exact_words<Tin, ENT, NW>(a, w, c2, c2p);
+    } else {
+        a.sA = fadd2(a.sA, c.sA);
+        a.sB = fadd2(a.sB, c.sB);
+        if (ENT) {
+            a.uA = fadd2(a.uA, c.uA);
+            a.uB = fadd2(a.uB, c.uB);
+        }
+    }
+#else
     const ThreadAcc saved = a;
     acc_words<Tin, ENT, POLY, NW>(a, w, c2p);
     if (needs_redo<ENT>(a)) {
         a = saved;
         exact_words<Tin, ENT, NW>(a, w, c2, c2p);
     }
+#endif
 }
 
 // One scalar logit (an unaligned row's head or tail element) folded exactly into the
@@ -710,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&S.full[s], 1);
-            mbar_init(&S.empty[s], kConsumerWarps);
+            mbar_init(&S.empty[s], kEmptyArrivals);
         }
         for (int s = 0; s < kSlots; ++s) {
             mbar_init(&S.row_full[s], kConsumerWarps);
@@ -959,23 +994,24 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
     int stage = 0;
     uint32_t phase = 0;
     const int64_t n_rows = N > (int64_t)blockIdx.x ? (N - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const int64_t nch = (row_bytes + kChunk - 1) / kChunk;
-    const int64_t ksplit = MODE == kModeLossGrad ? min((int64_t)kFusedSplit, nch) : nch;
+    // chunk bookkeeping in 32 bits (a row is < 2^31 bytes: V <= 2^28, checked on the host)
+    const int nch = (int)((row_bytes + kChunk - 1) / kChunk);
+    const int ksplit = MODE == kModeLossGrad ? min(kFusedSplit, nch) : nch;
     // forward state of the row in progress (survives an interleaved backward row)
     ThreadAcc acc{kMInit, 0ull, 0ull, 0ull, 0ull};
     float tgt = 0.f;
     bool have_tgt = false;
-    int64_t tchunk = -1;
+    int tchunk = -1;
     int tin = 0;
     bool towner = false;
     // unaligned rows (p.unaligned, not in the fused mode): the chunks cover the aligned
     // interior [h, h + ib) of the row; its < 16-byte head and tail are folded in by
     // scalar loads after the first chunk
     constexpr bool unal = UNAL;
-    int64_t ib = row_bytes, row_nch = nch;
+    int ib = (int)row_bytes, row_nch = nch;
     int row_h = 0, row_yv = -1;
-    auto fwd_chunks = [&](int64_t rl, int64_t c0, int64_t c1) {
-        for (int64_t ci = c0; ci < (unal ? (ci == 0 ? 1 : min(c1, row_nch)) : c1); ++ci) {
+    auto fwd_chunks = [&](int64_t rl, int c0, int c1) {
+        for (int ci = c0; ci < (unal ? (ci == 0 ? 1 : min(c1, row_nch)) : c1); ++ci) {
             mbar_wait_hint<ORL_K1_CONS_WAIT_NS>(&S.full[stage], phase);
             if (ci == 0) {  // row start: which chunk / thread holds the target logit
                 acc = ThreadAcc{kMInit, 0ull, 0ull, 0ull, 0ull};
@@ -984,17 +1020,17 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 row_yv = y;
                 if (unal) {
                     row_h = S.row_h[rl % kRowInfo];
-                    ib = (row_bytes - row_h) & ~(int64_t)15;
+                    ib = ((int)row_bytes - row_h) & ~15;
                     row_nch = (ib + kChunk - 1) / kChunk;
                 }
                 const bool y_ok = (y >= 0) && ((int64_t)y < p.V);
-                const int64_t ybyte = (int64_t)y * (int64_t)sizeof(Tin) - row_h;  // offset in the interior
+                const int ybyte = y * (int)sizeof(Tin) - row_h;  // offset in the interior
                 tchunk = (y_ok && ybyte >= 0 && ybyte < ib) ? ybyte / kChunk : -1;
-                tin = (int)(ybyte % kChunk);
+                tin = ybyte % kChunk;
                 towner = ((tin >> 4) % kConsumers) == ct;
             }
-            const int64_t off = ci * kChunk;
-            const int bytes = (int)min((int64_t)kChunk, ib - off);
+            const int off = ci * kChunk;
+            const int bytes = min(kChunk, ib - off);
             const uint8_t *sb = S.stage[stage];
             if (ci == tchunk && towner) {  // raw target value, before any clamping
                 tgt = sizeof(Tin) == 2
@@ -1007,8 +1043,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             uint32_t w[kW];
             if (bytes == kChunk) load_words<Tin, true>(w, sb, ct, kChunk >> 4);
             else load_words<Tin, false>(w, sb, ct, bytes >> 4);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[stage]);
+            release_stage(&S.empty[stage], lane);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
 #if ORL_K1_ABL & 1  // timing ablation: no forward math (loads kept)
             acc.sA ^= (uint64_t)w[0] ^ ((uint64_t)w[kW - 1] << 32);
@@ -1073,10 +1108,11 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         // unaligned rows: the chunks are the row's aligned interior [bh, bh + bib) (dlogits rows are
         // misaligned like the logits rows, checked on the host); head / tail written singly here
         const int bh = UNAL ? S.row_h[rb % kRowInfo] : 0;
-        const int64_t bib = UNAL ? ((row_bytes - bh) & ~(int64_t)15) : row_bytes;
+        const int rbytes = (int)row_bytes;
+        const int bib = UNAL ? ((rbytes - bh) & ~15) : rbytes;
         if (UNAL && warp == 0) {  // head / tail (<= 14 elements): warp 0
             const int head_e = bh / (int)sizeof(Tin);
-            const int tail_e = (int)((row_bytes - bh - bib) / (int64_t)sizeof(Tin));
+            const int tail_e = (rbytes - bh - bib) / (int)sizeof(Tin);
             int idx = -1;
             if (ct < head_e) idx = ct;
             else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
@@ -1092,19 +1128,19 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 }
             }
         }
-        const int64_t ybyte = (int64_t)g.y * (int64_t)sizeof(Tin) - bh;  // offset in the interior
+        const bool y_ok = g.y >= 0 && (int64_t)g.y < p.V;
+        const int ybyte = g.y * (int)sizeof(Tin) - bh;  // offset in the interior
 #ifndef ORL_K1_FUSED_STORE
 #define ORL_K1_FUSED_STORE 0  // dlogits stores: 0 evict_first hint, 1 .cs, 2 plain, 3 evict_normal hint, 4 evict_unchanged hint
 #endif
         const uint64_t st_pol = ORL_K1_FUSED_STORE == 3 ? l2_evict_normal_policy()
                                 : ORL_K1_FUSED_STORE == 4 ? l2_evict_unchanged_policy() : l2_evict_first_policy();
-        for (int64_t off = 0; off < bib; off += kChunk) {
-            const int bytes = (int)min((int64_t)kChunk, bib - off);
+        for (int off = 0; off < bib; off += kChunk) {
+            const int bytes = min(kChunk, bib - off);
             const int nvec = bytes >> 4;
             mbar_wait(&S.full[stage], phase);
             const uint8_t *sb = S.stage[stage];
-            const bool own_y = g.y >= 0 && (int64_t)g.y < p.V && ybyte >= 0 && ybyte >= off && ybyte < off + bytes &&
-                               (((int)(ybyte - off) >> 4) % kConsumers) == ct;
+            const bool own_y = y_ok && ybyte >= off && ybyte < off + bytes && (((ybyte - off) >> 4) % kConsumers) == ct;
             float xy = 0.f;
             if (own_y) {
                 const uint8_t *q = sb + (ybyte - off);
@@ -1117,8 +1153,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 const int vi = ct + k * kConsumers;
                 if (vi < nvec) v[k] = lds128(sb + vi * 16);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[stage]);
+            release_stage(&S.empty[stage], lane);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
             char *obase = reinterpret_cast<char *>(orow) + bh + off;
             // dL/dx of one 16-byte vector: the same per-element operations on every path (and as K5)

@@ -126,8 +126,9 @@ static orl_status validate_rows_logits(orl_ctx *ctx, const orl_rows *rows, const
         return fail(ctx, ORL_E_DTYPE, "unknown logits dtype %d", lg->dtype);
     orl_status st = validate_rows(ctx, rows, inv_temp);
     if (st) return st;
-    if (lg->V < 1 || lg->V >= ((int64_t)1 << 31))
-        return fail(ctx, ORL_E_SHAPE, "V=%lld invalid", (long long)lg->V);
+    // a row (V elements) must stay below 2^31 bytes: the kernels keep row offsets in 32 bits
+    if (lg->V < 1 || lg->V * (lg->dtype == ORL_BF16 ? 2 : 4) >= ((int64_t)1 << 31))
+        return fail(ctx, ORL_E_SHAPE, "V=%lld invalid (a row must be < 2 GiB)", (long long)lg->V);
     if (lg->stride_t < lg->V || lg->stride_b < 0)
         return fail(ctx, ORL_E_SHAPE, "strides (%lld, %lld) invalid for V=%lld", (long long)lg->stride_b,
                     (long long)lg->stride_t, (long long)lg->V);

@@ -509,6 +509,13 @@ def test_host_argument_errors(ctx):
     st = orl._lib.orl_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(lg), 1.0, ctypes.c_void_p(lp.data_ptr() + 2),
                                None, None, None, None, 1, 0.0, None, None, None, None)
     assert orl.STATUS[st] == "ORL_E_ALIGN"
+    # a logits row of 2 GiB or more (V * element size >= 2^31) is rejected before any access:
+    # the kernels keep row offsets in 32 bits (orl.h, orl_logits.V)
+    for dtype, V_big in ((0, 1 << 30), (1, 1 << 29)):   # ORL_BF16, ORL_F32
+        big = orl.Logits(x.data_ptr(), dtype, 0, V_big, V_big, V_big)
+        st = orl._lib.orl_logprobs(ctx.h, ctypes.byref(rows), ctypes.byref(big), 1.0, ctypes.c_void_p(lp.data_ptr()),
+                                   None, None, None, None, 1, 0.0, None, None, None, None)
+        assert orl.STATUS[st] == "ORL_E_SHAPE", (dtype, orl.STATUS[st])
 
 
 # --------------------------------------------------------------------------- determinism / DP

@@ -808,11 +808,18 @@ def run_e2e(args, env, W, R_dev):
     except Exception:  # pragma: no cover
         avail = None
     ok = avail is None or H * mb_bytes * world <= 0.6 * avail
+    # device staging (2 micro-batch slots x 3 models); with ORL_BENCH_SHARED_GPU every rank's
+    # copy lives on the one GPU
+    dev_need = 2 * mb_bytes * (world if env["shared"] else 1)
+    dev_ok = torch.cuda.mem_get_info(dev)[0] >= 1.1 * dev_need
+    ok = ok and dev_ok
     if env["dist_mode"]:                      # every rank takes the same decision
         t = torch.tensor([1.0 if ok else 0.0], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         ok = t.item() == 1.0
     if not ok:
+        if not dev_ok:
+            return {"skipped": f"needs {dev_need / 1e9:.0f} GB of free device memory for the staging slots"}
         return {"skipped": f"needs {H * mb_bytes * world / 1e9:.0f} GB of pinned host memory "
                            f"({(avail or 0) / 1e9:.0f} GB available on this node)"}
     # device view of slot h: pool slot h, or the resident micro-batch h

@@ -733,9 +733,6 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 #ifndef ORL_K1_PREMERGE
 #define ORL_K1_PREMERGE 1
 #endif
-#ifndef ORL_K1_BWD_POLY
-#define ORL_K1_BWD_POLY 0
-#endif
 #ifndef ORL_K1_ABL
 #define ORL_K1_ABL 0  // timing ablations of the fused pass (tools only): 1 fwd math, 2 bwd math, 4 bwd stores, 8 const wait
 #endif
@@ -1169,13 +1166,9 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[q]), c2p, nl2);
-#if ORL_K1_BWD_POLY > 0  // experiment: backward exps on the FMA pipe (inputs assumed in range)
-                        const uint64_t gr = fmul2(ex2_poly_x2<ORL_K1_BWD_POLY>(t2), ffma2(A1p, t2, A0p));
-#else
                         float t0, t1;
                         unpack2(t2, t0, t1);
                         const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
-#endif
                         float g0, g1;
                         unpack2(gr, g0, g1);
                         o[q] = f32x2_to_bf16x2_rn(g0, g1);

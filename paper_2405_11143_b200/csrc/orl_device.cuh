@@ -91,36 +91,6 @@ __device__ __forceinline__ uint64_t poly_ex2x2(uint64_t tt) {
     return pack2(__uint_as_float(o0), __uint_as_float(o1));
 }
 
-// 2^t for a packed pair on the FMA/ALU pipes, for t in [-126, 127] (the caller
-// guarantees the range): Cody-Waite split t = j + f, j = rint(t) by the
-// magic-number add, 2^f on [-1/2, 1/2] by a degree-D polynomial (near-minimax
-// relative error: D = 3 7.5e-5, D = 4 2.7e-6), then j added to the exponent
-// field (one LEA per lane).  8 (D = 3) / 9 (D = 4) FMA/ALU instructions per pair.
-template <int D>
-__device__ __forceinline__ uint64_t ex2_poly_x2(uint64_t t) {
-    const uint64_t r = fadd2(t, pack2(12582912.f, 12582912.f));  // 1.5 * 2^23: low bits = rint(t)
-    const uint64_t jf = fadd2(r, pack2(-12582912.f, -12582912.f));
-    const uint64_t f = ffma2(jf, pack2(-1.f, -1.f), t);            // t - j, exact
-    uint64_t q;
-    if (D == 3) {
-        q = ffma2(pack2(5.517132207751274e-2f, 5.517132207751274e-2f), f,
-                  pack2(2.4261054396629333e-1f, 2.4261054396629333e-1f));
-        q = ffma2(q, f, pack2(6.932609677314758e-1f, 6.932609677314758e-1f));
-        q = ffma2(q, f, pack2(9.999281167984009e-1f, 9.999281167984009e-1f));
-    } else {
-        q = ffma2(pack2(9.570068679749966e-3f, 9.570068679749966e-3f), f,
-                  pack2(5.5917806923389435e-2f, 5.5917806923389435e-2f));
-        q = ffma2(q, f, pack2(2.40247443318367e-1f, 2.40247443318367e-1f));
-        q = ffma2(q, f, pack2(6.931218504905701e-1f, 6.931218504905701e-1f));
-        q = ffma2(q, f, pack2(9.999992847442627e-1f, 9.999992847442627e-1f));
-    }
-    float q0, q1, r0, r1;
-    unpack2(q, q0, q1);
-    unpack2(r, r0, r1);
-    return pack2(__uint_as_float(__float_as_uint(q0) + (__float_as_uint(r0) << 23)),
-                 __uint_as_float(__float_as_uint(q1) + (__float_as_uint(r1) << 23)));
-}
-
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 

@@ -84,7 +84,15 @@ constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kProducerWarp = kConsumerWarps;      // TMA issue
 constexpr int kEpilogueWarp = kConsumerWarps + 1;  // first of the merge + fp64 epilogue warps
 constexpr int kEpiWarps = ORL_K1_EPI_WARPS;         // rows alternate between them
-constexpr int kThreads = kConsumers + 32 + 32 * kEpiWarps;
+// Fused actor pass: dlogits of full backward chunks written back into the chunk's stage and
+// stored by a TMA bulk copy from a dedicated store warp (1), or STG.128 from the consumer
+// threads (0).
+#ifndef ORL_K1_BWD_TMA_STORE
+#define ORL_K1_BWD_TMA_STORE 0
+#endif
+constexpr bool kTmaStore = ORL_K1_BWD_TMA_STORE != 0;
+constexpr int kStoreWarp = kConsumerWarps + 1 + ORL_K1_EPI_WARPS;
+constexpr int kThreads = kConsumers + 32 + 32 * kEpiWarps + (kTmaStore ? 32 : 0);
 constexpr int kChunk = ORL_K1_CHUNK;  // bytes per TMA stage
 constexpr int kStages = ORL_K1_STAGES;
 // Row-partial ring (consumers -> epilogue warps).  Row rl uses slot rl % kSlots
@@ -158,6 +166,8 @@ struct __align__(128) K1Smem {
     float row_x[kRowInfo][16];      // unaligned rows: raw head elements, then tail elements
     uint64_t grad_full[kGradRows];
     GradRow grad[kGradRows];
+    uint64_t written[kStages];      // kTmaStore: consumers -> store warp, chunk results in the stage
+    uint64_t st_dst[kStages];       // kTmaStore: global destination of the staged chunk
     RowSlot slot[kSlots];
     double wacc[kEpiWarps][kNumPartials];
 };
@@ -749,6 +759,8 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             mbar_init(&S.row_empty[s], 1);
         }
         for (int s = 0; s < kGradRows; ++s) mbar_init(&S.grad_full[s], 1);
+        if (kTmaStore)
+            for (int s = 0; s < kStages; ++s) mbar_init(&S.written[s], kConsumers);
         fence_mbar_init();
     }
     if (tid < kEpiWarps * kNumPartials) (&S.wacc[0][0])[tid] = 0.0;
@@ -869,6 +881,51 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
         return;
     }
 
+    if (kTmaStore && warp == kStoreWarp) {
+        // ===================== store warp (kTmaStore): one lane bulk-stores each full
+        // backward chunk the consumers wrote back into its stage, then frees the stage.
+        // It replays the producer's chunk schedule (all rows have nch chunks: aligned rows)
+        // and touches only the staged chunks.
+        if (MODE == kModeLossGrad && !UNAL && lane == 0) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            const uint64_t pol = l2_evict_first_policy();
+            const int64_t n_rows = N > (int64_t)blockIdx.x ? (N - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+            const int nch = (int)((row_bytes + kChunk - 1) / kChunk);
+            const int ksplit = min(kFusedSplit, nch);
+            int stage = 0;
+            uint32_t wph = 0;  // bit s: parity of written[s]
+            for (int64_t rl = 0; rl <= n_rows; ++rl) {
+                if (rl < n_rows) stage = (stage + ksplit) % kStages;
+                if (rl > 0) {
+                    // two bulk stores in flight: stage j is freed once store j+1 has been issued and
+                    // store j has read its shared memory; the row's last staged stage is freed
+                    // before the store warp waits on the next row (the ring needs it for the forward)
+                    int pend = -1;
+                    for (int c = 0; c < nch; ++c) {
+                        const int bytes = min(kChunk, (int)row_bytes - c * kChunk);
+                        if (bytes == kChunk) {
+                            mbar_wait(&S.written[stage], (wph >> stage) & 1u);
+                            wph ^= 1u << stage;
+                            tma_store_1d(reinterpret_cast<void *>(S.st_dst[stage]), S.stage[stage], kChunk, pol);
+                            if (pend >= 0) {
+                                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                                mbar_arrive_cnt(&S.empty[pend], kEmptyArrivals);
+                            }
+                            pend = stage;
+                        }
+                        stage = (stage + 1) % kStages;
+                    }
+                    if (pend >= 0) {
+                        tma_store_wait_read0();
+                        mbar_arrive_cnt(&S.empty[pend], kEmptyArrivals);
+                    }
+                }
+                if (rl < n_rows) stage = (stage + nch - ksplit) % kStages;
+            }
+            tma_store_wait_all();
+        }
+        return;
+    }
     if (warp >= kEpilogueWarp) {
         // ===================== epilogue: merge the partials, fp64 per-row math ===
         const int ew = warp - kEpilogueWarp;  // rows rl with rl % kEpiWarps == ew
@@ -1136,8 +1193,12 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             const int bytes = min(kChunk, bib - off);
             const int nvec = bytes >> 4;
             mbar_wait(&S.full[stage], phase);
+            const int cst = stage;  // this chunk's stage
             const uint8_t *sb = S.stage[stage];
             const bool own_y = y_ok && ybyte >= off && ybyte < off + bytes && (((ybyte - off) >> 4) % kConsumers) == ct;
+            // kTmaStore: a full chunk's results go back into its stage; the store warp bulk-stores
+            // the stage and frees it (same rule as the store warp's schedule: aligned rows, full chunk)
+            const bool staged = kTmaStore && !UNAL && bytes == kChunk;
             float xy = 0.f;
             if (own_y) {
                 const uint8_t *q = sb + (ybyte - off);
@@ -1150,7 +1211,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 const int vi = ct + k * kConsumers;
                 if (vi < nvec) v[k] = lds128(sb + vi * 16);
             }
-            release_stage(&S.empty[stage], lane);
+            if (!staged) release_stage(&S.empty[stage], lane);
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
             char *obase = reinterpret_cast<char *>(orow) + bh + off;
             // dL/dx of one 16-byte vector: the same per-element operations on every path (and as K5)
@@ -1202,6 +1263,29 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 stg128_hint(dst, make_uint4(o[0], o[1], o[2], o[3]), st_pol);
 #endif
             };
+            if (staged) {
+                uint32_t o[kVecPerThread][4];
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) grad_vec(v[k], o[k]);
+                uint8_t *wb = const_cast<uint8_t *>(sb);
+#pragma unroll
+                for (int k = 0; k < kVecPerThread; ++k) {
+                    uint4 *q = reinterpret_cast<uint4 *>(wb + (ct + k * kConsumers) * 16);
+                    *q = make_uint4(o[k][0], o[k][1], o[k][2], o[k][3]);
+                }
+                if (own_y) {  // the target element with the delta term, after its vector (program order)
+                    const float t2 = fmaf(xy, p.c2, -g.l2);
+                    const float gy = __fadd_rn(__fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0)), g.wt);
+                    if (sizeof(Tin) == 2)
+                        *reinterpret_cast<uint16_t *>(wb + (ybyte - off)) = (uint16_t)(f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu);
+                    else
+                        *reinterpret_cast<float *>(wb + (ybyte - off)) = gy;
+                }
+                fence_proxy_async();  // generic-proxy smem writes -> the bulk copy engine
+                if (ct == 0) S.st_dst[cst] = reinterpret_cast<uint64_t>(obase);
+                mbar_arrive(&S.written[cst]);
+                continue;
+            }
             if (nvec == kVecPerThread * kConsumers) {
                 // full chunk: every thread owns kVecPerThread vectors -- one straight-line block
                 // (no per-vector branches), so the vectors' MUFU / FMA chains interleave

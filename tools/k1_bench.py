@@ -123,11 +123,21 @@ if a.warm_seconds > 0:
     first = next(iter(ctxs))
     while time.time() - t0 < a.warm_seconds:
         timed(first, "loss")
-res = {}
+try:  # per-block SM clock / power (NVML, sampled right after each timed block)
+    import pynvml
+    pynvml.nvmlInit()
+    _nv = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    def _clk():
+        return (pynvml.nvmlDeviceGetClockInfo(_nv, pynvml.NVML_CLOCK_SM), pynvml.nvmlDeviceGetPowerUsage(_nv) / 1e3)
+except Exception:  # pragma: no cover
+    _clk = None
+res, rclk = {}, {}
 for r in range(a.repeat):
     for name in ctxs:
         for kind in a.kinds.split(","):
             res.setdefault((name, kind), []).append(timed(name, kind))
+            if _clk:
+                rclk.setdefault((name, kind), []).append(_clk())
 smi.terminate()
 out, _ = smi.communicate()
 clk = [float(l.split(",")[0]) for l in out.strip().splitlines() if l.strip()]
@@ -135,7 +145,10 @@ pw = [float(l.split(",")[1]) for l in out.strip().splitlines() if l.strip()]
 for (name, kind), v in res.items():
     ms = statistics.median(v)
     gb = a.mb * T * V * 2 / 1e9 * (2 if kind in ("copy", "grad", "lossgrad") else 1)
+    ck = rclk.get((name, kind))
+    cks = (f"  [{statistics.median(c for c, _ in ck):.0f} MHz {statistics.median(w for _, w in ck):.0f} W]"
+           if ck else "")
     print(f"{name:28s} {kind:7s} V={V}: {ms * 1e3:8.1f} us/launch  {gb / ms * 1e3:8.1f} GB/s  "
-          f"(min {min(v) * 1e3:.1f} max {max(v) * 1e3:.1f})")
+          f"(min {min(v) * 1e3:.1f} max {max(v) * 1e3:.1f}){cks}")
 if clk:
     print(f"SM clock median {statistics.median(clk):.0f} MHz (min {min(clk):.0f}), power median {statistics.median(pw):.0f} W")

@@ -15,10 +15,16 @@
 //     6-stage shared-memory ring guarded by full/empty mbarriers: ~192 KB in
 //     flight per SM (Little's law needs ~45 KB at ~7 TB/s).
 //   * Consumers copy their 4 x 16 B of a chunk to registers with conflict-free
-//     128-bit ld.shared, hand the stage back at once, and keep a per-thread
-//     online (max, sum, first-moment) state in log2 units with packed f32x2
-//     FMA/ADD (FFMA2/FADD2), one MUFU.EX2 per element; m is seeded from the
-//     thread's first vector and a chunk is redone exactly only if it overflows.
+//     128-bit ld.shared, hand the stage back at once (every thread arrives on
+//     the stage's empty barrier), and keep a per-thread online (max, sum,
+//     first-moment) state in log2 units with packed f32x2 FMA/ADD
+//     (FFMA2/FADD2), one MUFU.EX2 per element; m is seeded from the thread's
+//     first vector, a chunk is summed into fresh partials that join the row
+//     state only if the fast pass held, else the chunk is redone exactly.
+//   * Fused actor pass (loss + dL/dlogits): the backward of row i-1 re-reads
+//     the row from L2 after 3 forward chunks of row i; the epilogue publishes
+//     the row's gradient constants early (ratio chain beside the lse chain,
+//     per-row terms computed before the row arrives).
 //   * Row end: every consumer thread's state goes into a 4-slot row ring
 //     (mbarrier protected); the two epilogue warps take alternate rows, merge
 //     the 512 states in a fixed order and run the fp64 epilogue while the

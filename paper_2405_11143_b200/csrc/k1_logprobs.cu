@@ -91,12 +91,15 @@ constexpr int kProducerWarp = kConsumerWarps;      // TMA issue
 constexpr int kEpilogueWarp = kConsumerWarps + 1;  // first of the merge + fp64 epilogue warps
 constexpr int kEpiWarps = ORL_K1_EPI_WARPS;         // rows alternate between them
 // Fused actor pass: dlogits of full backward chunks written back into the chunk's stage and
-// stored by a TMA bulk copy from a dedicated store warp (1), or STG.128 from the consumer
-// threads (0).
+// stored by a TMA bulk copy from a dedicated store warp (n > 0: every n-th chunk of a row,
+// the others by STG.128), or STG.128 from the consumer threads only (0).
 #ifndef ORL_K1_BWD_TMA_STORE
 #define ORL_K1_BWD_TMA_STORE 0
 #endif
 constexpr bool kTmaStore = ORL_K1_BWD_TMA_STORE != 0;
+#ifndef ORL_K1_STORE_WAIT_NS
+#define ORL_K1_STORE_WAIT_NS 20000  // the store warp parks while the consumers compute a chunk
+#endif
 constexpr int kStoreWarp = kConsumerWarps + 1 + ORL_K1_EPI_WARPS;
 constexpr int kThreads = kConsumers + 32 + 32 * kEpiWarps + (kTmaStore ? 32 : 0);
 constexpr int kChunk = ORL_K1_CHUNK;  // bytes per TMA stage
@@ -909,8 +912,8 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                     int pend = -1;
                     for (int c = 0; c < nch; ++c) {
                         const int bytes = min(kChunk, (int)row_bytes - c * kChunk);
-                        if (bytes == kChunk) {
-                            mbar_wait(&S.written[stage], (wph >> stage) & 1u);
+                        if (bytes == kChunk && (c % ORL_K1_BWD_TMA_STORE) == 0) {
+                            mbar_wait_hint<ORL_K1_STORE_WAIT_NS>(&S.written[stage], (wph >> stage) & 1u);
                             wph ^= 1u << stage;
                             tma_store_1d(reinterpret_cast<void *>(S.st_dst[stage]), S.stage[stage], kChunk, pol);
                             if (pend >= 0) {
@@ -1204,7 +1207,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             const bool own_y = y_ok && ybyte >= off && ybyte < off + bytes && (((ybyte - off) >> 4) % kConsumers) == ct;
             // kTmaStore: a full chunk's results go back into its stage; the store warp bulk-stores
             // the stage and frees it (same rule as the store warp's schedule: aligned rows, full chunk)
-            const bool staged = kTmaStore && !UNAL && bytes == kChunk;
+            const bool staged = kTmaStore && !UNAL && bytes == kChunk && ((off / kChunk) % ORL_K1_BWD_TMA_STORE) == 0;
             float xy = 0.f;
             if (own_y) {
                 const uint8_t *q = sb + (ybyte - off);

@@ -97,6 +97,7 @@ constexpr int kEpiWarps = ORL_K1_EPI_WARPS;         // rows alternate between th
 #define ORL_K1_BWD_TMA_STORE 0
 #endif
 constexpr bool kTmaStore = ORL_K1_BWD_TMA_STORE != 0;
+constexpr int kTmaStoreEvery = ORL_K1_BWD_TMA_STORE > 0 ? ORL_K1_BWD_TMA_STORE : 1;
 #ifndef ORL_K1_STORE_WAIT_NS
 #define ORL_K1_STORE_WAIT_NS 20000  // the store warp parks while the consumers compute a chunk
 #endif
@@ -912,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                     int pend = -1;
                     for (int c = 0; c < nch; ++c) {
                         const int bytes = min(kChunk, (int)row_bytes - c * kChunk);
-                        if (bytes == kChunk && (c % ORL_K1_BWD_TMA_STORE) == 0) {
+                        if (bytes == kChunk && (c % kTmaStoreEvery) == 0) {
                             mbar_wait_hint<ORL_K1_STORE_WAIT_NS>(&S.written[stage], (wph >> stage) & 1u);
                             wph ^= 1u << stage;
                             tma_store_1d(reinterpret_cast<void *>(S.st_dst[stage]), S.stage[stage], kChunk, pol);
@@ -1207,7 +1208,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             const bool own_y = y_ok && ybyte >= off && ybyte < off + bytes && (((ybyte - off) >> 4) % kConsumers) == ct;
             // kTmaStore: a full chunk's results go back into its stage; the store warp bulk-stores
             // the stage and frees it (same rule as the store warp's schedule: aligned rows, full chunk)
-            const bool staged = kTmaStore && !UNAL && bytes == kChunk && ((off / kChunk) % ORL_K1_BWD_TMA_STORE) == 0;
+            const bool staged = kTmaStore && !UNAL && bytes == kChunk && ((off / kChunk) % kTmaStoreEvery) == 0;
             float xy = 0.f;
             if (own_y) {
                 const uint8_t *q = sb + (ybyte - off);

@@ -664,7 +664,11 @@ __device__ __forceinline__ void process_words(ThreadAcc &a, uint32_t (&w)[NW], b
     // fast pass held (no saved copy of the state to restore: fewer moves per chunk)
     ThreadAcc c{a.m, 0ull, 0ull, 0ull, 0ull};
     acc_words<Tin, ENT, POLY, NW>(c, w, c2p);
+#if ORL_K1_ABL & 16  // timing ablation: no overflow check (fast pass always accepted)
+    if (false) {
+#else
     if (needs_redo<ENT>(c)) {
+#endif
         exact_words<Tin, ENT, NW>(a, w, c2, c2p);
     } else {
         a.sA = fadd2(a.sA, c.sA);
@@ -754,7 +758,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
 #define ORL_K1_PREMERGE 1
 #endif
 #ifndef ORL_K1_ABL
-#define ORL_K1_ABL 0  // timing ablations of the fused pass (tools only): 1 fwd math, 2 bwd math, 4 bwd stores, 8 const wait
+#define ORL_K1_ABL 0  // timing ablations (tools only): 1 fwd math, 2 bwd math, 4 bwd stores, 8 const wait, 16 no overflow check, 32 no fp64 row epilogue
 #endif
     // 1: actor passes only; 2: every pass (A/B knob)
     constexpr bool kPremerge = ORL_K1_PREMERGE == 2 || (ORL_K1_PREMERGE == 1 && MODE != kModeLogprob);
@@ -1027,7 +1031,12 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         mbar_arrive(&S.grad_full[rl % kGradRows]);
                     }
                 };
+#if ORL_K1_ABL & 32  // timing ablation: no fp64 row epilogue (the backward's constants still published)
+                if (MODE == kModeLossGrad) publish(EpiOut{st.m, st.s, st.u});
+                else if (st.m == 1234.5f) p.logp[0] = st.s;
+#else
                 row_epilogue<MODE>(p, b, t, L, y, st, target, sv, wh, S.wacc[ew], &eo, publish, &pre);
+#endif
             }
             __syncwarp();
         }

@@ -28,7 +28,10 @@ static_assert(kStatsSlots == ORL_PARTIALS_N && kStatsOut == ORL_STATS_N, "stats 
 
 namespace {
 constexpr int kMaxWorld = 256;
-constexpr int kDefaultPoly = 0;
+#ifndef ORL_K1_POLY
+#define ORL_K1_POLY 0
+#endif
+constexpr int kDefaultPoly = ORL_K1_POLY;  // rejected (DESIGN 5.1); the library's numerics do not depend on the environment
 thread_local std::string g_thread_err;
 }  // namespace
 
@@ -186,10 +189,7 @@ static void fill_common(orl_ctx *ctx, K1Params &p, const orl_rows *rows, const o
     }
     p.inv_temp = inv_temp;
     p.c2 = inv_temp * 1.4426950408889634f;
-    {
-        const char *e = getenv("ORL_K1_POLY");   // tuning knob: 0, 4 or 8
-        p.poly = e ? atoi(e) : kDefaultPoly;
-    }
+    p.poly = kDefaultPoly;  // FMA-pipe exp2 offload: a build-time experiment (-DORL_K1_POLY=8|16), off
     p.B = (int)rows->B;
     p.T = (int)rows->T;
     p.seq_offset = rows->seq_offset;

@@ -640,6 +640,49 @@ def test_next1_logits_grad_parity(ctx, dtype, V, inv_temp):
                 0.01 / float(m.sum()), inv_temp)
 
 
+@pytest.mark.parametrize("fused", [True, False])
+def test_next1_masked_vocab_entries(ctx, fused):
+    """Vocabulary entries masked in the actor logits (Z39): a -inf logit has p = 0 and the
+    formula's p (ln p + H) is 0 * (-inf), so its gradient element is NaN on both sides (GPU
+    and the fp64 oracle); a large finite negative logit (-1e30, the documented mask value)
+    gets an exact zero gradient; every other element stays finite and matches the oracle."""
+    B, T, V = 3, 16, 2176
+    c = dict(synth.CONFIGS["llama8b"], c2=0.01, V=V)
+    g = _gpu_batch(17, B, T, V, "mixed", mode="realistic")
+    x = g["logits_new"]
+    tok = g["tokens"].long()
+    gen = torch.Generator(device="cpu").manual_seed(5)
+    masked = torch.rand(B, T, V, generator=gen) < 0.05
+    kind = torch.rand(B, T, V, generator=gen) < 0.5          # half -inf, half -1e30
+    masked.scatter_(2, tok.cpu().unsqueeze(-1), False)       # never the sampled token
+    neg_inf = (masked & kind).to(DEV)
+    neg_big = (masked & ~kind).to(DEV)
+    x[neg_inf] = float("-inf")
+    x[neg_big] = -1e30
+    cfg = PathConfig.from_synth(c)
+    dl = torch.full((B, T, V), 3.0, dtype=torch.bfloat16, device=DEV)
+    bufs = Buffers(B, T, DEV)
+    src = lambda role, s, e: g[f"logits_{role}"][s:e]  # noqa: E731
+    status, st = run_iteration(ctx, g, cfg, bufs, src, mb=2, grad_sink=lambda s, e: dl[s:e], fused_grad=fused)
+    torch.cuda.synchronize()
+    assert status == "ORL_OK", status
+    npb = synth.batch_to_numpy(g)
+    m = parity.valid_mask(npb["lengths"], T)
+    with np.errstate(invalid="ignore"):
+        o = oracle.logits_grad(npb["logits_new"], npb["tokens"], npb["lengths"], _np(bufs.dlogp).astype(np.float64),
+                               1.0, 0.01, float(m.sum()))
+    gg = dl.float().cpu().numpy()
+    vm = np.broadcast_to(m[..., None], gg.shape)
+    ni, nb = neg_inf.cpu().numpy() & vm, neg_big.cpu().numpy() & vm
+    assert ni.sum() > 0 and nb.sum() > 0
+    assert np.isnan(gg[ni]).all() and np.isnan(o[ni]).all()
+    assert (gg[nb] == 0).all() and (o[nb] == 0).all()
+    rest = vm & ~ni & ~nb
+    assert np.isfinite(gg[rest]).all()
+    err = np.abs(gg[rest] - o[rest])
+    assert (err <= 8e-3 * np.abs(o[rest]) + 1e-6).all(), float(err.max())
+
+
 def _grad_bound(x_rows, tok, lse, H, w, a, inv_temp, o, out_bf16):
     """Derived per-element bound for dL/dx (NEXT-1) of one row, GPU vs the fp64 oracle.
     The GPU evaluates g_v = inv_temp (p_v (a (ln p_v + H) - w) + [v = y] w) in fp32 from

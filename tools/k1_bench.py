@@ -132,8 +132,11 @@ try:  # per-block SM clock / power (NVML, sampled right after each timed block)
 except Exception:  # pragma: no cover
     _clk = None
 res, rclk = {}, {}
+names = list(ctxs)
 for r in range(a.repeat):
-    for name in ctxs:
+    # rotate the build order every repeat: the first build of a cycle runs at a higher clock
+    # under the power cap (measured ~8 %), so a fixed order biases interleaved A/Bs
+    for name in names[r % len(names):] + names[:r % len(names)]:
         for kind in a.kinds.split(","):
             res.setdefault((name, kind), []).append(timed(name, kind))
             if _clk:

@@ -394,19 +394,29 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
         const RowPre pr = pre ? *pre : row_pre(p, L, side, wh);
         const double A = pr.A;
         const double lpo = side[0];
-        // ratio rho = exp(logp - logp_old) (Z38: the fp64 log-prob of this epilogue).  For a
-        // finite row it is evaluated as exp(x_y / T - logp_old - ln2 m) / s, which does not
-        // wait for log2(s): this chain and the lse chain above run side by side, and the
-        // fused backward (which needs lse, H and w) starts sooner.
-        double rho = exp((double)target * (double)p.inv_temp - lpo - kLn2 * (double)tot.m) / (double)tot.s;
-        if (oob || dead || !isfinite(logp)) rho = exp(logp - lpo);
+        // The loss terms use the stored fp32 log-prob lpn (Z38), as every consumer of the
+        // per-token outputs does.  The ratio rho = exp(lpn - logp_old) is evaluated as
+        //   exp(x_y / T - logp_old - ln2 m) / s  *  exp(lpn - logp),
+        // the first factor (= exp(logp - logp_old)) on a chain that does not wait for log2(s),
+        // side by side with the lse chain, the second from |lpn - logp| <= 2^-24 |logp| as
+        // 1 + d + d^2 / 2 (error < d^3 ~ 1e-21): the fused backward (which needs lse, H and w)
+        // starts sooner, and rho matches exp(lpn - logp_old) to fp64 rounding.
+        const double lpn = (double)logp_f;
+        const double rho_x = exp((double)target * (double)p.inv_temp - lpo - kLn2 * (double)tot.m) / (double)tot.s;
+        double rho;
+        if (oob || dead || !isfinite(logp)) {
+            rho = exp(lpn - lpo);
+        } else {
+            const double d = lpn - logp;
+            rho = rho_x * fma(d, fma(d, 0.5, 1.0), 1.0);
+        }
         const double rc = fmin(fmax(rho, 1.0 - p.eps_low), 1.0 + p.eps_high);
         const double unc = rho * A, clt = rc * A;
         const bool clipped = clt < unc;
         const double obj = clipped ? clt : unc;
         double dr = 0.0, dkref = 0.0;
         if (p.logp_ref) {
-            dr = logp - (double)side[1];
+            dr = lpn - (double)side[1];
             dkref = kl_grad(dr, p.kl_loss_est);
         }
         const float wf = (float)(((clipped ? 0.0 : -rho * A) + (p.kl_in_loss ? p.beta_loss * dkref : 0.0)) * pr.invN);
@@ -435,9 +445,9 @@ __device__ void row_epilogue(const K1Params &p, int b, int t, int L, int y, Onli
             }
         }
         const double kref = p.logp_ref ? kl_est(dr, p.kl_loss_est) : 0.0;
-        const double k3old = kl_est(lpo - logp, 3);
+        const double k3old = kl_est(lpo - lpn, 3);
         const double Hd = (double)H_f;
-        const double dold = logp - lpo;
+        const double dold = lpn - lpo;
         wacc[0] += 1.0;
         wacc[1] += obj;
         wacc[2] += vl;

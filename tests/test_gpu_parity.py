@@ -63,23 +63,20 @@ def _isolated_oracle(npb, bufs, ocfg):
     return out, glob
 
 
-def _check_flags(bufs, sh, ocfg, mask, name):
-    """Per-token decisions bit-exact (SURVEY 8(c).4, P:197, P:94): the loss stage of the
-    oracle fed the GPU's own fp32 upstream (logp_new/old/ref, adv, ret, entropy; the
-    whitening moments taken by the oracle over the GPU's fp32 advantages) vs the actor
-    pass's flags output.  bit 0 clipped (Z16), 1 value-clipped (Z13), 2 ratio guard
-    (Z22), 3 non-finite.  Tie bands (excluded and counted): rho within 1e-9 of a clip
-    edge (fp64 exp may differ by an ulp), |A'| < 1e-12, |dold| within 1e-9 of the guard."""
+def _isolated_loss(bufs, sh, ocfg, mask):
+    """The oracle's loss stage fed the GPU's own fp32 upstream (logp_new/old/ref, adv + adv_lo,
+    ret, entropy), whitened with the oracle's moments over the GPU's advantages.  Returns the
+    oracle.ppo_loss result, the whitened advantages and the moments (mu, sd) or None."""
     L = sh["lengths"]
     f64 = lambda t: _np(t).astype(np.float64)  # noqa: E731
     adv = f64(bufs.adv) + f64(bufs.adv_lo)            # the value the actor pass whitens (Z33)
     kind = ocfg["adv_kind"]
     whiten = bool(ocfg["whiten"]) and kind != "grpo"
-    Aw = adv
+    Aw, mom = adv, None
     if whiten:
         mu, sd, warn = oracle.whiten_moments(adv[mask])
         if not warn:
-            Aw = oracle.whiten(adv, L, mu, sd)
+            Aw, mom = oracle.whiten(adv, L, mu, sd), (mu, sd)
     critic = kind == "gae" and sh.get("values_new") is not None
     res = oracle.ppo_loss(L, f64(bufs.logp_new), f64(bufs.logp_old), Aw, logp_ref=f64(bufs.logp_ref),
                           ret=f64(bufs.ret) if critic else None, v_new=sh["values_new"] if critic else None,
@@ -87,6 +84,18 @@ def _check_flags(bufs, sh, ocfg, mask, name):
                           eps_low=ocfg["eps_low"], eps_high=ocfg["eps_high"], eps_v=ocfg["eps_v"],
                           c1=ocfg["c1"] if critic else 0.0, beta_loss=ocfg["beta_loss"], kl_est=ocfg["kl_est_loss"],
                           kl_in_loss=ocfg["kl_mode"] == "loss", ratio_guard=ocfg["ratio_guard"])
+    return res, Aw, mom
+
+
+def _check_flags(bufs, sh, ocfg, mask, name):
+    """Per-token decisions bit-exact (SURVEY 8(c).4, P:197, P:94): the loss stage of the
+    oracle fed the GPU's own fp32 upstream (logp_new/old/ref, adv, ret, entropy; the
+    whitening moments taken by the oracle over the GPU's fp32 advantages) vs the actor
+    pass's flags output.  bit 0 clipped (Z16), 1 value-clipped (Z13), 2 ratio guard
+    (Z22), 3 non-finite.  Tie bands (excluded and counted): rho within 1e-9 of a clip
+    edge (fp64 exp may differ by an ulp), |A'| < 1e-12, |dold| within 1e-9 of the guard."""
+    f64 = lambda t: _np(t).astype(np.float64)  # noqa: E731
+    res, Aw, _ = _isolated_loss(bufs, sh, ocfg, mask)
     g, o = _np(bufs.flags).astype(np.int64), res["flags"].astype(np.int64)
     assert np.all(g[~mask] == 0), f"{name}: flags at masked positions"
     dold = f64(bufs.logp_new) - f64(bufs.logp_old)
@@ -111,9 +120,37 @@ def _check_downstream(bufs, o, glob, st, mask, cfg_name, ppo_tol=parity.REL, raw
     # (orl.h orl_advantages); the oracle shapes R_b - mu_g.  Compare the raw shaping then.
     parity.check_rel("shaped_reward", _np(bufs.shaped), o["shaped_reward"] if raw_shaped is None else raw_shaped,
                      mask)
-    parity.check_rel("adv", _np(bufs.adv), o["adv"], mask)
-    if o.get("ret") is not None:
-        parity.check_rel("ret", _np(bufs.ret), o["ret"], mask)
+    if raw_shaped is None:
+        parity.check_rel("adv", _np(bufs.adv), o["adv"], mask)
+        if o.get("ret") is not None:
+            parity.check_rel("ret", _np(bufs.ret), o["ret"], mask)
+    else:
+        # RPP-baseline, S4' in isolation: the oracle's returns of the GPU's own fp32 shaped
+        # rewards with mu_g subtracted at t = L_b - 1.  (From the log-probs, the oracle shapes
+        # R_b - mu_g - beta k in fp64, while the S3 output the GPU hands to K3 holds the fp32
+        # R_b - beta k: in a group of equal rewards the advantage is the KL shaping alone,
+        # ~1e-6, and that fp32 rounding (<= 2^-24 |R_b|) is its resolution -- Z40.)
+        L, Tn = glob["isolated_input"][0]["lengths"], mask.shape[1]
+        R = glob["isolated_input"][0]["seq_reward"].astype(np.float64)
+        G = glob["isolated_input"][1]["group_size"]
+        mu = R - oracle.group_mean_subtract(R, G)
+        r = _np(bufs.shaped).astype(np.float64)
+        for b_ in range(len(L)):
+            if L[b_] > 0:
+                r[b_, L[b_] - 1] -= mu[b_]
+        a_iso = oracle.discounted_returns(L, r, glob["isolated_input"][1]["gamma"])
+        parity.check_rel("adv", _np(bufs.adv), a_iso, mask)
+        if bufs.ret is not None and o.get("ret") is not None:
+            parity.check_rel("ret", _np(bufs.ret), a_iso, mask)
+        # the loss stage then in isolation too (fed the GPU's advantages)
+        sh_, ocfg_ = glob["isolated_input"]
+        res_, _, mom_ = _isolated_loss(bufs, sh_, ocfg_, mask)
+        o = dict(o, dlogp=res_["dlogp"], obj=res_["obj"], vl=res_["vl"])
+        iso_st = oracle.stats(res_["sums"], c1=0.0, c2=ocfg_["c2"], beta_loss=ocfg_["beta_loss"],
+                              kl_in_loss=ocfg_["kl_mode"] == "loss")
+        glob = dict(glob, stats=iso_st)
+        if mom_ is not None:
+            glob["adv_mean"], glob["adv_std"] = mom_
     parity.check_rel("dloss_dlogp", _np(bufs.dlogp), o["dlogp"], mask)
     if bufs.dv is not None:
         parity.check_rel("dloss_dv", _np(bufs.dv), o["dv"], mask)

@@ -8,6 +8,8 @@ downstream stage stage-isolated at the 1e-5 relative bar (test_gpu_parity helper
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -46,7 +48,7 @@ def _case(i):
     return dict(V=V, kind=kind, G=G, B=B, T=T, L=L.astype(np.int32), dtype=dtype, pad=pad, inv_temp=inv_temp, mb=mb)
 
 
-@pytest.mark.parametrize("i", range(26))
+@pytest.mark.parametrize("i", range(int(os.environ.get("ORL_SHAPE_SWEEP", "26"))))  # extended runs: ORL_SHAPE_SWEEP=N
 def test_random_shapes_end_to_end(i):
     from tests.test_gpu_parity import _check_downstream, _isolated_oracle, _np
     cs = _case(i)

@@ -362,10 +362,11 @@ orl_status orl_ppo_loss(orl_ctx *ctx, const orl_rows *rows, const orl_logits *ac
  * and must not alias any logits still being read.  zero_masked = 1 also
  * writes zeros into the rows with t >= L_b.  Outputs are rounded to the
  * logits dtype (bf16: round-to-nearest-even).  A -inf logit (allowed in the
- * forward passes) has p_v = 0 and its gradient element is NaN, as the formula's
- * p_v ln p_v = 0 * (-inf) is in the fp64 oracle (DESIGN Z39); mask vocabulary
+ * forward passes) has p_v = 0; with cfg->c2 != 0 its gradient element is NaN, as
+ * the entropy term's p_v ln p_v = 0 * (-inf) is in the fp64 oracle, with
+ * cfg->c2 = 0 (no entropy term) it is exactly 0 (DESIGN Z39); mask vocabulary
  * entries with a large finite negative logit (e.g. -1e30, which keeps
- * x * inv_temp * log2(e) finite in fp32) for an exact zero gradient. */
+ * x * inv_temp * log2(e) finite in fp32) for an exact zero gradient either way. */
 orl_status orl_logits_grad(orl_ctx *ctx, const orl_rows *rows, const orl_logits *actor,
                            float inv_temp, const orl_ppo_cfg *cfg, const float *lse,
                            const float *entropy, const float *dloss_dlogp, void *dlogits,

@@ -481,8 +481,10 @@ int oracle_stats(const double *sums, double c1, double c2, double beta_loss,
  *       dL/dz_v = w (delta_vy - p_v) + a p_v (ln p_v + H),   a = c2/N
  *       dL/dx_v = inv_temp dL/dz_v
  *     w = dL/dlogp_new (the per-token derivative of oracle_ppo_loss).  The
- *     entropy part is the derivative of -c2 mean(H); the policy and KL-loss
- *     parts reach the logits only through logp_new = z_y - lse.
+ *     entropy part is the derivative of -c2 mean(H), present only when the
+ *     loss has that term (a != 0: with c2 = 0 a -inf logit, p_v = 0, gets
+ *     the gradient -w p_v = 0, not 0 * (-inf); DESIGN Z39); the policy and
+ *     KL-loss parts reach the logits only through logp_new = z_y - lse.
  * ---------------------------------------------------------------------- */
 void oracle_logits_grad_row(const double *x, int64_t V, int64_t y, double inv_temp, double w,
                             double a, double *grad)
@@ -494,7 +496,8 @@ void oracle_logits_grad_row(const double *x, int64_t V, int64_t y, double inv_te
     for (int64_t v = 0; v < V; ++v) {
         double lp = z[v] - lse;
         double p = exp(lp);
-        double dz = w * ((v == y ? 1.0 : 0.0) - p) + a * p * (lp + H);
+        double dz = w * ((v == y ? 1.0 : 0.0) - p);
+        if (a != 0.0) dz += a * p * (lp + H);  /* c2 = 0: no entropy term in the loss (Z39) */
         grad[v] = inv_temp * dz;
     }
     free(z);

@@ -757,7 +757,10 @@ __device__ void finish_partials_warp(const K1Params &p, const double (&wacc)[kNu
 }
 
 // ---------------------------------------------------------------- TMA kernel
-template <typename Tin, int MODE, int POLY, bool UNAL = false>
+// GENT (fused actor pass only): the loss has an entropy term (c2 != 0), so the backward's
+// factor is A1 t + A0; with c2 = 0 it is the row constant A0 (one FFMA2 per pair less, and
+// a -inf logit gets the exact zero gradient -w p = 0 instead of 0 * (-inf); DESIGN Z39).
+template <typename Tin, int MODE, int POLY, bool UNAL = false, bool GENT = true>
 __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(const K1Params p) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     K1Smem &S = *reinterpret_cast<K1Smem *>(smem_raw);
@@ -1201,7 +1204,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
             if (idx >= 0) {
                 const float t2 = fmaf(S.row_x[rb % kRowInfo][ct], p.c2, -g.l2);
-                float gv = __fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0));  // no contraction: same bits on every path
+                float gv = __fmul_rn(ex2(t2), GENT ? fmaf(g.A1, t2, g.A0) : g.A0);  // no contraction: same bits on every path
                 if (idx == g.y) gv = __fadd_rn(gv, g.wt);
                 if (sizeof(Tin) == 2) {
                     const uint32_t hb = f32x2_to_bf16x2_rn(gv, 0.f) & 0xffffu;
@@ -1258,7 +1261,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         const uint64_t t2 = ffma2(bf16x2_to_f32x2(w4[q]), c2p, nl2);
                         float t0, t1;
                         unpack2(t2, t0, t1);
-                        const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
+                        const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), GENT ? ffma2(A1p, t2, A0p) : A0p);
                         float g0, g1;
                         unpack2(gr, g0, g1);
                         o[q] = f32x2_to_bf16x2_rn(g0, g1);
@@ -1271,7 +1274,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                         const uint64_t t2 = ffma2(x, c2p, nl2);
                         float t0, t1;
                         unpack2(t2, t0, t1);
-                        const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), ffma2(A1p, t2, A0p));
+                        const uint64_t gr = fmul2(pack2(ex2(t0), ex2(t1)), GENT ? ffma2(A1p, t2, A0p) : A0p);
                         float g0, g1;
                         unpack2(gr, g0, g1);
                         o[2 * q] = __float_as_uint(g0);
@@ -1304,7 +1307,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
                 }
                 if (own_y) {  // the target element with the delta term, after its vector (program order)
                     const float t2 = fmaf(xy, p.c2, -g.l2);
-                    const float gy = __fadd_rn(__fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0)), g.wt);
+                    const float gy = __fadd_rn(__fmul_rn(ex2(t2), GENT ? fmaf(g.A1, t2, g.A0) : g.A0), g.wt);
                     if (sizeof(Tin) == 2)
                         *reinterpret_cast<uint16_t *>(wb + (ybyte - off)) = (uint16_t)(f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu);
                     else
@@ -1336,7 +1339,7 @@ __global__ void __launch_bounds__(kThreads, ORL_K1_MINBLOCKS) k1_tma_kernel(cons
             }
             if (own_y) {  // program-ordered rewrite of the target element with the delta term
                 const float t2 = fmaf(xy, p.c2, -g.l2);
-                const float gy = __fadd_rn(__fmul_rn(ex2(t2), fmaf(g.A1, t2, g.A0)), g.wt);  // p (A1 t + A0) + wt, not contracted
+                const float gy = __fadd_rn(__fmul_rn(ex2(t2), GENT ? fmaf(g.A1, t2, g.A0) : g.A0), g.wt);  // p (A1 t + A0) + wt, not contracted
                 if (sizeof(Tin) == 2) {
                     const uint32_t hb = f32x2_to_bf16x2_rn(gy, 0.f) & 0xffffu;
                     asm volatile("st.global.u16 [%0], %1;" ::"l"(orow + g.y), "h"((unsigned short)hb) : "memory");
@@ -1553,8 +1556,13 @@ template <typename Tin, int MODE, int POLY>
 static cudaError_t launch_tma(const K1Params &p, int num_sms, cudaStream_t s) {
     const int64_t N_upper = (int64_t)p.B * p.T;  // rows are counted on device; size by the bound
     const size_t smem = k1_tma_smem_bytes(p.B);
-    // unaligned rows: a separate instantiation, so the aligned path carries none of it
-    auto kern = (POLY == 0 && p.unaligned) ? k1_tma_kernel<Tin, MODE, 0, true> : k1_tma_kernel<Tin, MODE, POLY, false>;
+    // unaligned rows: a separate instantiation, so the aligned path carries none of it; the fused
+    // pass without an entropy term (c2 = 0) likewise
+    const bool gent = MODE != kModeLossGrad || p.c2_ent != 0.0;
+    auto kern = (POLY == 0 && p.unaligned) ? (gent ? k1_tma_kernel<Tin, MODE, 0, true, true>
+                                                   : k1_tma_kernel<Tin, MODE, 0, true, MODE != kModeLossGrad>)
+                                           : (gent ? k1_tma_kernel<Tin, MODE, POLY, false, true>
+                                                   : k1_tma_kernel<Tin, MODE, POLY, false, MODE != kModeLossGrad>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;

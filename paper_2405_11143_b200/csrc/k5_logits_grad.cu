@@ -139,7 +139,10 @@ __device__ __forceinline__ k5::RowInfo row_info(const K5Params &p, int64_t gi, i
     return r;
 }
 
-template <typename Tin, bool UNAL = false>
+// GENT: the loss has an entropy term (c2 != 0): factor A1 t + A0; with c2 = 0 the row constant
+// A0 (one FFMA2 per pair less; a -inf logit gets the exact zero gradient, DESIGN Z39).  The
+// fused actor pass (K1, kModeLossGrad) makes the same choice, so both paths give the same bits.
+template <typename Tin, bool UNAL = false, bool GENT = true>
 __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params p) {
     using namespace k5;
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                     else if (ct < head_e + tail_e) idx = (int)p.V - tail_e + (ct - head_e);
                     if (idx >= 0) {
                         const float t2 = fmaf(ri.hx[ct], p.c2x, -ri.l2);
-                        float g = __fmul_rn(ex2(t2), fmaf(ri.A1, t2, ri.A0));  // no contraction: same bits on every path
+                        float g = __fmul_rn(ex2(t2), GENT ? fmaf(ri.A1, t2, ri.A0) : ri.A0);  // no contraction: same bits on every path
                         if (idx == ri.y) g = __fadd_rn(g, ri.wt);
                         st_elem<Tin>(orow, idx, g);
                     }
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                         float t0, t1;
                         unpack2(t2, t0, t1);
                         const uint64_t pr = pack2(ex2(t0), ex2(t1));     // p
-                        const uint64_t g = fmul2(pr, ffma2(A1p, t2, A0p));
+                        const uint64_t g = fmul2(pr, GENT ? ffma2(A1p, t2, A0p) : A0p);
                         float g0, g1;
                         unpack2(g, g0, g1);
                         o[q] = f32x2_to_bf16x2(g0, g1);
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                         float t0, t1;
                         unpack2(t2, t0, t1);
                         const uint64_t pr = pack2(ex2(t0), ex2(t1));
-                        const uint64_t g = fmul2(pr, ffma2(A1p, t2, A0p));
+                        const uint64_t g = fmul2(pr, GENT ? ffma2(A1p, t2, A0p) : A0p);
                         float g0, g1;
                         unpack2(g, g0, g1);
                         o[2 * q] = __float_as_uint(g0);
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
             // delta term at v = y: the owner of y's vector rewrites that element
             if (own_y) {
                 const float t2 = fmaf(xy, p.c2x, -ri.l2);
-                const float g = __fadd_rn(__fmul_rn(ex2(t2), fmaf(ri.A1, t2, ri.A0)), ri.wt);  // not contracted
+                const float g = __fadd_rn(__fmul_rn(ex2(t2), GENT ? fmaf(ri.A1, t2, ri.A0) : ri.A0), ri.wt);  // not contracted
                 st_elem<Tin>(orow, ri.y, g);
             }
         }
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
 }
 
 // Generic path (unaligned rows): one row per CTA iteration, scalar accesses.
-template <typename Tin>
+template <typename Tin, bool GENT = true>
 __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     int32_t *cum_s = reinterpret_cast<int32_t *>(smem_raw);
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(256) k5_generic_kernel(const K5Params p) {
             if (sizeof(Tin) == 2) x = __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t *>(row)[v]) << 16);
             else x = reinterpret_cast<const float *>(row)[v];
             const float t2 = fmaf(x, p.c2x, -ri.l2);
-            float g = __fmul_rn(ex2(t2), fmaf(ri.A1, t2, ri.A0));  // no contraction: same bits on every path
+            float g = __fmul_rn(ex2(t2), GENT ? fmaf(ri.A1, t2, ri.A0) : ri.A0);  // no contraction: same bits on every path
             if (v == ri.y) g = __fadd_rn(g, ri.wt);
             if (sizeof(Tin) == 2) {
                 const uint32_t hb = f32x2_to_bf16x2(g, 0.f) & 0xffffu;
@@ -379,7 +382,9 @@ static cudaError_t launch_k5_typed(const K5Params &p, bool tma, int num_sms, cud
     cfg.stream = s;
     if (tma) {
         const size_t smem = k5_smem_bytes(p.B);
-        auto kern = p.unaligned ? k5_tma_kernel<Tin, true> : k5_tma_kernel<Tin, false>;
+        const bool gent = p.c2 != 0.0;
+        auto kern = p.unaligned ? (gent ? k5_tma_kernel<Tin, true, true> : k5_tma_kernel<Tin, true, false>)
+                                : (gent ? k5_tma_kernel<Tin, false, true> : k5_tma_kernel<Tin, false, false>);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int64_t grid = num_sms;
@@ -390,14 +395,15 @@ static cudaError_t launch_k5_typed(const K5Params &p, bool tma, int num_sms, cud
         return cudaLaunchKernelEx(&cfg, kern, p);
     }
     const size_t smem = sizeof(int32_t) * (size_t)((p.cum_global ? 0 : p.B) + 32);
-    cudaError_t e = cudaFuncSetAttribute(k5_generic_kernel<Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto gkern = p.c2 != 0.0 ? k5_generic_kernel<Tin, true> : k5_generic_kernel<Tin, false>;
+    cudaError_t e = cudaFuncSetAttribute(gkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int64_t grid = (int64_t)num_sms * 4;
     if (grid > rows) grid = rows;
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem;
-    return cudaLaunchKernelEx(&cfg, k5_generic_kernel<Tin>, p);
+    return cudaLaunchKernelEx(&cfg, gkern, p);
 }
 
 cudaError_t launch_k5(const K5Params &p, bool tma, int num_sms, cudaStream_t s) {

@@ -677,14 +677,16 @@ def test_next1_logits_grad_parity(ctx, dtype, V, inv_temp):
                 0.01 / float(m.sum()), inv_temp)
 
 
+@pytest.mark.parametrize("c2", [0.01, 0.0])
 @pytest.mark.parametrize("fused", [True, False])
-def test_next1_masked_vocab_entries(ctx, fused):
-    """Vocabulary entries masked in the actor logits (Z39): a -inf logit has p = 0 and the
-    formula's p (ln p + H) is 0 * (-inf), so its gradient element is NaN on both sides (GPU
-    and the fp64 oracle); a large finite negative logit (-1e30, the documented mask value)
-    gets an exact zero gradient; every other element stays finite and matches the oracle."""
+def test_next1_masked_vocab_entries(ctx, fused, c2):
+    """Vocabulary entries masked in the actor logits (Z39): a -inf logit has p = 0; with an
+    entropy term (c2 != 0) the formula's p (ln p + H) is 0 * (-inf), so its gradient element
+    is NaN on both sides (GPU and the fp64 oracle), without one (c2 = 0) it is -w p = 0 on
+    both sides; a large finite negative logit (-1e30, the documented mask value) gets an
+    exact zero gradient; every other element stays finite and matches the oracle."""
     B, T, V = 3, 16, 2176
-    c = dict(synth.CONFIGS["llama8b"], c2=0.01, V=V)
+    c = dict(synth.CONFIGS["llama8b"], c2=c2, V=V)
     g = _gpu_batch(17, B, T, V, "mixed", mode="realistic")
     x = g["logits_new"]
     tok = g["tokens"].long()
@@ -707,12 +709,15 @@ def test_next1_masked_vocab_entries(ctx, fused):
     m = parity.valid_mask(npb["lengths"], T)
     with np.errstate(invalid="ignore"):
         o = oracle.logits_grad(npb["logits_new"], npb["tokens"], npb["lengths"], _np(bufs.dlogp).astype(np.float64),
-                               1.0, 0.01, float(m.sum()))
+                               1.0, c2, float(m.sum()))
     gg = dl.float().cpu().numpy()
     vm = np.broadcast_to(m[..., None], gg.shape)
     ni, nb = neg_inf.cpu().numpy() & vm, neg_big.cpu().numpy() & vm
     assert ni.sum() > 0 and nb.sum() > 0
-    assert np.isnan(gg[ni]).all() and np.isnan(o[ni]).all()
+    if c2 != 0.0:
+        assert np.isnan(gg[ni]).all() and np.isnan(o[ni]).all()
+    else:
+        assert (gg[ni] == 0).all() and (o[ni] == 0).all()
     assert (gg[nb] == 0).all() and (o[nb] == 0).all()
     rest = vm & ~ni & ~nb
     assert np.isfinite(gg[rest]).all()

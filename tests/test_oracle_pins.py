@@ -519,6 +519,36 @@ def test_next1_logits_grad_finite_differences(k):
             assert abs(g[b, t].sum()) < 1e-13
 
 
+@pytest.mark.parametrize("c2", [0.0, 0.05])
+def test_next1_masked_entries_equal_reduced_vocabulary(c2):
+    """Z39: a -inf logit leaves the softmax as if its entry did not exist, so on the finite
+    entries the gradient equals that of the row with the entry removed (a plain
+    re-evaluation on the reduced vocabulary).  At the -inf entry itself p = 0: with c2 = 0
+    the loss has no entropy term and the gradient is -w p = 0 exactly; with c2 != 0 the
+    formula's p (ln p + H) is 0 * (-inf) = NaN."""
+    V, y, inv_temp, w, n = 9, 4, 1.3, -0.7, 5.0
+    x = rng.normal(0, 2.0, V)
+    masked = np.array([1, 6])
+    xm = x.copy()
+    xm[masked] = -np.inf
+    with np.errstate(invalid="ignore"):
+        g = oracle.logits_grad(xm.reshape(1, 1, V), np.array([[y]], np.int32), np.array([1], np.int32),
+                               np.array([[w]]), inv_temp, c2, n)[0, 0]
+    keep = np.setdiff1d(np.arange(V), masked)
+    gr = oracle.logits_grad(x[keep].reshape(1, 1, -1), np.array([[int(np.searchsorted(keep, y))]], np.int32),
+                            np.array([1], np.int32), np.array([[w]]), inv_temp, c2, n)[0, 0]
+    assert np.allclose(g[keep], gr, rtol=1e-14, atol=1e-16)
+    if c2 == 0.0:
+        assert (g[masked] == 0.0).all()
+        # and the plain definition: inv_temp w (delta_vy - p_v)
+        z = inv_temp * x[keep]
+        p = np.exp(z - z.max()) / np.exp(z - z.max()).sum()
+        ref = inv_temp * w * ((keep == y).astype(float) - p)
+        assert np.allclose(g[keep], ref, rtol=1e-13, atol=1e-16)
+    else:
+        assert np.isnan(g[masked]).all()
+
+
 # ----------------------------------------------------------------------------- NEXT-3
 def test_next3_kl_controller_spec_examples(golden):
     for c in golden("spec_examples.json")["kl_controller"]:

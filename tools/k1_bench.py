@@ -29,6 +29,7 @@ ap.add_argument("--kinds", default="logp,logp+H,loss,sum,copy")
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--warm-seconds", type=float, default=0.0)
 ap.add_argument("--libs", default="")
+ap.add_argument("--c2", type=float, default=0.01, help="entropy coefficient of the loss (0: no entropy term)")
 ap.add_argument("--l2-persist-mb", type=float, default=-1.0,
                 help="experiment: cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize) before the run")
 a = ap.parse_args()
@@ -78,7 +79,7 @@ for name, orl in mods:
     orl.orl_begin_iteration(ctx)
     orl.orl_advantages(ctx, L, adv, kind="rpp", shaped_reward=z())
     orl.orl_whiten_stats(ctx, True)
-    cfg = orl.PPOConfig(c2=0.01)
+    cfg = orl.PPOConfig(c2=a.c2)
     orl.orl_ppo_loss(ctx, tok, L, x[: a.mb], cfg, lo, adv, lpn, entropy=ent, lse=lse, dloss_dlogp=dl)
     ctxs[name] = (orl, ctx, cfg)
 

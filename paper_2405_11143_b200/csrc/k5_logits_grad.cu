@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&S.full[s], 1);
-            mbar_init(&S.empty[s], kConsumerWarps);
+            mbar_init(&S.empty[s], kConsumers);  // every consumer thread releases its own loads
         }
         fence_mbar_init();
     }
@@ -263,16 +263,12 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                 const int vi = ct + k * kConsumers;
                 if (vi < nvec) v[k] = lds128(sb + vi * 16);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[stage]);
+            mbar_arrive(&S.empty[stage]);  // release: this thread's loads of the stage happen before
             if (++stage == kStages) { stage = 0; phase ^= 1u; }
             char *obase = reinterpret_cast<char *>(orow) + (UNAL ? ri.h : 0) + off;
-#pragma unroll
-            for (int k = 0; k < kVPT; ++k) {
-                const int vi = ct + k * kConsumers;
-                if (vi >= nvec) continue;
-                const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                uint32_t o[4];
+            // dL/dx of one 16-byte vector (the same per-element operations as the fused pass)
+            auto grad_vec = [&](const uint4 &vv, uint32_t (&o)[4]) {
+                const uint32_t w4[4] = {vv.x, vv.y, vv.z, vv.w};
                 if (sizeof(Tin) == 2) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -302,7 +298,25 @@ __global__ void __launch_bounds__(k5::kThreads, 1) k5_tma_kernel(const K5Params 
                         o[2 * q + 1] = __float_as_uint(g1);
                     }
                 }
-                stg128(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+            };
+            if (nvec == kVPT * kConsumers) {
+                // full chunk: every thread owns kVPT vectors -- one straight-line block (no
+                // per-vector branches), so the vectors' MUFU / FMA chains interleave
+                uint32_t o[kVPT][4];
+#pragma unroll
+                for (int k = 0; k < kVPT; ++k) grad_vec(v[k], o[k]);
+#pragma unroll
+                for (int k = 0; k < kVPT; ++k)
+                    stg128(obase + (ct + k * kConsumers) * 16, make_uint4(o[k][0], o[k][1], o[k][2], o[k][3]));
+            } else {
+#pragma unroll
+                for (int k = 0; k < kVPT; ++k) {
+                    const int vi = ct + k * kConsumers;
+                    if (vi >= nvec) continue;
+                    uint32_t o[4];
+                    grad_vec(v[k], o);
+                    stg128(obase + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+                }
             }
             // delta term at v = y: the owner of y's vector rewrites that element
             if (own_y) {

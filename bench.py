@@ -96,6 +96,10 @@ def _workload_desc(name, c, W):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi samples (every 50 ms) of SM clock, power and throttle reasons, kept for
+    the timed region only.  start() returns once the first sample has arrived (nvidia-smi
+    takes ~1 s to start), so even a sub-second timed region is covered; call it before the
+    ranks' barrier so the wait does not skew the ranks' start."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -103,28 +107,52 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.lines = []
+        self.t0 = self.t1 = None
 
-    def start(self):
+    def start(self, wait_s: float = 10.0):
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.perf_counter(), line))
+                first.set()
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        first.wait(wait_s)
         return self
+
+    def begin(self):
+        self.t0 = time.perf_counter()
+
+    def end(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
             return None
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-            out, _ = self.proc.communicate()
+        self.thread.join(timeout=5)
+        t0 = self.t0 if self.t0 is not None else -1e300
+        t1 = (self.t1 if self.t1 is not None else 1e300) + 0.06   # a sample in flight at the end
+        inside = [ln for t, ln in self.lines if t0 <= t <= t1]
         sm, mx, reasons, pw = [], None, set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in out.strip().splitlines():
+        for line in inside:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -334,10 +362,11 @@ def timed_steps(ctx, W, env, steps, warmup, pdl_chain=True):
     for _ in range(warmup):
         status, st = step(False)
     torch.cuda.synchronize()
+    clocks = ClockSampler(env["local"]).start()   # before the barrier: its start-up wait is not timed
     if env["dist_mode"]:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(env["local"]).start()
+    clocks.begin()
     l0 = ctx.launch_count
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     evs[0].record(stream)
@@ -345,6 +374,7 @@ def timed_steps(ctx, W, env, steps, warmup, pdl_chain=True):
         status, st = step(True)
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
+    clocks.end()
     if env["dist_mode"]:
         dist.barrier()
     torch.cuda.synchronize()

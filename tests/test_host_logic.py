@@ -62,3 +62,35 @@ def test_bench_reference_arm_on_cpu():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "tokens/s" and d["dtype"] == "f64"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_clock_sampler_keeps_only_the_timed_region(tmp_path, monkeypatch):
+    """bench.py's nvidia-smi sampler (CPU, with a stand-in nvidia-smi that starts slowly and
+    then prints one sample every 50 ms): start() returns once sampling runs, and only
+    samples between begin() and end() are reported -- a short timed region still gets some."""
+    import os
+    import sys
+    import time
+
+    fake = tmp_path / "nvidia-smi"
+    fake.write_text("#!/bin/bash\nsleep 0.5\ni=0\nwhile true; do i=$((i+1));\n"
+                    "  if [ -f " + str(tmp_path / "hot") + " ]; then c=1500; r=Active; else c=1965; r='Not Active'; fi\n"
+                    "  echo \"0, $c, 1965, 900.0, 0x0, Not Active, Not Active, Not Active, $r\"; sleep 0.05; done\n")
+    fake.chmod(0o755)
+    monkeypatch.setenv("PATH", f"{tmp_path}{os.pathsep}{os.environ['PATH']}")
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    c = bench.ClockSampler(0).start()
+    assert c.lines, "start() must wait for the first sample"
+    time.sleep(0.3)                                  # samples before the timed region: 1965 MHz
+    (tmp_path / "hot").write_text("")
+    time.sleep(0.12)
+    c.begin()
+    time.sleep(0.25)                                 # the timed region: 1500 MHz, sw_power_cap
+    c.end()
+    (tmp_path / "hot").unlink()
+    time.sleep(0.3)
+    r = c.stop()
+    assert r is not None and r["samples"] >= 3
+    assert r["sm_mhz"] == 1500.0 and r["reasons"] == ["sw_power_cap"] and r["sm_max_mhz"] == 1965.0

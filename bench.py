@@ -239,7 +239,7 @@ def run_reference(args):
               f"({toks} tokens, 3 x {toks} vocab rows of V={V}), per step")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: T={T} V={V} {c['dtype']} logits, adv={c['adv_kind']} "
                                    "(oracle sample on the host cores)",
                        "global_batch": n_seq, "seq_len": T, "parallelism": "host threads"},

@@ -73,6 +73,10 @@ MUTATIONS = [
      "keep[g] = (mx - mn > 1e-12) ? 1 : 0;"),
     ("C: ratio guard not counted", "oracle/orl_oracle.c", "if (guard) sums[9] += 1.0;", ""),
     ("C: decision flag bits swapped", "oracle/orl_oracle.c", "(uint8_t)(clipped | (vclipped << 1)", "(uint8_t)(vclipped | (clipped << 1)"),
+    ("C: entropy term kept at c2 = 0 (Z39)", "oracle/orl_oracle.c", "if (a != 0.0) dz += a * p * (lp + H);",
+     "dz += a * p * (lp + H);"),
+    ("C: logits-gradient entropy term sign", "oracle/orl_oracle.c", "if (a != 0.0) dz += a * p * (lp + H);",
+     "if (a != 0.0) dz -= a * p * (lp + H);"),
 ]
 
 SUITES = ["tests/test_oracle_pins.py", "tests/test_oracle_pipeline_pins.py", "tests/test_oracle_properties.py"]

@@ -97,10 +97,11 @@ def _workload_desc(name, c, W):
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi samples (every 50 ms) of SM clock, power and throttle reasons, kept for
-    the timed region only.  start() returns once the first sample has arrived (nvidia-smi
-    takes ~1 s to start), so even a sub-second timed region is covered; call it before the
-    ranks' barrier so the wait does not skew the ranks' start."""
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    the timed region only, by nvidia-smi's own sample timestamps (a reader thread may see a
+    line late).  start() returns once the first sample has arrived (nvidia-smi takes ~1 s to
+    start); call it before the ranks' barrier so the wait does not skew the ranks' start.
+    A region shorter than the sampling interval reports the first sample after its start."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -124,7 +125,7 @@ class ClockSampler:
 
         def reader():
             for line in self.proc.stdout:
-                self.lines.append((time.perf_counter(), line))
+                self.lines.append((time.time(), line))
                 first.set()
 
         self.thread = threading.Thread(target=reader, daemon=True)
@@ -133,42 +134,56 @@ class ClockSampler:
         return self
 
     def begin(self):
-        self.t0 = time.perf_counter()
+        self.t0 = time.time()
 
     def end(self):
-        self.t1 = time.perf_counter()
+        self.t1 = time.time()
+
+    @staticmethod
+    def _stamp(field, t_read):
+        import datetime
+        try:
+            return datetime.datetime.strptime(field.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return t_read
 
     def stop(self):
         if self.proc is None:
             return None
+        # a region shorter than the sampling interval: let the first sample after its start arrive
+        deadline = time.time() + 1.0
+        t0 = self.t0 if self.t0 is not None else -1e300
+        while time.time() < deadline and not (
+                self.lines and self._stamp(self.lines[-1][1].split(",")[0], self.lines[-1][0]) >= t0):
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
         self.thread.join(timeout=5)
-        t0 = self.t0 if self.t0 is not None else -1e300
-        t1 = (self.t1 if self.t1 is not None else 1e300) + 0.06   # a sample in flight at the end
-        inside = [ln for t, ln in self.lines if t0 <= t <= t1]
-        sm, mx, reasons, pw = [], None, set(), []
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in inside:
+        rows = []
+        for t_read, line in self.lines:
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-                pw.append(float(f[3]))
+                rows.append((self._stamp(f[0], t_read), float(f[2]), float(f[3]), float(f[4]), f[6:10]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+        t0 = self.t0 if self.t0 is not None else -1e300
+        t1 = self.t1 if self.t1 is not None else 1e300
+        inside = [r for r in rows if t0 <= r[0] <= t1]
+        if not inside:                     # shorter than the sampling interval: the next sample
+            after = [r for r in rows if t0 <= r[0] <= t1 + 0.5]
+            inside = after[:1]
+        if not inside:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm), "power_w_median": statistics.median(pw) if pw else None}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = {n for r in inside for n, v in zip(names, r[4]) if v.lower() == "active"}
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": inside[-1][2],
+                "reasons": sorted(reasons), "samples": len(inside),
+                "power_w_median": statistics.median(r[3] for r in inside)}
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) leg

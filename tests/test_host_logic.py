@@ -75,7 +75,8 @@ def test_clock_sampler_keeps_only_the_timed_region(tmp_path, monkeypatch):
     fake = tmp_path / "nvidia-smi"
     fake.write_text("#!/bin/bash\nsleep 0.5\ni=0\nwhile true; do i=$((i+1));\n"
                     "  if [ -f " + str(tmp_path / "hot") + " ]; then c=1500; r=Active; else c=1965; r='Not Active'; fi\n"
-                    "  echo \"0, $c, 1965, 900.0, 0x0, Not Active, Not Active, Not Active, $r\"; sleep 0.05; done\n")
+                    "  echo \"$(date +'%Y/%m/%d %H:%M:%S.%3N'), 0, $c, 1965, 900.0, 0x0, Not Active, Not Active, "
+                    "Not Active, $r\"; sleep 0.05; done\n")
     fake.chmod(0o755)
     monkeypatch.setenv("PATH", f"{tmp_path}{os.pathsep}{os.environ['PATH']}")
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -94,3 +95,9 @@ def test_clock_sampler_keeps_only_the_timed_region(tmp_path, monkeypatch):
     r = c.stop()
     assert r is not None and r["samples"] >= 3
     assert r["sm_mhz"] == 1500.0 and r["reasons"] == ["sw_power_cap"] and r["sm_max_mhz"] == 1965.0
+    # a region shorter than the sampling interval reports the next sample
+    c = bench.ClockSampler(0).start()
+    c.begin()
+    c.end()
+    r = c.stop()                                     # waits for the sample after begin()
+    assert r is not None and r["samples"] == 1

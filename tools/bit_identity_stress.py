@@ -25,7 +25,8 @@ for it in range(iters):
     B = int(rng.integers(1, 5)) * G
     T = int(rng.choice([16, 64, 200]))
     mb = int(rng.integers(1, B + 1))
-    c = dict(synth.CONFIGS["llama8b"], V=V, adv_kind=kind, group_size=G, c2=0.01)
+    c2 = float(rng.choice([0.0, 0.01]))  # c2 = 0: the backward instantiations without the entropy term
+    c = dict(synth.CONFIGS["llama8b"], V=V, adv_kind=kind, group_size=G, c2=c2)
     if kind == "grpo":
         c.update(kl_mode="loss", beta_loss=0.01, whiten=False, eps_v=0.0, c1=0.0)
     cfg = PathConfig.from_synth(c)

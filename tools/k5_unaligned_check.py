@@ -30,7 +30,7 @@ for it in range(iters):
         adv = z()
         orl.orl_advantages(ctx, L, adv, kind="rpp", shaped_reward=z())
         orl.orl_whiten_stats(ctx, False)
-        cfg = orl.PPOConfig(c2=0.01)
+        cfg = orl.PPOConfig(c2=0.01 if it % 2 else 0.0)  # both backward instantiations
         outs = {}
         for mode in ("tma", "generic", "tma2"):
             if mode == "generic":

@@ -734,7 +734,7 @@ def run_next1(args, ctx, W):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    reps = max(3, args.leg_steps // 2)
+    reps = max(10, args.leg_steps)       # each rep = every micro-batch of the actor logits (~12 ms)
     prev = ctx.pdl_chain
     ctx.pdl_chain = True
     ms = timed(once)
